@@ -1,0 +1,498 @@
+/*
+ * ORACLE -- test infrastructure, NOT part of the product path.
+ *
+ * A plain, slow, single-purpose CPU implementation of the Tier-2/Tier-3 hot
+ * path of arXiv 1910.07776 ("A Tool for Automatically Suggesting Source-Code
+ * Optimizations for Complex GPU Kernels"), written from PAPER.md (cited P:n)
+ * and the readings fixed in DESIGN.md §3 (SPEC.md S:n).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code, header,
+ * table or constant generator with paper_1910_07776_b200/ (the CUDA path).
+ *
+ * Precision policy (reading R20): inputs, rates, labels, min-max
+ * scaled features and every comparison are IEEE FP64, exactly as defined;
+ * the least-squares solve and the prediction are carried out in __float128
+ * (quad) and rounded once to FP64, so that the oracle's own error (~1e-23
+ * relative even at kappa ~ 1e11) is far below the 1e-9 parity tolerance.
+ *
+ * Structure (each step in the paper's order, no fusion or reordering):
+ *   or_rates          Tier 1: features / cycles
+ *   membership        train/test slots of a split                    (Table 2)
+ *   pairs             before/after pairs per optimization
+ *   or_scale          per-fit min-max scaling                         (reading D3)
+ *   or_fit_predict    ridge least squares + prediction                (reading D1)
+ *   or_rank           sort, threshold, truncate
+ *   score             sign accuracy, AC/EX, recommendation hits
+ */
+#include <math.h>
+#include <pthread.h>
+#include <quadmath.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef __float128 quad;
+
+/* ------------------------------------------------------------------ */
+/* Plain data passed in from Python (oracle-private layout).            */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  int32_t P, I, R, m, C, O;        /* programs, inputs, runs, opt bits, counters, opt ids */
+  const double* counters;          /* [N][C], slot t = ((p*I+i)*R+r)*2^m + v */
+  const double* cycles;            /* [N] */
+  const double* runtime_ms;        /* [N] */
+  const int8_t* opt_bit;           /* [P][O], -1 = optimization absent in program */
+} or_dataset;
+
+typedef struct {
+  int32_t kind;                    /* 0 groups, 1 leave-one-out, 2 random */
+  int32_t group_words;
+  int64_t n_splits;
+  const uint64_t* train_groups;    /* groups: [n_splits][group_words] */
+  const uint64_t* test_groups;     /* groups: [n_splits][group_words] */
+  const uint32_t* split_opt_masks; /* groups: [n_splits] or NULL */
+  const uint64_t* pool_groups;     /* loo: [group_words] */
+  uint64_t seed;                   /* random */
+  uint32_t opt_mask;               /* scored ids when split_opt_masks == NULL */
+  int32_t all_subsets_k;           /* >0: feature mask f = subset bits of counters [0,k) */
+  int64_t n_masks;
+  const uint64_t* feature_masks;   /* [n_masks][2] or NULL (= all counters when k == 0) */
+} or_scenarios;
+
+typedef struct {
+  double ridge;                    /* lambda, 1e-8 */
+  double threshold;                /* 1.05 */
+  double clamp_floor;              /* 0.01 */
+  double guard_tol;                /* 1e-9 (reading R21) */
+  int32_t max_count;               /* 3 */
+} or_params;
+
+typedef struct {
+  int32_t n_train, n_test, n_correct, n_clamped;
+  double sum_ratio, min_ratio, max_ratio;
+  uint64_t fp_train, fp_test;
+} or_opt_score;
+
+typedef struct {
+  int32_t n_rec, n_rec_hit, n_untrained, n_guard;
+} or_scn_score;
+
+/* ------------------------------------------------------------------ */
+/* Tier 1: "We normalize these features by the cycle count".    */
+/* ------------------------------------------------------------------ */
+void or_rates(const double* counters, const double* cycles, int64_t n_slots, int32_t n_counters,
+              double* x_out) {
+  for (int64_t t = 0; t < n_slots; ++t)
+    for (int32_t c = 0; c < n_counters; ++c)
+      x_out[t * n_counters + c] = counters[t * n_counters + c] / cycles[t];
+}
+
+/* SplitMix64 finalizer (reading O2 / R17): the counter-based generator both
+ * sides implement independently for random splits and fingerprints. */
+uint64_t or_mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+/* Random split k: slot t is a training slot iff bit (t mod 64) of
+ * mix(mix(seed ^ mix(k)) + floor(t/64)) is 1, else a test slot (O2). */
+uint64_t or_split_word(uint64_t seed, int64_t split, int64_t word) {
+  return or_mix64(or_mix64(seed ^ or_mix64((uint64_t)split)) + (uint64_t)word);
+}
+
+/* ------------------------------------------------------------------ */
+/* Per-fit min-max scaling (reading D3):  */
+/* over the n training before-vectors, mn/mx per feature; a feature is    */
+/* active iff mx > mn; x' = (x - mn) / (mx - mn) in FP64, unclamped.      */
+/* Writes only active columns; returns d_eff.                             */
+/* ------------------------------------------------------------------ */
+int32_t or_scale(int32_t n, int32_t d, const double* X, int32_t t, const double* Xt,
+                 double* Xs, double* Xts, int32_t* active_cols) {
+  int32_t d_eff = 0;
+  for (int32_t a = 0; a < d; ++a) {
+    double mn = X[a], mx = X[a];
+    for (int32_t i = 1; i < n; ++i) {
+      double v = X[(int64_t)i * d + a];
+      if (v < mn) mn = v;
+      if (v > mx) mx = v;
+    }
+    if (!(mx > mn)) continue;               /* constant feature -> 0 */
+    double rg = mx - mn;
+    for (int32_t i = 0; i < n; ++i) Xs[(int64_t)i * d + d_eff] = (X[(int64_t)i * d + a] - mn) / rg;
+    for (int32_t j = 0; j < t; ++j) Xts[(int64_t)j * d + d_eff] = (Xt[(int64_t)j * d + a] - mn) / rg;
+    if (active_cols) active_cols[d_eff] = a;
+    ++d_eff;
+  }
+  return d_eff;
+}
+
+/* ------------------------------------------------------------------ */
+/* Ridge least squares (reading D1: "linear ... regression";        */
+/* S:253 "lambda = 1e-8 on the normal equations"; intercept unpenalized    */
+/* so that a label shift shifts every prediction):                  */
+/*   (b, w) = argmin sum_i (y_i - b - w.x'_i)^2 + lambda |w|^2             */
+/* written out as its normal equations in centred form:                    */
+/*   xbar = mean x'_i, ybar = mean y_i, Xc = X' - 1 xbar^T, yc = y - ybar  */
+/*   (Xc^T Xc + lambda I) w = Xc^T yc   (Cholesky, quad),  b = ybar - w.xbar */
+/* Prediction EX_j = b + w.x'_j (quad), rounded to FP64 (P:60 Tier 2).      */
+/* Xs is [n][ld], Xts is [t][ld]; only the first d columns are used.        */
+/* coef_out (optional) receives [b, w_0..w_{d-1}] rounded to FP64.          */
+/* Returns 0, or -1 if the Cholesky pivot is not positive.                 */
+/* ------------------------------------------------------------------ */
+int32_t or_fit_predict(int32_t n, int32_t d, int32_t ld, const double* Xs, const double* y,
+                       int32_t t, const double* Xts, double lambda, double* ex_out,
+                       double* coef_out) {
+  quad* xbar = (quad*)calloc((size_t)d + 1, sizeof(quad));
+  quad* G = (quad*)calloc((size_t)d * d + 1, sizeof(quad));
+  quad* rhs = (quad*)calloc((size_t)d + 1, sizeof(quad));
+  quad* w = (quad*)calloc((size_t)d + 1, sizeof(quad));
+  quad ybar = 0;
+  int32_t rc = 0;
+  for (int32_t i = 0; i < n; ++i) ybar += (quad)y[i];
+  ybar /= (quad)n;
+  for (int32_t a = 0; a < d; ++a) {
+    quad s = 0;
+    for (int32_t i = 0; i < n; ++i) s += (quad)Xs[(int64_t)i * ld + a];
+    xbar[a] = s / (quad)n;
+  }
+  /* G = Xc^T Xc + lambda I ; rhs = Xc^T yc */
+  for (int32_t a = 0; a < d; ++a) {
+    for (int32_t c = 0; c <= a; ++c) {
+      quad s = 0;
+      for (int32_t i = 0; i < n; ++i)
+        s += ((quad)Xs[(int64_t)i * ld + a] - xbar[a]) * ((quad)Xs[(int64_t)i * ld + c] - xbar[c]);
+      G[a * d + c] = s;
+      G[c * d + a] = s;
+    }
+    G[a * d + a] += (quad)lambda;
+    quad r = 0;
+    for (int32_t i = 0; i < n; ++i) r += ((quad)Xs[(int64_t)i * ld + a] - xbar[a]) * ((quad)y[i] - ybar);
+    rhs[a] = r;
+  }
+  /* Cholesky G = L L^T (lower triangle stored in G) */
+  for (int32_t j = 0; j < d && rc == 0; ++j) {
+    quad s = G[j * d + j];
+    for (int32_t k = 0; k < j; ++k) s -= G[j * d + k] * G[j * d + k];
+    if (!(s > 0)) { rc = -1; break; }
+    quad ljj = sqrtq(s);
+    G[j * d + j] = ljj;
+    for (int32_t i = j + 1; i < d; ++i) {
+      quad u = G[i * d + j];
+      for (int32_t k = 0; k < j; ++k) u -= G[i * d + k] * G[j * d + k];
+      G[i * d + j] = u / ljj;
+    }
+  }
+  if (rc == 0) {
+    /* L z = rhs ; L^T w = z */
+    for (int32_t i = 0; i < d; ++i) {
+      quad u = rhs[i];
+      for (int32_t k = 0; k < i; ++k) u -= G[i * d + k] * w[k];
+      w[i] = u / G[i * d + i];
+    }
+    for (int32_t i = d - 1; i >= 0; --i) {
+      quad u = w[i];
+      for (int32_t k = i + 1; k < d; ++k) u -= G[k * d + i] * w[k];
+      w[i] = u / G[i * d + i];
+    }
+    quad b = ybar;
+    for (int32_t a = 0; a < d; ++a) b -= w[a] * xbar[a];
+    for (int32_t j = 0; j < t; ++j) {
+      quad e = b;
+      for (int32_t a = 0; a < d; ++a) e += w[a] * (quad)Xts[(int64_t)j * ld + a];
+      ex_out[j] = (double)e;
+    }
+    if (coef_out) {
+      coef_out[0] = (double)b;
+      for (int32_t a = 0; a < d; ++a) coef_out[1 + a] = (double)w[a];
+    }
+  }
+  free(xbar); free(G); free(rhs); free(w);
+  return rc;
+}
+
+/* ------------------------------------------------------------------ */
+/* Tier 3: "sorts them by expected benefit. It then outputs the    */
+/* top choices if their benefit is above a preset threshold."  Sort by    */
+/* (EX desc, id asc), keep EX >= threshold (reading R8), first    */
+/* max_count (R9).  rec_out gets the kept ids; returns how many.          */
+/* ------------------------------------------------------------------ */
+int32_t or_rank(int32_t n_cand, const double* ex, const int32_t* ids, double threshold,
+                int32_t max_count, int32_t* order_out, int32_t* rec_out) {
+  int32_t ord[64];
+  for (int32_t i = 0; i < n_cand; ++i) ord[i] = i;
+  /* insertion sort: plain and stable */
+  for (int32_t i = 1; i < n_cand; ++i) {
+    int32_t cur = ord[i];
+    int32_t j = i - 1;
+    while (j >= 0 && (ex[ord[j]] < ex[cur] || (ex[ord[j]] == ex[cur] && ids[ord[j]] > ids[cur]))) {
+      ord[j + 1] = ord[j];
+      --j;
+    }
+    ord[j + 1] = cur;
+  }
+  if (order_out)
+    for (int32_t i = 0; i < n_cand; ++i) order_out[i] = ids[ord[i]];
+  int32_t n_rec = 0;
+  for (int32_t i = 0; i < n_cand && n_rec < max_count; ++i) {
+    if (ex[ord[i]] >= threshold) rec_out[n_rec++] = ids[ord[i]];
+    else break;
+  }
+  return n_rec;
+}
+
+/* Sign accuracy (Table 3): correct iff both sides of 1.0 agree;
+ * exactly 1.0 counts as "no gain" (reading R11). */
+int32_t or_sign_correct(double ex, double ac) {
+  return (ex > 1.0 && ac > 1.0) || (ex <= 1.0 && ac <= 1.0);
+}
+
+static int near_(double a, double b, double tol) {
+  double s = fabs(a) > 1.0 ? fabs(a) : 1.0;
+  return fabs(a - b) <= tol * s;
+}
+
+/* ------------------------------------------------------------------ */
+/* One scenario, all steps.  See the file header for the step order.      */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  const or_dataset* ds;
+  const or_scenarios* sc;
+  const or_params* pr;
+  int64_t first, count;
+  or_opt_score* opt_scores;   /* [count][O] */
+  or_scn_score* scn_scores;   /* [count] */
+  double* ex;                 /* [count][O][G * 2^(m-1)] or NULL */
+  int8_t* recs;               /* [count][N][max_count] or NULL */
+  const double* x;            /* rates [N][C] */
+  int32_t rc;
+} or_job;
+
+static int bit_of(const uint64_t* words, int64_t i) { return (int)((words[i >> 6] >> (i & 63)) & 1u); }
+
+static void eval_scenario(const or_job* J, int64_t s, or_opt_score* orow, or_scn_score* srow,
+                          double* ex_tab, int8_t* rec_tab) {
+  const or_dataset* ds = J->ds;
+  const or_scenarios* sc = J->sc;
+  const or_params* pr = J->pr;
+  const int32_t P = ds->P, I = ds->I, R = ds->R, m = ds->m, C = ds->C, O = ds->O;
+  const int64_t V = (int64_t)1 << m, half = V >> 1;
+  const int64_t G = (int64_t)P * I * R, N = G * V;
+  const int64_t split = s % sc->n_splits, fmask_idx = s / sc->n_splits;
+
+  /* --- feature set F (counter-index order) --- */
+  int32_t* F = (int32_t*)malloc(sizeof(int32_t) * (size_t)C);
+  int32_t d = 0;
+  for (int32_t c = 0; c < C; ++c) {
+    int in;
+    if (sc->all_subsets_k > 0) in = c < sc->all_subsets_k && ((fmask_idx >> c) & 1);
+    else if (sc->feature_masks) in = (int)((sc->feature_masks[fmask_idx * 2 + (c >> 6)] >> (c & 63)) & 1u);
+    else in = 1;
+    if (in) F[d++] = c;
+  }
+
+  /* --- membership of every slot (Table 2; reading R17) --- */
+  uint8_t* tr = (uint8_t*)calloc((size_t)N, 1);
+  uint8_t* te = (uint8_t*)calloc((size_t)N, 1);
+  if (sc->kind == 0) {
+    const uint64_t* trw = sc->train_groups + split * sc->group_words;
+    const uint64_t* tew = sc->test_groups + split * sc->group_words;
+    for (int64_t t = 0; t < N; ++t) { tr[t] = (uint8_t)bit_of(trw, t / V); te[t] = (uint8_t)bit_of(tew, t / V); }
+  } else if (sc->kind == 1) {
+    int64_t k = 0, held = -1;
+    for (int64_t t = 0; t < N; ++t) {
+      if (!bit_of(sc->pool_groups, t / V)) continue;
+      if (k == split) held = t; else tr[t] = 1;
+      ++k;
+    }
+    if (held >= 0) te[held] = 1;
+  } else {
+    for (int64_t t = 0; t < N; ++t) {
+      uint64_t wv = or_split_word(sc->seed, split, t / 64);
+      tr[t] = (uint8_t)((wv >> (t % 64)) & 1u);
+      te[t] = (uint8_t)!tr[t];
+    }
+  }
+  uint32_t omask = sc->split_opt_masks ? sc->split_opt_masks[split] : sc->opt_mask;
+
+  memset(srow, 0, sizeof(*srow));
+  int64_t maxpairs = G * half;
+  int32_t* tr_before = (int32_t*)malloc(sizeof(int32_t) * (size_t)maxpairs);
+  double* tr_y = (double*)malloc(sizeof(double) * (size_t)maxpairs);
+  int32_t* te_before = (int32_t*)malloc(sizeof(int32_t) * (size_t)maxpairs);
+  int64_t* te_pair = (int64_t*)malloc(sizeof(int64_t) * (size_t)maxpairs);
+  double* te_ac = (double*)malloc(sizeof(double) * (size_t)maxpairs);
+  double* te_ex = (double*)malloc(sizeof(double) * (size_t)maxpairs);
+  double* Xr = (double*)malloc(sizeof(double) * (size_t)maxpairs * (size_t)(d > 0 ? d : 1));
+  double* Xtr = (double*)malloc(sizeof(double) * (size_t)maxpairs * (size_t)(d > 0 ? d : 1));
+  double* Xs = (double*)malloc(sizeof(double) * (size_t)maxpairs * (size_t)(d > 0 ? d : 1));
+  double* Xts = (double*)malloc(sizeof(double) * (size_t)maxpairs * (size_t)(d > 0 ? d : 1));
+  /* per (o, pair) EX and AC for the ranking step */
+  double* EXo = (double*)calloc((size_t)O * (size_t)(G * half), sizeof(double));
+  double* ACo = (double*)calloc((size_t)O * (size_t)(G * half), sizeof(double));
+  uint8_t* CLo = (uint8_t*)calloc((size_t)O * (size_t)(G * half), 1);
+  uint8_t* trained = (uint8_t*)calloc((size_t)O, 1);
+
+  for (int32_t o = 0; o < O; ++o) {
+    or_opt_score* os = &orow[o];
+    memset(os, 0, sizeof(*os));
+    if (!((omask >> o) & 1u)) continue;
+    /* --- pairs ("pairs of before and after code samples"; P:118 the
+     *     32/32 lattice split; label = rt_before / rt_after, reading D2) --- */
+    int32_t n = 0, nt = 0;
+    uint64_t fptr = 0, fpte = 0;
+    for (int64_t g = 0; g < G; ++g) {
+      int32_t p = (int32_t)(g / ((int64_t)I * R));
+      int32_t b = ds->opt_bit[p * O + o];
+      if (b < 0) continue;
+      int64_t k = 0;
+      for (int64_t v = 0; v < V; ++v) {
+        if ((v >> b) & 1) continue;
+        int64_t before = g * V + v, after = g * V + (v | ((int64_t)1 << b));
+        double y = ds->runtime_ms[before] / ds->runtime_ms[after];
+        uint64_t pid = (uint64_t)((g * O + o) * half + k);
+        if (tr[before] && tr[after]) {
+          tr_before[n] = (int32_t)before; tr_y[n] = y; ++n;
+          fptr ^= or_mix64(pid);
+        }
+        if (te[before]) {
+          te_before[nt] = (int32_t)before; te_pair[nt] = g * half + k; te_ac[nt] = y; ++nt;
+          fpte ^= or_mix64(pid);
+        }
+        ++k;
+      }
+    }
+    os->n_train = n; os->n_test = nt; os->fp_train = fptr; os->fp_test = fpte;
+    if (n == 0) {                       /* untrained (reading R18) */
+      srow->n_untrained += nt;
+      continue;
+    }
+    trained[o] = 1;
+    if (nt == 0) continue;              /* nothing to predict or score */
+    /* --- gather rates of the chosen features --- */
+    for (int32_t i = 0; i < n; ++i)
+      for (int32_t a = 0; a < d; ++a) Xr[(int64_t)i * d + a] = J->x[(int64_t)tr_before[i] * C + F[a]];
+    for (int32_t j = 0; j < nt; ++j)
+      for (int32_t a = 0; a < d; ++a) Xtr[(int64_t)j * d + a] = J->x[(int64_t)te_before[j] * C + F[a]];
+    int32_t d_eff = d > 0 ? or_scale(n, d, Xr, nt, Xtr, Xs, Xts, NULL) : 0;
+    if (or_fit_predict(n, d_eff, d > 0 ? d : 1, Xs, tr_y, nt, Xts, pr->ridge, te_ex, NULL) != 0) {
+      /* unreachable for lambda > 0 (G + lambda I is SPD); poison the row */
+      srow->n_guard = -1000000;
+    }
+    /* --- clamp (reading R7) and score --- */
+    quad sum = 0;
+    double mnr = 0, mxr = 0;
+    for (int32_t j = 0; j < nt; ++j) {
+      double e = te_ex[j];
+      if (near_(e, 0.0, pr->guard_tol) || near_(e, 1.0, pr->guard_tol)) srow->n_guard++;
+      if (e <= 0.0) {
+        e = pr->clamp_floor; os->n_clamped++;
+        CLo[(int64_t)o * G * half + te_pair[j]] = 1;
+      }
+      te_ex[j] = e;
+      double ac = te_ac[j];
+      os->n_correct += or_sign_correct(e, ac);
+      double ratio = ac / e;
+      sum += (quad)ratio;
+      if (j == 0 || ratio < mnr) mnr = ratio;
+      if (j == 0 || ratio > mxr) mxr = ratio;
+      EXo[(int64_t)o * G * half + te_pair[j]] = e;
+      ACo[(int64_t)o * G * half + te_pair[j]] = ac;
+      if (ex_tab) ex_tab[(int64_t)o * G * half + te_pair[j]] = e;
+    }
+    os->sum_ratio = (double)sum; os->min_ratio = mnr; os->max_ratio = mxr;
+  }
+
+  /* --- rank + recommend per test slot (reading R13) --- */
+  for (int64_t t = 0; t < N; ++t) {
+    if (!te[t]) continue;
+    int64_t g = t / V, v = t % V;
+    int32_t p = (int32_t)(g / ((int64_t)I * R));
+    double cex[32];
+    int32_t cid[32], rec[32];
+    uint8_t ccl[32];
+    int32_t nc = 0;
+    for (int32_t o = 0; o < O && nc < 32; ++o) {
+      if (!((omask >> o) & 1u) || !trained[o]) continue;
+      int32_t b = ds->opt_bit[p * O + o];
+      if (b < 0 || ((v >> b) & 1)) continue;
+      int64_t k = (v & (((int64_t)1 << b) - 1)) | ((v >> (b + 1)) << b);
+      cex[nc] = EXo[(int64_t)o * G * half + g * half + k];
+      ccl[nc] = CLo[(int64_t)o * G * half + g * half + k];
+      cid[nc] = o;
+      ++nc;
+    }
+    /* guard cases (reading R21): a decision closer than guard_tol to its
+     * boundary; two clamped candidates tie exactly by rule, not by rounding */
+    for (int32_t i = 0; i < nc; ++i) {
+      if (near_(cex[i], pr->threshold, pr->guard_tol)) srow->n_guard++;
+      for (int32_t j = i + 1; j < nc; ++j)
+        if (!(ccl[i] && ccl[j]) && near_(cex[i], cex[j], pr->guard_tol)) srow->n_guard++;
+    }
+    int32_t nr = or_rank(nc, cex, cid, pr->threshold, pr->max_count, NULL, rec);
+    srow->n_rec += nr;
+    for (int32_t i = 0; i < nr; ++i) {
+      int32_t o = rec[i];
+      int32_t b = ds->opt_bit[p * O + o];
+      int64_t k = (v & (((int64_t)1 << b) - 1)) | ((v >> (b + 1)) << b);
+      if (ACo[(int64_t)o * G * half + g * half + k] > 1.0) srow->n_rec_hit++;
+    }
+    if (rec_tab) {
+      for (int32_t i = 0; i < pr->max_count; ++i) rec_tab[t * pr->max_count + i] = (int8_t)(i < nr ? rec[i] : -1);
+    }
+  }
+
+  free(F); free(tr); free(te); free(tr_before); free(tr_y); free(te_before); free(te_pair);
+  free(te_ac); free(te_ex); free(Xr); free(Xtr); free(Xs); free(Xts); free(EXo); free(ACo);
+  free(CLo); free(trained);
+}
+
+static void* job_run(void* arg) {
+  or_job* J = (or_job*)arg;
+  const or_dataset* ds = J->ds;
+  const int64_t V = (int64_t)1 << ds->m, G = (int64_t)ds->P * ds->I * ds->R;
+  const int64_t ex_stride = (int64_t)ds->O * G * (V >> 1);
+  const int64_t rec_stride = G * V * J->pr->max_count;
+  for (int64_t j = 0; j < J->count; ++j) {
+    double* ex = J->ex ? J->ex + j * ex_stride : NULL;
+    int8_t* rc = J->recs ? J->recs + j * rec_stride : NULL;
+    if (ex) memset(ex, 0, sizeof(double) * (size_t)ex_stride);
+    if (rc) memset(rc, -1, (size_t)rec_stride);
+    eval_scenario(J, J->first + j, J->opt_scores + j * ds->O, J->scn_scores + j, ex, rc);
+  }
+  return NULL;
+}
+
+/* Evaluate scenarios [first, first+count) with n_threads POSIX threads
+ * (contiguous chunks).  Output layout matches the CUDA path's sr_outputs. */
+int32_t or_evaluate(const or_dataset* ds, const or_scenarios* sc, const or_params* pr,
+                    int64_t first, int64_t count, or_opt_score* opt_scores,
+                    or_scn_score* scn_scores, double* ex, int8_t* recs, int32_t n_threads) {
+  const int64_t N = ((int64_t)ds->P * ds->I * ds->R) << ds->m;
+  double* x = (double*)malloc(sizeof(double) * (size_t)N * (size_t)ds->C);
+  or_rates(ds->counters, ds->cycles, N, ds->C, x);
+  if (n_threads < 1) n_threads = 1;
+  if (n_threads > count) n_threads = (int32_t)(count > 0 ? count : 1);
+  or_job* jobs = (or_job*)calloc((size_t)n_threads, sizeof(or_job));
+  pthread_t* th = (pthread_t*)calloc((size_t)n_threads, sizeof(pthread_t));
+  const int64_t V = (int64_t)1 << ds->m, G = (int64_t)ds->P * ds->I * ds->R;
+  const int64_t ex_stride = (int64_t)ds->O * G * (V >> 1);
+  const int64_t rec_stride = G * V * pr->max_count;
+  int64_t base = 0;
+  for (int32_t k = 0; k < n_threads; ++k) {
+    int64_t c = count / n_threads + (k < count % n_threads ? 1 : 0);
+    or_job* J = &jobs[k];
+    J->ds = ds; J->sc = sc; J->pr = pr; J->first = first + base; J->count = c; J->x = x;
+    J->opt_scores = opt_scores + base * ds->O;
+    J->scn_scores = scn_scores + base;
+    J->ex = ex ? ex + base * ex_stride : NULL;
+    J->recs = recs ? recs + base * rec_stride : NULL;
+    base += c;
+    pthread_create(&th[k], NULL, job_run, J);
+  }
+  for (int32_t k = 0; k < n_threads; ++k) pthread_join(th[k], NULL);
+  free(th); free(jobs); free(x);
+  return 0;
+}

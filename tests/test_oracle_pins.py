@@ -1,0 +1,386 @@
+"""Pins of the oracle against what the paper, SPEC and mathematics fix.
+
+None of these tests retypes the oracle's own formula: each compares it with
+a worked example (tests/golden/spec_examples.json, cited), exact rational
+arithmetic (fractions.Fraction), a closed form, an invariant, an independent
+brute-force enumeration, or a library routine on a special case.
+"""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from gen.synth import Dataset
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+M64 = 2**64 - 1
+
+
+# --------------------------------------------------------------------- Tier 1
+def test_rates_worked_examples():
+    for case in GOLD["normalize"]["cases"]:
+        c = np.array([case["counters"]], dtype=np.float64)
+        cyc = np.array([case["cycles"]], dtype=np.float64)
+        if "scaled_by" in case:
+            k = case["scaled_by"]
+            np.testing.assert_array_equal(oracle.rates(c * k, cyc * k)[0], case["expect"])
+        np.testing.assert_array_equal(oracle.rates(c, cyc)[0], case["expect"])
+
+
+def test_rates_scale_invariance():
+    # multiplying cycles and all counters by the same constant leaves
+    # the vector unchanged within 1e-12 relative.
+    rng = np.random.default_rng(0)
+    c = np.rint(rng.uniform(0, 1e7, size=(50, 16)))
+    cyc = np.rint(rng.uniform(1e5, 1e8, size=50))
+    base = oracle.rates(c, cyc)
+    for k in (3.0, 7.5, 1e3):
+        np.testing.assert_allclose(oracle.rates(c * k, cyc * k), base, rtol=1e-12, atol=0)
+
+
+# ----------------------------------------------------------- split hashing
+def _py_mix(x):
+    x = (x + 0x9E3779B97F4A7C15) & M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M64
+    return x ^ (x >> 31)
+
+
+def test_mix64_public_test_vector():
+    g = int(GOLD["splitmix64"]["gamma"], 16)
+    for k, out in enumerate(GOLD["splitmix64"]["outputs"]):
+        assert oracle.mix64((k * g) & M64) == int(out, 16)
+
+
+def test_split_word_independent_python():
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        seed, split, word = (int(v) for v in rng.integers(0, 2**62, size=3))
+        expect = _py_mix((_py_mix(seed ^ _py_mix(split)) + word) & M64)
+        assert oracle.split_word(seed, split, word) == expect
+
+
+# ----------------------------------------------------------- lattice / pairs
+def _brute_pairs(ds, tr, te, o):
+    """Independent enumeration of (training pairs, test cases) by brute force
+    over all slot pairs that differ in exactly optimization o's bit."""
+    V = 1 << ds.n_opt_bits
+    G = ds.n_groups
+    ntr = nte = 0
+    fptr = fpte = 0
+    for g in range(G):
+        p = g // (ds.n_inputs * ds.n_runs)
+        b = int(ds.opt_bit[p, o])
+        if b < 0:
+            continue
+        befores = sorted(v for v in range(V) if not (v >> b) & 1)
+        assert len(befores) == V // 2       # P:118 "32 versions ... do not ... include"
+        for k, v in enumerate(befores):
+            t, a = g * V + v, g * V + (v | (1 << b))
+            assert bin((t ^ a)).count("1") == 1
+            pid = (g * ds.n_opt_ids + o) * (V // 2) + k
+            if tr[t] and tr[a]:
+                ntr += 1
+                fptr ^= _py_mix(pid)
+            if te[t]:
+                nte += 1
+                fpte ^= _py_mix(pid)
+    return ntr, nte, fptr, fpte
+
+
+def test_random_split_counts_and_fingerprints_brute_force():
+    cfg = gen.make_config("C3", n_splits=12)
+    ds, sc = cfg.dataset, cfg.scenarios
+    r = oracle.evaluate(ds, sc, 0, 12)
+    N = ds.n_slots
+    for s in range(12):
+        tr = [(_py_mix((_py_mix(sc.seed ^ _py_mix(s)) + t // 64) & M64) >> (t % 64)) & 1 for t in range(N)]
+        te = [1 - v for v in tr]
+        for o in range(ds.n_opt_ids):
+            row = r["opt"][s, o]
+            ntr, nte, fptr, fpte = _brute_pairs(ds, tr, te, o)
+            assert (row["n_train"], row["n_test"]) == (ntr, nte)
+            assert (int(row["fp_train"]), int(row["fp_test"])) == (fptr, fpte)
+
+
+def test_loo_removes_exactly_one_pair():
+    # "always leaves 32 feature vectors"; LOO over one 64-version group:
+    # every optimization keeps 31 training pairs; the held-out version is a
+    # test case exactly for the optimizations it lacks (6 - popcount).
+    cfg = gen.make_config("C1")
+    r = oracle.evaluate(cfg.dataset, cfg.scenarios, 0, 64)
+    for v in range(64):
+        row = r["opt"][v]
+        assert (row["n_train"] == 31).all()
+        assert list(row["n_test"]) == [1 - ((v >> b) & 1) for b in range(6)]
+
+
+def test_table2_counts():
+    cfg = gen.make_config("C2")
+    ds, sc = cfg.dataset, cfg.scenarios
+    assert sc.n_splits == 240
+    r = oracle.evaluate(ds, sc, 0, 240)
+    ftz, rsq = ds.opt_names.index("FTZ"), ds.opt_names.index("RSQRT")
+    for s in range(240):
+        e = str(int(sc.experiment[s]))
+        n, t = GOLD["table2_counts"]["per_experiment"][e]
+        om = int(sc.split_opt_masks[s])
+        for o in range(ds.n_opt_ids):
+            row = r["opt"][s, o]
+            if (om >> o) & 1:
+                assert (row["n_train"], row["n_test"]) == (n, t), (s, e, o)
+            else:
+                assert row["n_train"] == 0 and row["n_test"] == 0
+        if e in ("5", "6"):
+            assert om == (1 << ftz) | (1 << rsq)
+
+
+# ------------------------------------------------------------------ scaling
+def test_scale_invariants():
+    rng = np.random.default_rng(2)
+    X = rng.uniform(0, 1, size=(20, 6))
+    X[:, 3] = 0.25                                       # constant feature -> dropped
+    Xt = rng.uniform(-0.5, 1.5, size=(7, 6))
+    Xs, Xts, act = oracle.scale(X, Xt)
+    assert list(act) == [0, 1, 2, 4, 5]
+    assert (Xs.min(0) == 0).all() and (Xs.max(0) == 1).all()   # exact in IEEE
+    # power-of-two rescaling of a raw feature is exact -> identical scaled values
+    X2, Xt2 = X.copy(), Xt.copy()
+    X2[:, 1] *= 8.0
+    Xt2[:, 1] *= 8.0
+    Xs2, Xts2, _ = oracle.scale(X2, Xt2)
+    np.testing.assert_array_equal(Xs2, Xs)
+    np.testing.assert_array_equal(Xts2, Xts)
+    # permuting features permutes the scaled columns
+    perm = [5, 2, 0, 4, 1, 3]
+    Xs3, Xts3, act3 = oracle.scale(X[:, perm], Xt[:, perm])
+    for j, a in enumerate(act3):
+        k = list(act).index(perm[a])
+        np.testing.assert_array_equal(Xs3[:, j], Xs[:, k])
+
+
+# --------------------------------------------------------------- ridge fit
+def _exact_ridge(Xs, y, Xts, lam):
+    """Exact rational ridge with unpenalized intercept, UNcentred augmented
+    normal equations (a different route than the oracle's centred one):
+    ([1 X]^T [1 X] + diag(0, lam..lam)) beta = [1 X]^T y."""
+    n, d = Xs.shape
+    A = [[Fraction(1)] + [Fraction(float(v)) for v in row] for row in Xs]
+    Y = [Fraction(float(v)) for v in y]
+    L = Fraction(lam)
+    p = d + 1
+    M = [[sum(A[i][a] * A[i][b] for i in range(n)) + (L if (a == b and a > 0) else 0)
+          for b in range(p)] + [sum(A[i][a] * Y[i] for i in range(n))] for a in range(p)]
+    for c in range(p):                                   # Gauss-Jordan, exact
+        piv = next(r for r in range(c, p) if M[r][c] != 0)
+        M[c], M[piv] = M[piv], M[c]
+        for r in range(p):
+            if r != c and M[r][c] != 0:
+                f = M[r][c] / M[c][c]
+                M[r] = [M[r][k] - f * M[c][k] for k in range(p + 1)]
+    beta = [M[a][p] / M[a][a] for a in range(p)]
+    return [beta[0] + sum(beta[1 + a] * Fraction(float(v)) for a, v in enumerate(row)) for row in Xts]
+
+
+@pytest.mark.parametrize("n,d", [(8, 3), (5, 3), (3, 3), (2, 2), (6, 1), (4, 3)])
+def test_fit_exact_rational_bruteforce(n, d):
+    rng = np.random.default_rng(100 + 10 * n + d)
+    for lam in (1e-8, 0.5):
+        X = rng.uniform(0, 1, size=(n, d))
+        Xs, Xts, _ = oracle.scale(X, rng.uniform(-0.2, 1.2, size=(4, d)))
+        y = rng.uniform(0.6, 1.4, size=n)
+        ex, _ = oracle.fit_predict(Xs, y, Xts, ridge=lam)
+        exact = _exact_ridge(Xs, y, Xts, lam)
+        for e, q in zip(ex, exact):
+            assert abs(Fraction(float(e)) - q) <= abs(q) * Fraction(1, 2**52) + Fraction(1, 10**30)
+
+
+def test_fit_planted_linear_model_recovered():
+    # Overdetermined, lambda = 0: coefficients of y = c0 + c.x' recovered.
+    rng = np.random.default_rng(3)
+    Xs = rng.uniform(0, 1, size=(40, 5))
+    c0, c = 1.1, np.array([0.3, -0.2, 0.05, 0.0, 0.4])
+    y = c0 + Xs @ c
+    Xts = rng.uniform(0, 1, size=(10, 5))
+    ex, coef = oracle.fit_predict(Xs, y, Xts, ridge=0.0)
+    np.testing.assert_allclose(coef, np.r_[c0, c], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(ex, c0 + Xts @ c, rtol=0, atol=1e-13)
+    # lambda = 1e-8: within the ridge-bias bound lambda*|w|/sigma_min^2
+    ex2, _ = oracle.fit_predict(Xs, y, Xts, ridge=1e-8)
+    Xc = Xs - Xs.mean(0)
+    smin2 = np.linalg.svd(Xc, compute_uv=False)[-1] ** 2
+    bound = 1e-8 * np.linalg.norm(c) / smin2 * np.abs(Xts - Xs.mean(0)).sum(1).max() * 2
+    assert np.max(np.abs(ex2 - (c0 + Xts @ c))) <= bound
+
+
+def test_fit_lstsq_special_case():
+    # lambda -> 0 on a well-conditioned overdetermined fit = ordinary least squares.
+    rng = np.random.default_rng(4)
+    Xs = rng.uniform(0, 1, size=(60, 8))
+    y = rng.uniform(0.5, 1.5, size=60)
+    Xts = rng.uniform(0, 1, size=(9, 8))
+    ex, _ = oracle.fit_predict(Xs, y, Xts, ridge=0.0)
+    A = np.c_[np.ones(60), Xs]
+    beta = np.linalg.lstsq(A, y, rcond=None)[0]
+    np.testing.assert_allclose(ex, np.c_[np.ones(9), Xts] @ beta, rtol=1e-12, atol=1e-12)
+
+
+def test_fit_label_shift_and_constant_labels():
+    rng = np.random.default_rng(5)
+    for n, d in ((31, 32), (16, 64), (63, 20)):          # under- and overdetermined
+        Xs, Xts, _ = oracle.scale(rng.uniform(0, 1, (n, d)), rng.uniform(0, 1, (7, d)))
+        y = rng.uniform(0.6, 1.4, n)
+        ex, _ = oracle.fit_predict(Xs, y, Xts)
+        ex2, _ = oracle.fit_predict(Xs, y + 0.5, Xts)     # S:246 label shift
+        np.testing.assert_allclose(ex2, ex + 0.5, rtol=0, atol=1e-12)
+        exc, _ = oracle.fit_predict(Xs, np.full(n, 1.23), Xts)
+        np.testing.assert_array_equal(exc, 1.23)
+
+
+def test_fit_degenerate_cases():
+    y1 = np.array([1.37])
+    ex, _ = oracle.fit_predict(np.zeros((1, 0)), y1, np.zeros((3, 0)))
+    np.testing.assert_array_equal(ex, 1.37)             # n = 1 -> EX = y_1
+    y = np.array([0.9, 1.2, 1.5])
+    ex, _ = oracle.fit_predict(np.zeros((3, 0)), y, np.zeros((2, 0)))
+    assert np.all(np.abs(ex - 1.2) <= 2.3e-16)           # d_eff = 0 -> EX = ybar
+
+
+def test_fit_feature_permutation_invariance():
+    rng = np.random.default_rng(6)
+    for n, d in ((16, 64), (40, 8)):
+        Xs, Xts, _ = oracle.scale(rng.uniform(0, 1, (n, d)), rng.uniform(0, 1, (9, d)))
+        y = rng.uniform(0.6, 1.4, n)
+        perm = rng.permutation(d)
+        ex, _ = oracle.fit_predict(Xs, y, Xts)
+        exp_, _ = oracle.fit_predict(Xs[:, perm], y, Xts[:, perm])
+        np.testing.assert_allclose(exp_, ex, rtol=1e-15, atol=1e-15)
+
+
+def test_fit_dual_identity_training_residual():
+    # Underdetermined ridge: training residual y_c - Xc w = lambda * alpha with
+    # alpha = (Xc Xc^T + lambda I)^-1 y_c (exact algebra).  Predicting the
+    # training rows themselves gives EX_i = y_i - lambda*alpha_i.
+    rng = np.random.default_rng(7)
+    n, d = 6, 12
+    Xs, _, _ = oracle.scale(rng.uniform(0, 1, (n, d)), np.zeros((0, d)))
+    y = rng.uniform(0.6, 1.4, n)
+    lam = 1e-3
+    ex, _ = oracle.fit_predict(Xs, y, Xs, ridge=lam)
+    F = lambda v: Fraction(float(v))
+    Xc = [[F(Xs[i, a]) - sum(F(Xs[k, a]) for k in range(n)) / n for a in range(d)] for i in range(n)]
+    yc = [F(y[i]) - sum(F(v) for v in y) / n for i in range(n)]
+    K = [[sum(Xc[i][a] * Xc[j][a] for a in range(d)) + (Fraction(lam) if i == j else 0) for j in range(n)]
+         for i in range(n)]
+    M = [K[i] + [yc[i]] for i in range(n)]
+    for c in range(n):
+        for r in range(n):
+            if r != c:
+                f = M[r][c] / M[c][c]
+                M[r] = [M[r][k] - f * M[c][k] for k in range(n + 1)]
+    alpha = [M[i][n] / M[i][i] for i in range(n)]
+    for i in range(n):
+        q = F(y[i]) - Fraction(lam) * alpha[i]
+        assert abs(Fraction(float(ex[i])) - q) <= abs(q) * Fraction(1, 2**52)
+
+
+# ------------------------------------------------------------------- Tier 3
+def test_rank_worked_examples():
+    for case in GOLD["rank_and_filter"]["cases"]:
+        names = list(case["pred"])
+        ex = [case["pred"][k] for k in names]
+        ids = [case["ids"][k] for k in names]
+        _, rec = oracle.rank(ex, ids, case["threshold"], case["max_count"])
+        inv = {v: k for k, v in case["ids"].items()}
+        assert [inv[i] for i in rec] == case["expect"]
+
+
+def test_rank_properties():
+    rng = np.random.default_rng(8)
+    for _ in range(2000):
+        k = int(rng.integers(1, 10))
+        ex = rng.choice([0.8, 1.0, 1.05, 1.2, 2.0], size=k) if rng.random() < 0.3 else rng.uniform(0.5, 1.6, k)
+        ids = rng.permutation(16)[:k]
+        th = float(rng.uniform(0.9, 1.3))
+        mc = int(rng.integers(1, 6))
+        order, rec = oracle.rank(ex, ids, th, mc)
+        pos = {i: j for j, i in enumerate(ids)}
+        vals = [ex[pos[i]] for i in order]
+        assert all(vals[j] > vals[j + 1] or (vals[j] == vals[j + 1] and order[j] < order[j + 1])
+                   for j in range(k - 1))                                       # ordering soundness
+        assert len(rec) <= mc and all(ex[pos[i]] >= th for i in rec)
+        _, rec_hi = oracle.rank(ex, ids, th + 0.1, mc)                          # threshold monotonicity
+        assert rec_hi == rec[:len(rec_hi)]
+        order2, _ = oracle.rank(np.exp(3 * ex) - 7, ids, -1e300, 100)           # monotone invariance
+        assert order2 == order
+
+
+def test_sign_accuracy_worked_example():
+    g = GOLD["sign_accuracy"]
+    correct = sum(oracle.sign_correct(e, a) for e, a in zip(g["ex"], g["ac"]))
+    assert correct == g["expect_correct"]
+    assert oracle.sign_correct(1.0, 1.0) and oracle.sign_correct(1.0, 0.5) and not oracle.sign_correct(1.0, 1.1)
+
+
+# -------------------------------------------------------- end-to-end plants
+def _plant_dataset(seed, C=4, y_of=None):
+    """One program, one input, one run; labels planted per optimization."""
+    rng = np.random.default_rng(seed)
+    V = 64
+    counters = np.rint(rng.uniform(1e3, 1e6, size=(V, C)))
+    cycles = np.rint(rng.uniform(1e6, 2e6, size=V))
+    x = counters / cycles[:, None]
+    return counters, cycles, x
+
+
+def test_pipeline_planted_linear_speedup():
+    # rt(v | 2^b) = rt(v) / f(x(v)) for bit-clear v, f linear in raw rates
+    # (hence in min-max scaled ones): with LOO (n = 31 > d_eff + 1 = 5) the
+    # prediction of the held-out case recovers f within the ridge bias, so
+    # every sign is right and every AC/EX ratio is 1 within 1e-6.
+    counters, cycles, x = _plant_dataset(9)
+    b = 2
+    rng = np.random.default_rng(10)
+    rt = rng.uniform(5, 10, size=64)
+    coef = np.array([0.4, -0.3, 0.2, 0.1])
+    for v in range(64):
+        if not (v >> b) & 1:
+            f = 0.7 + x[v] @ coef * 3.0
+            rt[v | (1 << b)] = rt[v] / f
+    ob = np.array([[0, 1, 2, 3, 4, 5]], dtype=np.int8)
+    ds = Dataset(1, 1, 1, 6, 4, 6, counters, cycles, rt, ob, [f"O{j}" for j in range(6)], ["P0"])
+    sc = gen.configs.Scenarios(kind="loo", n_splits=64, group_words=1,
+                               pool_groups=np.array([1], dtype=np.uint64), opt_mask=1 << b)
+    r = oracle.evaluate(ds, sc, 0, 64, want_ex=True)
+    rows = r["opt"][:, b]
+    sel = rows["n_test"] > 0
+    assert sel.sum() == 32
+    assert (rows["n_correct"][sel] == 1).all()
+    np.testing.assert_allclose(rows["sum_ratio"][sel], 1.0, rtol=0, atol=1e-6)
+
+
+def test_pipeline_recommendation_rule():
+    # SPEC acceptance #7 analogue: optimization 0 halves the runtime (AC = 2
+    # exactly), optimization 1 slows it (AC = 0.8).  Constant labels give
+    # EX = AC exactly, so every test version lacking bit 0 gets exactly one
+    # recommendation, [0], and it is a hit; versions with bit 0 get none.
+    counters, cycles, _ = _plant_dataset(11)
+    v = np.arange(64)
+    rt = 8.0 * np.where(v & 1, 0.5, 1.0) * np.where(v & 2, 1.25, 1.0)
+    ob = np.array([[0, 1, 2, 3, 4, 5]], dtype=np.int8)
+    ds = Dataset(1, 1, 1, 6, 4, 6, counters, cycles, rt, ob, [f"O{j}" for j in range(6)], ["P0"])
+    sc = gen.configs.Scenarios(kind="loo", n_splits=64, group_words=1,
+                               pool_groups=np.array([1], dtype=np.uint64), opt_mask=0b11)
+    r = oracle.evaluate(ds, sc, 0, 64, want_recs=True)
+    for s in range(64):
+        recs = r["recs"][s, s]
+        if s & 1:
+            assert list(recs) == [-1, -1, -1]
+        else:
+            assert list(recs) == [0, -1, -1]
+    assert r["scn"]["n_rec"].sum() == 32 and r["scn"]["n_rec_hit"].sum() == 32
+    assert (r["opt"][:, 0]["n_correct"] == r["opt"][:, 0]["n_test"]).all()
