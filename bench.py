@@ -1,0 +1,298 @@
+#!/usr/bin/env python
+"""Benchmark: train/test scenario evaluations per second of the fused
+Tier-2/Tier-3 path (arXiv 1910.07776) on B200, with the roofline of the
+dominant kernel and the CPU oracle as a reported baseline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+
+One step = one sr_evaluate call over the rank's batch of scenarios: A0 rates,
+A1 labels + pairs, A2-A7 fused (three kernel launches).  Default workload =
+config C3 (2 programs x 64 variants x 64 counters, 1e6 random train/test
+splits per GPU; weak scaling: rank r evaluates splits [r*S, (r+1)*S)).
+Under torchrun each rank drives one GPU; the only collective is the NCCL
+all-reduce of the pooled integer totals (A7 "per config") and of the timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_FMA_PER_CLK_PER_SM = 64   # inferred from the measured DMMA loop (profiles/fp64_peak.txt)
+
+
+def fit_flops(n: np.ndarray, t: np.ndarray, d: int, refine: int = 2) -> float:
+    """Algorithmic FP64 flops of the fits a batch performed:
+    per fit with n training pairs, t test cases and d active features,
+      dual   (n-1 < d): n(n+1)/2*d + n^3/6 + refine*(2nd + n^2) + nd + td   FMA
+      primal (else)   : n*d(d+1)/2 + d^3/6 + nd + refine*(2nd + d^2) + td  FMA
+    flop = 2 * FMA.  Fits with n == 0 or t == 0 do no work."""
+    n = n.astype(np.float64)
+    t = t.astype(np.float64)
+    live = (n > 0) & (t > 0)
+    dual = (n - 1) < d
+    fd = n * (n + 1) / 2 * d + n ** 3 / 6 + refine * (2 * n * d + n ** 2) + n * d + t * d
+    fp = n * d * (d + 1) / 2 + d ** 3 / 6 + n * d + refine * (2 * n * d + d ** 2) + t * d
+    return float(2.0 * np.where(live, np.where(dual, fd, fp), 0.0).sum())
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, fl in rows for i, f in enumerate(fl) if f.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def oracle_rate(cfg, first: int, count: int, threads: int):
+    import oracle
+    t0 = time.perf_counter()
+    oracle.evaluate(cfg.dataset, cfg.scenarios, first, count, n_threads=threads)
+    return count / (time.perf_counter() - t0)
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle (this tier's reference arm) on host cores."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample = args.ref_sample
+    for _ in range(args.warmup):
+        oracle_rate(cfg, 0, max(threads, sample // 10), threads)
+    rates = []
+    for k in range(args.steps):
+        rates.append(oracle_rate(cfg, (k * sample) % cfg.scenarios.n_splits, sample, threads))
+    v = float(np.mean(rates))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "scenario_evals/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sample / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+quad",
+        "data": "synthetic", "config": workload_config(cfg, args, sample),
+        "cpu_baseline": {"value": v, "unit": "scenario_evals/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{sample} scenarios of {args.config} per step (splits "
+                                   f"[k*{sample}, (k+1)*{sample}))"},
+        "e2e": {"value": v, "unit": "scenario_evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "train/test scenario evals/sec at 1/2/4/8 B200 (roofline frac) vs CPU oracle"
+
+
+def workload_config(cfg, args, per_gpu):
+    ds = cfg.dataset
+    return {"workload": f"{cfg.name}: {cfg.description}", "splits_per_gpu": per_gpu,
+            "programs": ds.n_programs, "variants": ds.n_slots, "counters": ds.n_counters,
+            "optimizations": ds.n_opt_ids, "parallelism": f"scenario-sharded x{args.gpus}",
+            "l2": "flushed between timed steps (256 MiB write); dataset 64 KiB is L2/smem resident by design"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--splits", type=int, default=None, help="scenarios per GPU (default: config size)")
+    ap.add_argument("--impl", default="own", choices=["own", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=4000)
+    ap.add_argument("--cpu-sample", type=int, default=4000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import gen
+    per_gpu = args.splits or {"C3": 1_000_000, "C1": 64, "C2": 240}.get(args.config, 100_000)
+    cfg = gen.make_config(args.config, n_splits=per_gpu * world if args.config in ("C3", "C4") else None,
+                          n_masks_k=10 if args.config == "C5" else None)
+    if args.config not in ("C3", "C4"):
+        per_gpu = cfg.scenarios.n_scenarios // world
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1910_07776_b200 import Context
+    from paper_1910_07776_b200.speedrec import OPT_SCORE_DTYPE, SCN_SCORE_DTYPE
+    stream = torch.cuda.current_stream()
+    ctx = Context(local, stream=stream.cuda_stream)
+    ds = cfg.dataset
+    ctx.load(ds)
+    ctx.define_scenarios(cfg.scenarios)
+    first, count = rank * per_gpu, per_gpu
+    O = ds.n_opt_ids
+    dev = torch.device("cuda", local)
+    out = dict(opt=torch.empty(count * O * OPT_SCORE_DTYPE.itemsize, dtype=torch.uint8, device=dev),
+               scn=torch.empty(count * SCN_SCORE_DTYPE.itemsize, dtype=torch.uint8, device=dev),
+               totals=torch.zeros(4, dtype=torch.int64, device=dev))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    for _ in range(args.warmup):
+        ctx.evaluate(first, count, out=out)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K steps, device events, L2 flushed between steps
+    ctx.set_timing(True)
+    ctx.reset_kernel_stats()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            evs[k][0].record(stream)
+            ctx.evaluate(first, count, out=out)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    stats = ctx.kernel_stats()
+    ctx.set_timing(False)
+    launches = sum(v[0] for v in stats.values())
+    my_ms = float(np.mean(step_ms))
+    t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+    tot = out["totals"].clone()
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    ms = float(t.item())
+    value = world * count / (ms / 1e3)
+
+    # ---------------- roofline of the dominant kernel (FP64 ALU/DMMA bound)
+    opt = out["opt"].cpu().numpy().view(OPT_SCORE_DTYPE).reshape(count, O)
+    flops_launch = fit_flops(opt["n_train"].ravel(), opt["n_test"].ravel(), ds.n_counters)
+    name_dom = "k_eval_warp"
+    n_dom, ms_dom = stats.get(name_dom, (0, 0.0))
+    avg_dom = ms_dom / max(n_dom, 1)
+    clk_sum = clk.summary()
+    sm_max = clk_sum.get("sm_max_mhz") or 1965.0
+    props = torch.cuda.get_device_properties(dev)
+    peak = props.multi_processor_count * FP64_FMA_PER_CLK_PER_SM * 2 * sm_max * 1e6 / 1e12
+    achieved = flops_launch / (avg_dom / 1e3) / 1e12 if avg_dom > 0 else 0.0
+    share = ms_dom / max(sum(v[1] for v in stats.values()), 1e-9)
+
+    # ---------------- end to end: host buffers through the C-ABI, copies inside
+    e2e = None
+    if True:
+        hc = torch.from_numpy(ds.counters).pin_memory()
+        hy = torch.from_numpy(ds.cycles).pin_memory()
+        hr = torch.from_numpy(ds.runtime_ms).pin_memory()
+        hb = torch.from_numpy(ds.opt_bit).pin_memory()
+        hopt = torch.empty(count * O * OPT_SCORE_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+        hscn = torch.empty(count * SCN_SCORE_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+        htot = torch.zeros(4, dtype=torch.int64).pin_memory()
+        from paper_1910_07776_b200.speedrec import sr_outputs, lib, default_params
+        import ctypes as ct
+        hout = sr_outputs(hopt.data_ptr(), hscn.data_ptr(), None, None, htot.data_ptr(), 0)
+        prm = default_params()
+        e2e_ms = []
+        for k in range(max(2, min(args.steps, 5)) + 1):
+            flush.fill_(float(k))
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.load_dataset(ds.n_programs, ds.n_inputs, ds.n_runs, ds.n_counters, ds.n_opt_ids,
+                             hc.numpy(), hy.numpy(), hr.numpy(), hb.numpy())
+            ctx.define_scenarios(cfg.scenarios)
+            ctx._check(lib().sr_evaluate(ctx._h, ct.byref(prm), first, count, ct.byref(hout)))
+            b.record(stream)
+            torch.cuda.synchronize()
+            if k > 0:
+                e2e_ms.append(a.elapsed_time(b))
+        te = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * count / (te.item() / 1e3), "unit": "scenario_evals/s",
+               "h2d_bytes_per_step": int(hc.numel() * 8 + hy.numel() * 8 + hr.numel() * 8 + hb.numel()),
+               "d2h_bytes_per_step": int(hopt.numel() + hscn.numel() + 32)}
+
+    # ---------------- CPU oracle baseline (rank 0, N=1 only, bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v = oracle_rate(cfg, 0, args.cpu_sample, threads)
+        cpu = {"value": v, "unit": "scenario_evals/s", "cores": threads, "kind": "oracle",
+               "sample": f"first {args.cpu_sample} scenarios of {args.config} (same splits the GPU evaluates)"}
+
+    if rank == 0:
+        tt = tot.cpu().numpy()
+        line = {
+            "metric": METRIC, "value": value, "unit": "scenario_evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg, args, count),
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "kernel": name_dom, "kernel_ms": avg_dom, "kernel_share_of_step": share,
+                         "flops_per_launch": flops_launch,
+                         "peak_note": f"FP64 (DFMA/DMMA shared pipe): {props.multi_processor_count} SMs x "
+                                      f"{FP64_FMA_PER_CLK_PER_SM} FMA/clk x 2 x {sm_max:.0f} MHz"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk_sum,
+            "accuracy": {"pooled_sign_accuracy_pct": 100.0 * tt[0] / max(tt[1], 1), "cases": int(tt[1]),
+                         "recommendations": int(tt[2]), "rec_hits": int(tt[3])},
+            "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in stats.items()},
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

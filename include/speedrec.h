@@ -141,7 +141,8 @@ typedef struct {
   int32_t learner;       /* SR_LINREG (ridge LS, reading D1); SR_IBK -> SR_E_UNSUPPORTED (NEXT-1) */
   int32_t max_count;     /* Tier-3 max recommendations, 3 */
   int32_t refine_steps;  /* iterative-refinement steps of the solve, 2 */
-  int32_t reserved;
+  int32_t debug_mcap;    /* 0 = auto; >0 caps the shared-memory Cholesky size so larger
+                            systems take the global-scratch path (tests only) */
   double ridge;          /* lambda, 1e-8 */
   double threshold;      /* recommend iff EX >= threshold, 1.05 (reading R8) */
   double clamp_floor;    /* EX <= 0 -> clamp_floor, 0.01 */
@@ -177,6 +178,9 @@ typedef struct {
   sr_scn_score* scn_scores; /* required: [count] */
   double* ex;               /* optional: [count][O][G*32] EX per (optimization, pair), 0 = not a predicted test case */
   int8_t* recs;             /* optional: [count][N][max_count] recommended ids per test slot, -1 padded */
+  int64_t* totals;          /* optional: [4] pooled over the range (A7 "per config"):
+                               sum n_correct, sum n_test, sum n_rec, sum n_rec_hit;
+                               pooled sign accuracy = 100 * totals[0] / totals[1] (Table 3) */
   int32_t on_device;        /* 0: host buffers (copied back, call is synchronous); 1: device buffers */
 } sr_outputs;
 
@@ -202,6 +206,7 @@ sr_status sr_synchronize(sr_ctx* ctx);
 sr_status sr_set_timing(sr_ctx* ctx, int32_t enable);
 int32_t sr_kernel_stats(sr_ctx* ctx, int32_t cap, const char** names, int32_t* launches,
                         double* ms);
+sr_status sr_reset_kernel_stats(sr_ctx* ctx); /* zero the accumulated counts and times */
 /* Kernels launched by the last sr_evaluate call. */
 int32_t sr_last_launch_count(const sr_ctx* ctx);
 

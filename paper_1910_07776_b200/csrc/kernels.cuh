@@ -1,0 +1,200 @@
+// kernels.cuh -- sm_100a kernels of the Tier-2/Tier-3 hot path of
+// arXiv 1910.07776 (see include/speedrec.h for the step list A0-A7 and
+// DESIGN.md §5-6 for the data layout and the roofline of each kernel).
+//
+// Design (B200-first):
+//  * k_rates / k_labels: elementwise FP64 IEEE divisions (A0, A1 labels),
+//    grid-stride, coalesced; bit-exact by construction.
+//  * k_eval_warp: one warp owns one scenario end to end (A1-A7): split
+//    membership from the counter-based hash, pair compaction by ballot,
+//    per-fit min-max statistics, the centred Gram (dual n x n when the fit is
+//    underdetermined, primal d x d otherwise) accumulated on the FP64 tensor
+//    pipe with mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), a packed warp Cholesky
+//    with rsqrt pivots, two refinement steps whose residual is formed from
+//    the data rows, prediction, clamping, warp-shuffle top-k ranking and the
+//    segmented score reduction.  No inter-warp synchronisation: a persistent
+//    grid of warps strides over scenarios.  The scenario's rate matrix is
+//    staged once per CTA in shared memory when it fits (C1, C3, C5).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace speedrec {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kMaxOpt = 16;
+constexpr int kMaxGroups = 64;
+constexpr int kMaxCounters = 128;
+constexpr int kMaxRec = 8;
+
+struct OptScore {
+  int32_t n_train, n_test, n_correct, n_clamped;
+  double sum_ratio, min_ratio, max_ratio;
+  uint64_t fp_train, fp_test;
+};
+struct ScnScore {
+  int32_t n_rec, n_rec_hit, n_untrained, n_guard;
+};
+
+// Per-warp shared-memory layout (byte offsets inside the warp's slab).
+struct WarpLayout {
+  int bytes;            // slab size (multiple of 16)
+  int off_trw, off_tew; // uint64 [G]
+  int off_gidx;         // int16 [G]   group -> index among test groups (-1)
+  int off_F;            // int16 [dmax] feature columns of the scenario
+  int off_ex;           // double [ex_cap]  EX per (o_idx, test group, k)
+  int off_excl;         // uint8 [ex_cap]   clamped flag
+  int ex_cap;
+  int off_trs;          // int32 [np_tr]  training before-slots
+  int off_try;          // double [np_tr] training labels
+  int off_tes;          // int32 [np_te]  test before-slots
+  int off_tek;          // int32 [np_te]  g*32+k of the test case
+  int off_tey;          // double [np_te] AC of the test case
+  int np_tr, np_te;
+  int off_col;          // int16 [dmax] active feature columns
+  int off_xb;           // double [dmax]
+  int off_s;            // double [dmax]
+  int off_w;            // double [dmax]  weights on scaled features
+  int off_u;            // double [dmax]  weights on raw centred features
+  int off_v1, off_v2, off_v3;  // double [vmax] solve vectors
+  int off_invd;         // double [vmax]
+  int vmax;
+  int off_M;            // double [mcap(mcap+1)/2] packed Cholesky factor
+  int mcap;
+};
+
+struct EvalArgs {
+  // dataset (device)
+  const double* x;       // rates [N][C]
+  const double* ylab;    // labels [G][O][32]
+  const int8_t* opt_bit; // [P][O]
+  int P, IR, C, O, G;
+  // scenario batch (device)
+  int kind;              // 0 groups, 1 loo, 2 random
+  int gw;                // group words
+  long long n_splits;
+  const uint64_t* train_g;
+  const uint64_t* test_g;
+  const uint32_t* split_om;
+  const int32_t* pool_list;   // pool groups ascending
+  int n_pool;
+  unsigned long long seed;
+  uint32_t opt_mask;
+  int subsets_k;
+  long long n_masks;
+  const uint64_t* fmasks;     // [n_masks][2] or null
+  // params
+  double lambda, threshold, clamp_floor, guard_tol;
+  int max_count, refine;
+  // range
+  long long first, count;
+  // outputs (device)
+  OptScore* opt_out;
+  ScnScore* scn_out;
+  double* ex_out;
+  int8_t* rec_out;
+  unsigned long long* totals;  // [4] or null
+  // workspace
+  WarpLayout L;
+  int warps_per_block;
+  int stage_x;           // 1: stage x [N][C] in smem with ld = ldxs
+  int ldxs;
+  int off_stage;         // byte offset of the staged x (after opt_bit table)
+  int off_warps;         // byte offset of the first warp slab
+  double* gscratch;      // per global warp: mscratch doubles for M overflow
+  long long mscratch;
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ int ins0(int k, int b) { return ((k >> b) << (b + 1)) | (k & ((1 << b) - 1)); }
+__device__ __forceinline__ int rmv(int v, int b) { return (v & ((1 << b) - 1)) | ((v >> (b + 1)) << b); }
+__device__ __forceinline__ int pk(int r, int c) { return ((r * (r + 1)) >> 1) + c; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_isum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_xor(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v ^= __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ bool near_tol(double a, double b, double tol) {
+  double s = fabs(a) > 1.0 ? fabs(a) : 1.0;
+  return fabs(a - b) <= tol * s;
+}
+// D(8x8) += A(8x4) * B(4x8), FP64 tensor pipe (SASS DMMA.8x8x4).
+// Lane l holds A[l>>2][l&3], B[l&3][l>>2], D[l>>2][2(l&3) + {0,1}].
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------- A0 / A1
+// x = counters / cycles, IEEE division => bit-exact with any
+// correctly rounded implementation.
+__global__ void k_rates(const double* __restrict__ counters, const double* __restrict__ cycles,
+                        double* __restrict__ x, long long n_slots, int C) {
+  long long total = n_slots * C;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = counters[i] / cycles[i / C];
+}
+
+// ylab[g][o][k] = rt[before] / rt[after] (reading D2), 0 when the
+// optimization is absent from the group's program.
+__global__ void k_labels(const double* __restrict__ rt, const int8_t* __restrict__ opt_bit,
+                         double* __restrict__ ylab, int G, int O, int IR) {
+  int total = G * O * 32;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    int k = i & 31, o = (i >> 5) % O, g = (i >> 5) / O;
+    int b = opt_bit[(g / IR) * O + o];
+    double y = 0.0;
+    if (b >= 0) {
+      int v = ins0(k, b);
+      y = rt[g * 64 + v] / rt[g * 64 + (v | (1 << b))];
+    }
+    ylab[i] = y;
+  }
+}
+
+// Validation of the Tier-1 input: first offending flat index.
+__global__ void k_validate(const double* __restrict__ counters, const double* __restrict__ cycles,
+                           const double* __restrict__ rt, long long n_slots, int C,
+                           unsigned long long* __restrict__ bad) {
+  long long total = n_slots * C;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    double c = counters[i];
+    if (!(c >= 0.0) || !isfinite(c)) atomicMin(&bad[0], (unsigned long long)i);
+    if (i < n_slots) {
+      double cy = cycles[i], r = rt[i];
+      if (!(cy > 0.0) || !isfinite(cy)) atomicMin(&bad[1], (unsigned long long)i);
+      if (!(r > 0.0) || !isfinite(r)) atomicMin(&bad[2], (unsigned long long)i);
+    }
+  }
+}
+
+}  // namespace speedrec

@@ -1,0 +1,663 @@
+// speedrec.cu -- runtime + C-ABI of the B200-native Tier-2/Tier-3 path of
+// arXiv 1910.07776.  The ABI is declared (with argument semantics, layout,
+// ownership and errors) in include/speedrec.h.  Everything numerical runs in
+// the kernels of kernels.cuh / eval_warp.cuh; this file validates arguments,
+// owns device memory, plans the launch (shared-memory layout, occupancy) and
+// accounts for launches and their live CUDA-event timing.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/speedrec.h"
+#include "eval_warp.cuh"
+#include "kernels.cuh"
+
+using namespace speedrec;
+
+static_assert(sizeof(sr_opt_score) == 56, "sr_opt_score layout");
+static_assert(sizeof(OptScore) == sizeof(sr_opt_score), "OptScore layout");
+static_assert(sizeof(ScnScore) == sizeof(sr_scn_score), "ScnScore layout");
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct KStat {
+  const char* name;
+  int launches = 0;
+  double ms = 0.0;
+};
+
+}  // namespace
+
+struct sr_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int sm_count = 0;
+  int max_smem_optin = 0;
+  // dataset
+  bool have_ds = false;
+  int P = 0, I = 0, R = 0, m = 0, C = 0, O = 0, G = 0;
+  long long N = 0;
+  DevBuf counters, cycles, runtime, opt_bit, x, ylab, bad;
+  std::vector<int8_t> h_opt_bit;
+  // scenarios
+  bool have_sc = false;
+  sr_scenarios sc{};
+  DevBuf train_g, test_g, split_om, pool_list, fmasks;
+  std::vector<uint64_t> h_train, h_test, h_fmasks;
+  std::vector<uint32_t> h_om;
+  std::vector<int32_t> h_pool;
+  int dmax = 0, np_tr = 0, np_te = 0, n_tg = 0, n_os = 0;
+  // scratch + outputs
+  DevBuf gscratch, out_opt, out_scn, out_ex, out_rec, out_tot;
+  // accounting
+  bool timing = false;
+  std::vector<KStat> kstats;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  int last_launches = 0;
+};
+
+namespace {
+
+sr_status fail(sr_ctx* c, sr_status st, const char* fmt, ...) {
+  static const char* names[] = {"SR_OK", "SR_E_ARG", "SR_E_DATA", "SR_E_LATTICE", "SR_E_EMPTY",
+                                "SR_E_STATE", "SR_E_OOM", "SR_E_CUDA", "SR_E_UNSUPPORTED"};
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = std::string(names[-(int)st]) + " " + buf;
+  return st;
+}
+
+#define CU(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) return fail(c, SR_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+sr_status ensure(sr_ctx* c, DevBuf& b, size_t bytes) {
+  if (b.bytes >= bytes && b.p) return SR_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  if (bytes == 0) return SR_OK;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, SR_E_OOM, "device allocation of %zu bytes: %s", bytes, cudaGetErrorString(e));
+  }
+  b.bytes = bytes;
+  return SR_OK;
+}
+
+void release(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+int kstat_id(sr_ctx* c, const char* name) {
+  for (size_t i = 0; i < c->kstats.size(); ++i)
+    if (c->kstats[i].name == name) return (int)i;
+  c->kstats.push_back(KStat{name, 0, 0.0});
+  return (int)c->kstats.size() - 1;
+}
+
+cudaEvent_t take_event(sr_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Bracket a launch with events when timing is on; count it always.
+template <typename F>
+sr_status launch(sr_ctx* c, const char* name, F&& f) {
+  const int id = kstat_id(c, name);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {
+    e0 = take_event(c);
+    e1 = take_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  f();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, SR_E_CUDA, "launch of %s: %s", name, cudaGetErrorString(e));
+  if (c->timing) {
+    cudaEventRecord(e1, c->stream);
+    c->pending.push_back({id, {e0, e1}});
+  }
+  c->kstats[id].launches++;
+  c->last_launches++;
+  return SR_OK;
+}
+
+void collect_timing(sr_ctx* c) {
+  for (auto& pe : c->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(pe.second.second);
+    cudaEventElapsedTime(&ms, pe.second.first, pe.second.second);
+    c->kstats[pe.first].ms += ms;
+    c->ev_pool.push_back(pe.second.first);
+    c->ev_pool.push_back(pe.second.second);
+  }
+  c->pending.clear();
+}
+
+int grid_for(const sr_ctx* c, long long work, int block) {
+  long long g = (work + block - 1) / block;
+  long long cap = (long long)c->sm_count * 8;
+  return (int)std::max(1LL, std::min(g, cap));
+}
+
+int align16(int x) { return (x + 15) & ~15; }
+
+}  // namespace
+
+extern "C" {
+
+const char* sr_version(void) { return "speedrec 0.1 (sm_100a)"; }
+
+sr_status sr_create(int32_t cuda_device, void* cuda_stream, sr_ctx** out) {
+  if (!out) return SR_E_ARG;
+  *out = nullptr;
+  sr_ctx* c = new sr_ctx();
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || cuda_device < 0 || cuda_device >= n) {
+    cudaGetLastError();
+    delete c;
+    return SR_E_CUDA;
+  }
+  c->device = cuda_device;
+  cudaSetDevice(cuda_device);
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
+  cudaDeviceGetAttribute(&c->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cuda_device);
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cuda_device);
+  if (major != 10) {
+    delete c;
+    return SR_E_UNSUPPORTED;
+  }
+  if (cuda_stream) {
+    c->stream = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      return SR_E_CUDA;
+    }
+    c->own_stream = true;
+  }
+  *out = c;
+  return SR_OK;
+}
+
+void sr_destroy(sr_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  collect_timing(c);
+  for (DevBuf* b : {&c->counters, &c->cycles, &c->runtime, &c->opt_bit, &c->x, &c->ylab, &c->bad,
+                    &c->train_g, &c->test_g, &c->split_om, &c->pool_list, &c->fmasks, &c->gscratch,
+                    &c->out_opt, &c->out_scn, &c->out_ex, &c->out_rec, &c->out_tot})
+    release(*b);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* sr_last_error(const sr_ctx* c) { return c ? c->err.c_str() : "SR_E_ARG null context"; }
+
+void sr_default_params(sr_params* p) {
+  if (!p) return;
+  p->learner = SR_LINREG;
+  p->max_count = 3;
+  p->refine_steps = 2;
+  p->debug_mcap = 0;
+  p->ridge = 1e-8;
+  p->threshold = 1.05;
+  p->clamp_floor = 0.01;
+  p->guard_tol = 1e-9;
+}
+
+sr_status sr_load_dataset(sr_ctx* c, const sr_dataset* d) {
+  if (!c) return SR_E_ARG;
+  c->err.clear();
+  if (!d || !d->counters || !d->cycles || !d->runtime_ms || !d->opt_bit)
+    return fail(c, SR_E_ARG, "dataset: null pointer");
+  if (d->n_programs <= 0 || d->n_inputs <= 0 || d->n_runs <= 0 || d->n_counters <= 0 || d->n_opt_ids <= 0)
+    return fail(c, SR_E_ARG, "dataset: non-positive size (P=%d I=%d R=%d C=%d O=%d)", d->n_programs,
+                d->n_inputs, d->n_runs, d->n_counters, d->n_opt_ids);
+  if (d->n_opt_bits != 6) return fail(c, SR_E_UNSUPPORTED, "dataset: n_opt_bits=%d (only 6)", d->n_opt_bits);
+  if (d->n_counters > kMaxCounters) return fail(c, SR_E_UNSUPPORTED, "dataset: n_counters=%d > 128", d->n_counters);
+  if (d->n_opt_ids > kMaxOpt) return fail(c, SR_E_UNSUPPORTED, "dataset: n_opt_ids=%d > 16", d->n_opt_ids);
+  cudaSetDevice(c->device);
+  const long long G = (long long)d->n_programs * d->n_inputs * d->n_runs;
+  const long long N = G * 64;
+  const int C = d->n_counters, O = d->n_opt_ids, P = d->n_programs;
+  sr_status st;
+  if ((st = ensure(c, c->counters, N * C * 8)) || (st = ensure(c, c->cycles, N * 8)) ||
+      (st = ensure(c, c->runtime, N * 8)) || (st = ensure(c, c->opt_bit, (size_t)P * O)) ||
+      (st = ensure(c, c->x, N * C * 8)) || (st = ensure(c, c->ylab, G * O * 32 * 8)) ||
+      (st = ensure(c, c->bad, 3 * 8)))
+    return st;
+  // opt_bit is small: validate on host (copy first when it lives on device)
+  c->h_opt_bit.assign((size_t)P * O, 0);
+  cudaMemcpyKind k = d->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CU(cudaMemcpyAsync(c->counters.p, d->counters, N * C * 8, k, c->stream));
+  CU(cudaMemcpyAsync(c->cycles.p, d->cycles, N * 8, k, c->stream));
+  CU(cudaMemcpyAsync(c->runtime.p, d->runtime_ms, N * 8, k, c->stream));
+  CU(cudaMemcpyAsync(c->h_opt_bit.data(), d->opt_bit, (size_t)P * O,
+                     d->on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (int p = 0; p < P; ++p) {
+    unsigned seen = 0;
+    for (int o = 0; o < O; ++o) {
+      int b = c->h_opt_bit[(size_t)p * O + o];
+      if (b < -1 || b >= 6) return fail(c, SR_E_LATTICE, "program %d optimization %d: bit %d out of range", p, o, b);
+      if (b >= 0) {
+        if (seen & (1u << b)) return fail(c, SR_E_LATTICE, "program %d: bit %d used by two optimizations", p, b);
+        seen |= 1u << b;
+      }
+    }
+  }
+  CU(cudaMemcpyAsync(c->opt_bit.p, c->h_opt_bit.data(), (size_t)P * O, cudaMemcpyHostToDevice, c->stream));
+  unsigned long long init[3] = {~0ull, ~0ull, ~0ull};
+  CU(cudaMemcpyAsync(c->bad.p, init, sizeof init, cudaMemcpyHostToDevice, c->stream));
+  c->have_ds = false;
+  c->last_launches = 0;
+  sr_status ls = launch(c, "k_validate", [&] {
+    k_validate<<<grid_for(c, N * C, 256), 256, 0, c->stream>>>(
+        (const double*)c->counters.p, (const double*)c->cycles.p, (const double*)c->runtime.p, N, C,
+        (unsigned long long*)c->bad.p);
+  });
+  if (ls) return ls;
+  unsigned long long bad[3];
+  CU(cudaMemcpyAsync(bad, c->bad.p, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  collect_timing(c);
+  if (bad[0] != ~0ull)
+    return fail(c, SR_E_DATA, "slot %llu counter %llu: negative or non-finite count", bad[0] / C, bad[0] % C);
+  if (bad[1] != ~0ull) return fail(c, SR_E_DATA, "slot %llu: cycles must be > 0 and finite", bad[1]);
+  if (bad[2] != ~0ull) return fail(c, SR_E_DATA, "slot %llu: runtime_ms must be > 0 and finite", bad[2]);
+  c->P = P;
+  c->I = d->n_inputs;
+  c->R = d->n_runs;
+  c->m = 6;
+  c->C = C;
+  c->O = O;
+  c->G = (int)G;
+  c->N = N;
+  c->have_ds = true;
+  c->have_sc = false;
+  return SR_OK;
+}
+
+sr_status sr_define_scenarios(sr_ctx* c, const sr_scenarios* s, int64_t* n_scenarios) {
+  if (!c) return SR_E_ARG;
+  c->err.clear();
+  if (!c->have_ds) return fail(c, SR_E_STATE, "define_scenarios: no dataset loaded");
+  if (!s || !n_scenarios) return fail(c, SR_E_ARG, "define_scenarios: null pointer");
+  const int G = c->G, gw = (G + 63) / 64;
+  if (s->kind < 0 || s->kind > 2) return fail(c, SR_E_ARG, "scenarios: kind %d", s->kind);
+  if (s->n_splits <= 0 || s->n_masks <= 0) return fail(c, SR_E_ARG, "scenarios: n_splits/n_masks must be > 0");
+  if (s->group_words != gw) return fail(c, SR_E_ARG, "scenarios: group_words=%d, expected %d", s->group_words, gw);
+  if (G > kMaxGroups) return fail(c, SR_E_UNSUPPORTED, "scenarios: %d groups > %d", G, kMaxGroups);
+  if (s->all_subsets_k < 0 || s->all_subsets_k > 20 || s->all_subsets_k > c->C)
+    return fail(c, SR_E_ARG, "scenarios: all_subsets_k=%d", s->all_subsets_k);
+  if (s->all_subsets_k > 0 && s->n_masks != (1LL << s->all_subsets_k))
+    return fail(c, SR_E_ARG, "scenarios: n_masks must be 2^all_subsets_k");
+  if (s->all_subsets_k == 0 && s->n_masks > 1 && !s->feature_masks)
+    return fail(c, SR_E_ARG, "scenarios: n_masks > 1 needs feature_masks");
+  const uint32_t valid_ids = (c->O >= 32) ? ~0u : ((1u << c->O) - 1u);
+  cudaSetDevice(c->device);
+  sr_status st;
+  c->sc = *s;
+  int np_tr = 0, np_te = 0, n_tg = 0, n_os = 0;
+  if (s->kind == SR_SPLIT_GROUPS) {
+    if (!s->train_groups || !s->test_groups) return fail(c, SR_E_ARG, "scenarios: GROUPS needs train/test group sets");
+    const size_t nw = (size_t)s->n_splits * gw;
+    c->h_train.assign(s->train_groups, s->train_groups + nw);
+    c->h_test.assign(s->test_groups, s->test_groups + nw);
+    for (long long k = 0; k < s->n_splits; ++k) {
+      int a = 0, b = 0;
+      for (int w = 0; w < gw; ++w) {
+        uint64_t lim = (w == gw - 1 && G % 64) ? ((1ull << (G % 64)) - 1) : ~0ull;
+        if ((c->h_train[k * gw + w] & ~lim) || (c->h_test[k * gw + w] & ~lim))
+          return fail(c, SR_E_ARG, "split %lld: group bit beyond G=%d", k, G);
+        a += __builtin_popcountll(c->h_train[k * gw + w]);
+        b += __builtin_popcountll(c->h_test[k * gw + w]);
+      }
+      if (b == 0) return fail(c, SR_E_EMPTY, "split %lld: no test group", k);
+      np_tr = std::max(np_tr, 32 * a);
+      np_te = std::max(np_te, 32 * b);
+      n_tg = std::max(n_tg, b);
+    }
+    if ((st = ensure(c, c->train_g, nw * 8)) || (st = ensure(c, c->test_g, nw * 8))) return st;
+    CU(cudaMemcpyAsync(c->train_g.p, c->h_train.data(), nw * 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->test_g.p, c->h_test.data(), nw * 8, cudaMemcpyHostToDevice, c->stream));
+  } else if (s->kind == SR_SPLIT_LOO) {
+    if (!s->pool_groups) return fail(c, SR_E_ARG, "scenarios: LOO needs pool_groups");
+    c->h_pool.clear();
+    for (int g = 0; g < G; ++g)
+      if ((s->pool_groups[g >> 6] >> (g & 63)) & 1ull) c->h_pool.push_back(g);
+    if (c->h_pool.empty()) return fail(c, SR_E_EMPTY, "scenarios: LOO pool is empty");
+    if (s->n_splits > (long long)c->h_pool.size() * 64)
+      return fail(c, SR_E_EMPTY, "scenarios: split %lld beyond the %zu pool slots", (long long)s->n_splits - 1,
+                  c->h_pool.size() * 64);
+    np_tr = 32 * (int)c->h_pool.size();
+    np_te = 32;
+    n_tg = 1;
+    if ((st = ensure(c, c->pool_list, c->h_pool.size() * 4))) return st;
+    CU(cudaMemcpyAsync(c->pool_list.p, c->h_pool.data(), c->h_pool.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    np_tr = np_te = 32 * G;
+    n_tg = G;
+  }
+  if (s->split_opt_masks) {
+    if (s->kind != SR_SPLIT_GROUPS) return fail(c, SR_E_ARG, "scenarios: split_opt_masks only for GROUPS");
+    c->h_om.assign(s->split_opt_masks, s->split_opt_masks + s->n_splits);
+    for (uint32_t mk : c->h_om) n_os = std::max(n_os, __builtin_popcount(mk & valid_ids));
+    if ((st = ensure(c, c->split_om, c->h_om.size() * 4))) return st;
+    CU(cudaMemcpyAsync(c->split_om.p, c->h_om.data(), c->h_om.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    n_os = __builtin_popcount(s->opt_mask & valid_ids);
+  }
+  int dmax = c->C;
+  if (s->all_subsets_k > 0) {
+    dmax = s->all_subsets_k;
+  } else if (s->feature_masks) {
+    c->h_fmasks.assign(s->feature_masks, s->feature_masks + 2 * s->n_masks);
+    dmax = 0;
+    for (long long f = 0; f < s->n_masks; ++f) {
+      uint64_t m0 = c->h_fmasks[2 * f], m1 = c->h_fmasks[2 * f + 1];
+      if (c->C < 64) m0 &= (1ull << c->C) - 1;
+      if (c->C <= 64) m1 = 0;
+      else if (c->C < 128) m1 &= (1ull << (c->C - 64)) - 1;
+      dmax = std::max(dmax, __builtin_popcountll(m0) + __builtin_popcountll(m1));
+    }
+    if ((st = ensure(c, c->fmasks, c->h_fmasks.size() * 8))) return st;
+    CU(cudaMemcpyAsync(c->fmasks.p, c->h_fmasks.data(), c->h_fmasks.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  c->dmax = std::max(dmax, 1);
+  c->np_tr = std::max(np_tr, 32);
+  c->np_te = std::max(np_te, 32);
+  c->n_tg = std::max(n_tg, 1);
+  c->n_os = std::max(n_os, 1);
+  c->have_sc = true;
+  *n_scenarios = s->n_splits * s->n_masks;
+  return SR_OK;
+}
+
+namespace {
+
+// Shared-memory plan of k_eval_warp for the current batch.
+WarpLayout plan_layout(const sr_ctx* c, int mcap) {
+  WarpLayout L{};
+  int off = 0;
+  auto take = [&](int bytes) {
+    int o = off;
+    off = align16(off + bytes);
+    return o;
+  };
+  const int G = c->G, d = c->dmax, vmax = std::max(c->np_tr, d);
+  L.off_trw = take(8 * G);
+  L.off_tew = take(8 * G);
+  L.off_gidx = take(2 * G);
+  L.off_F = take(2 * d);
+  L.ex_cap = c->n_os * c->n_tg * 32;
+  L.off_ex = take(8 * L.ex_cap);
+  L.off_excl = take(L.ex_cap);
+  L.np_tr = c->np_tr;
+  L.np_te = c->np_te;
+  L.off_trs = take(4 * c->np_tr);
+  L.off_try = take(8 * c->np_tr);
+  L.off_tes = take(4 * c->np_te);
+  L.off_tek = take(4 * c->np_te);
+  L.off_tey = take(8 * c->np_te);
+  L.off_col = take(2 * d);
+  L.off_xb = take(8 * d);
+  L.off_s = take(8 * d);
+  L.off_w = take(8 * d);
+  L.off_u = take(8 * d);
+  L.vmax = vmax;
+  L.off_v1 = take(8 * vmax);
+  L.off_v2 = take(8 * vmax);
+  L.off_v3 = take(8 * vmax);
+  L.off_invd = take(8 * vmax);
+  L.mcap = mcap;
+  L.off_M = take(8 * (mcap * (mcap + 1) / 2));
+  L.bytes = align16(off);
+  return L;
+}
+
+}  // namespace
+
+sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t count, sr_outputs* out) {
+  if (!c) return SR_E_ARG;
+  c->err.clear();
+  if (!c->have_ds || !c->have_sc) return fail(c, SR_E_STATE, "evaluate: dataset and scenarios must be defined first");
+  if (!prm || !out || !out->opt_scores || !out->scn_scores) return fail(c, SR_E_ARG, "evaluate: null pointer");
+  const long long total = c->sc.n_splits * c->sc.n_masks;
+  if (first < 0 || count < 0 || first + count > total)
+    return fail(c, SR_E_ARG, "evaluate: range [%lld, %lld) outside [0, %lld)", (long long)first,
+                (long long)(first + count), total);
+  if (prm->learner != SR_LINREG) return fail(c, SR_E_UNSUPPORTED, "evaluate: learner %d (IBK is NEXT-1)", prm->learner);
+  if (prm->max_count < 1 || prm->max_count > kMaxRec) return fail(c, SR_E_ARG, "evaluate: max_count=%d", prm->max_count);
+  if (prm->refine_steps < 0 || prm->refine_steps > 8) return fail(c, SR_E_ARG, "evaluate: refine_steps=%d", prm->refine_steps);
+  if (!(prm->ridge > 0.0)) return fail(c, SR_E_ARG, "evaluate: ridge must be > 0");
+  cudaSetDevice(c->device);
+  c->last_launches = 0;
+  const int G = c->G, O = c->O, C = c->C;
+  const long long N = c->N;
+  sr_status st;
+
+  // ---- A0 + A1 labels (per call: part of the step) ----
+  if ((st = launch(c, "k_rates", [&] {
+         k_rates<<<grid_for(c, N * C, 256), 256, 0, c->stream>>>((const double*)c->counters.p,
+                                                                 (const double*)c->cycles.p,
+                                                                 (double*)c->x.p, N, C);
+       })))
+    return st;
+  if ((st = launch(c, "k_labels", [&] {
+         k_labels<<<grid_for(c, (long long)G * O * 32, 256), 256, 0, c->stream>>>(
+             (const double*)c->runtime.p, (const int8_t*)c->opt_bit.p, (double*)c->ylab.p, G, O,
+             c->I * c->R);
+       })))
+    return st;
+  if (count == 0) return SR_OK;
+
+  // ---- plan k_eval_warp ----
+  const int budget = c->max_smem_optin;                  // 232448 on B200
+  const int head = align16(c->P * O);
+  const int ldxs = C | 1;
+  const long long stage_bytes = N * ldxs * 8;
+  const int mmax = std::min(c->np_tr, c->dmax + 1);      // largest system any fit can need
+  int stage = stage_bytes <= 96 * 1024 ? 1 : 0;
+  int mcap = std::min(mmax, 32);
+  if (prm->debug_mcap > 0) mcap = std::min(mcap, prm->debug_mcap);
+  WarpLayout L = plan_layout(c, mcap);
+  int avail = budget - head - (stage ? align16((int)stage_bytes) : 0);
+  int wpb = std::min(16, avail / std::max(L.bytes, 1));
+  while (wpb < 4 && mcap > 8 && prm->debug_mcap == 0) {
+    mcap /= 2;
+    L = plan_layout(c, mcap);
+    wpb = std::min(16, avail / L.bytes);
+  }
+  if (wpb < 1 && stage) {
+    stage = 0;
+    avail = budget - head;
+    wpb = std::min(16, avail / L.bytes);
+  }
+  if (wpb < 1) return fail(c, SR_E_UNSUPPORTED, "evaluate: per-warp workspace %d B exceeds shared memory", L.bytes);
+  const long long mscr = (mmax > mcap) ? (long long)mmax * (mmax + 1) / 2 : 0;
+
+  EvalArgs A{};
+  A.x = (const double*)c->x.p;
+  A.ylab = (const double*)c->ylab.p;
+  A.opt_bit = (const int8_t*)c->opt_bit.p;
+  A.P = c->P;
+  A.IR = c->I * c->R;
+  A.C = C;
+  A.O = O;
+  A.G = G;
+  A.kind = c->sc.kind;
+  A.gw = (G + 63) / 64;
+  A.n_splits = c->sc.n_splits;
+  A.train_g = (const uint64_t*)c->train_g.p;
+  A.test_g = (const uint64_t*)c->test_g.p;
+  A.split_om = c->sc.split_opt_masks ? (const uint32_t*)c->split_om.p : nullptr;
+  A.pool_list = (const int32_t*)c->pool_list.p;
+  A.n_pool = (int)c->h_pool.size();
+  A.seed = c->sc.seed;
+  A.opt_mask = c->sc.opt_mask;
+  A.subsets_k = c->sc.all_subsets_k;
+  A.n_masks = c->sc.n_masks;
+  A.fmasks = (c->sc.feature_masks && c->sc.all_subsets_k == 0) ? (const uint64_t*)c->fmasks.p : nullptr;
+  A.lambda = prm->ridge;
+  A.threshold = prm->threshold;
+  A.clamp_floor = prm->clamp_floor;
+  A.guard_tol = prm->guard_tol;
+  A.max_count = prm->max_count;
+  A.refine = prm->refine_steps;
+  A.first = first;
+  A.count = count;
+  A.L = L;
+  A.warps_per_block = wpb;
+  A.stage_x = stage;
+  A.ldxs = ldxs;
+  A.off_stage = head;
+  A.off_warps = head + (stage ? align16((int)stage_bytes) : 0);
+  const int smem = A.off_warps + wpb * L.bytes;
+  const int cmax = c->n_os <= 8 ? 8 : 16;
+  auto kern = cmax == 8 ? k_eval_warp<8> : k_eval_warp<16>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem));
+  per_sm = std::max(per_sm, 1);
+  long long blocks = std::min<long long>((long long)c->sm_count * per_sm, (count + wpb - 1) / wpb);
+  blocks = std::max(1LL, blocks);
+  const long long nwarps = blocks * wpb;
+  if (mscr > 0) {
+    if ((st = ensure(c, c->gscratch, (size_t)(nwarps * mscr * 8)))) return st;
+    A.gscratch = (double*)c->gscratch.p;
+    A.mscratch = mscr;
+  }
+
+  // ---- outputs ----
+  const size_t b_opt = (size_t)count * O * sizeof(sr_opt_score), b_scn = (size_t)count * sizeof(sr_scn_score);
+  const size_t b_ex = (size_t)count * O * G * 32 * 8, b_rec = (size_t)count * N * prm->max_count;
+  if (out->on_device) {
+    A.opt_out = (OptScore*)out->opt_scores;
+    A.scn_out = (ScnScore*)out->scn_scores;
+    A.ex_out = out->ex;
+    A.rec_out = out->recs;
+    A.totals = (unsigned long long*)out->totals;
+  } else {
+    if ((st = ensure(c, c->out_opt, b_opt)) || (st = ensure(c, c->out_scn, b_scn))) return st;
+    A.opt_out = (OptScore*)c->out_opt.p;
+    A.scn_out = (ScnScore*)c->out_scn.p;
+    if (out->ex) {
+      if ((st = ensure(c, c->out_ex, b_ex))) return st;
+      A.ex_out = (double*)c->out_ex.p;
+    }
+    if (out->recs) {
+      if ((st = ensure(c, c->out_rec, b_rec))) return st;
+      A.rec_out = (int8_t*)c->out_rec.p;
+    }
+    if (out->totals) {
+      if ((st = ensure(c, c->out_tot, 32))) return st;
+      A.totals = (unsigned long long*)c->out_tot.p;
+    }
+  }
+  if (A.totals) CU(cudaMemsetAsync(A.totals, 0, 32, c->stream));
+  if ((st = launch(c, "k_eval_warp", [&] {
+         kern<<<(unsigned)blocks, wpb * 32, smem, c->stream>>>(A);
+       })))
+    return st;
+  if (!out->on_device) {
+    CU(cudaMemcpyAsync(out->opt_scores, c->out_opt.p, b_opt, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(out->scn_scores, c->out_scn.p, b_scn, cudaMemcpyDeviceToHost, c->stream));
+    if (out->ex) CU(cudaMemcpyAsync(out->ex, c->out_ex.p, b_ex, cudaMemcpyDeviceToHost, c->stream));
+    if (out->recs) CU(cudaMemcpyAsync(out->recs, c->out_rec.p, b_rec, cudaMemcpyDeviceToHost, c->stream));
+    if (out->totals) CU(cudaMemcpyAsync(out->totals, c->out_tot.p, 32, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+  }
+  return SR_OK;
+}
+
+sr_status sr_rates(sr_ctx* c, double* x_out, int32_t on_device) {
+  if (!c) return SR_E_ARG;
+  c->err.clear();
+  if (!c->have_ds) return fail(c, SR_E_STATE, "rates: no dataset loaded");
+  if (!x_out) return fail(c, SR_E_ARG, "rates: null output");
+  cudaSetDevice(c->device);
+  c->last_launches = 0;
+  const long long N = c->N;
+  const int C = c->C;
+  sr_status st = launch(c, "k_rates", [&] {
+    k_rates<<<grid_for(c, N * C, 256), 256, 0, c->stream>>>((const double*)c->counters.p,
+                                                            (const double*)c->cycles.p, (double*)c->x.p, N, C);
+  });
+  if (st) return st;
+  CU(cudaMemcpyAsync(x_out, c->x.p, N * C * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return SR_OK;
+}
+
+sr_status sr_synchronize(sr_ctx* c) {
+  if (!c) return SR_E_ARG;
+  cudaSetDevice(c->device);
+  CU(cudaStreamSynchronize(c->stream));
+  return SR_OK;
+}
+
+sr_status sr_set_timing(sr_ctx* c, int32_t enable) {
+  if (!c) return SR_E_ARG;
+  c->timing = enable != 0;
+  return SR_OK;
+}
+
+int32_t sr_kernel_stats(sr_ctx* c, int32_t cap, const char** names, int32_t* launches, double* ms) {
+  if (!c) return (int32_t)SR_E_ARG;
+  cudaSetDevice(c->device);
+  collect_timing(c);
+  const int n = (int)c->kstats.size();
+  for (int i = 0; i < n && i < cap; ++i) {
+    if (names) names[i] = c->kstats[i].name;
+    if (launches) launches[i] = c->kstats[i].launches;
+    if (ms) ms[i] = c->kstats[i].ms;
+  }
+  return n;
+}
+
+sr_status sr_reset_kernel_stats(sr_ctx* c) {
+  if (!c) return SR_E_ARG;
+  cudaSetDevice(c->device);
+  collect_timing(c);
+  for (auto& k : c->kstats) k.launches = 0, k.ms = 0.0;
+  return SR_OK;
+}
+
+int32_t sr_last_launch_count(const sr_ctx* c) { return c ? c->last_launches : (int32_t)SR_E_ARG; }
+
+}  // extern "C"

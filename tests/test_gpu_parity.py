@@ -1,0 +1,175 @@
+"""GPU parity: the CUDA path through the C-ABI vs the oracle, element by element.
+
+Sizes: the small configs completely (C1 64, C2 240 scenarios), C3/C5 at sizes
+the oracle finishes in seconds that still span many warps/CTAs and a ragged
+tail, and the FULL bench configuration (C3, 1e6 splits, the same launch as
+bench.py) on sampled scenarios the oracle computes one by one.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from tests.parity import compare
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def Context():
+    from paper_1910_07776_b200 import Context as C
+    return C
+
+
+def _run(Context, cfg, first, count, params=None, **kw):
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    from paper_1910_07776_b200 import default_params
+    p = default_params(**(params or {}))
+    got = ctx.evaluate(first, count, params=p, want_ex=True, want_recs=True)
+    ctx.close()
+    ref = oracle.evaluate(cfg.dataset, cfg.scenarios, first, count, want_ex=True, want_recs=True, **kw)
+    return got, ref
+
+
+def test_rates_bit_exact(Context):
+    for name in ("C1", "C2", "C3"):
+        cfg = gen.make_config(name, n_splits=8)
+        ctx = Context(0)
+        ctx.load(cfg.dataset)
+        x = ctx.rates()
+        ctx.close()
+        assert np.array_equal(x, oracle.rates(cfg.dataset.counters, cfg.dataset.cycles))
+
+
+def test_c1_all(Context):
+    cfg = gen.make_config("C1")
+    got, ref = _run(Context, cfg, 0, 64)
+    st = compare(got, ref, max_guard_frac=0.05)
+    print("C1", st)
+
+
+def test_c2_all_table2(Context):
+    cfg = gen.make_config("C2")
+    got, ref = _run(Context, cfg, 0, 240)
+    st = compare(got, ref, max_guard_frac=0.05)
+    print("C2", st)
+
+
+def test_c3_small_ragged(Context):
+    cfg = gen.make_config("C3", n_splits=3001)
+    got, ref = _run(Context, cfg, 0, 3001)
+    print("C3", compare(got, ref))
+    got, ref = _run(Context, cfg, 1234, 77)         # ragged sub-range
+    compare(got, ref)
+
+
+def test_c5_small_masks(Context):
+    cfg = gen.make_config("C5", n_masks_k=5)        # 32 masks x 128 folds
+    n = cfg.scenarios.n_scenarios
+    got, ref = _run(Context, cfg, 0, n)
+    print("C5k5", compare(got, ref))
+
+
+def test_global_scratch_path(Context):
+    # Force the Cholesky factor out of shared memory (debug_mcap=8): same results.
+    for name, n in (("C3", 500), ("C2", 240), ("C1", 64)):
+        cfg = gen.make_config(name, n_splits=n)
+        got, ref = _run(Context, cfg, 0, min(n, cfg.scenarios.n_scenarios), params=dict(debug_mcap=8))
+        compare(got, ref, max_guard_frac=0.05)
+
+
+def test_degenerate_inputs(Context):
+    # constant counters (d_eff = 0 -> EX = mean label), zero counters, a
+    # single feature, and feature masks selecting nothing
+    cfg = gen.make_config("C1")
+    ds = cfg.dataset
+    ds.counters[:, :8] = ds.cycles[:, None] * 0.25   # constant rates -> inactive features
+    ds.counters[:, 8:16] = 0.0                       # all-zero features -> inactive
+    sc = cfg.scenarios
+    got, ref = _run(Context, cfg, 0, 64)
+    compare(got, ref, max_guard_frac=0.05)
+    sc.feature_masks = np.array([[0, 0], [1 << 20, 0], [0xFFFF0000, 0]], dtype=np.uint64)
+    sc.n_masks = 3
+    got, ref = _run(Context, cfg, 0, 64 * 3)
+    compare(got, ref, max_guard_frac=0.05)
+
+
+def test_determinism_and_sharding_invariance(Context):
+    cfg = gen.make_config("C3", n_splits=4000)
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    a = ctx.evaluate(0, 4000)
+    b = ctx.evaluate(0, 4000)
+    parts = [ctx.evaluate(k * 1000, 1000) for k in range(4)]
+    ctx.close()
+    assert a["opt"].tobytes() == b["opt"].tobytes() and a["scn"].tobytes() == b["scn"].tobytes()
+    assert np.concatenate([p["opt"] for p in parts]).tobytes() == a["opt"].tobytes()
+    assert np.concatenate([p["scn"] for p in parts]).tobytes() == a["scn"].tobytes()
+
+
+def test_c3_full_size_sampled(Context):
+    """Full bench workload (C3, 1e6 splits) in the bench's launch; sampled rows
+    checked against the oracle one by one."""
+    import torch
+    from paper_1910_07776_b200.speedrec import OPT_SCORE_DTYPE, SCN_SCORE_DTYPE
+    cfg = gen.make_config("C3")
+    S = cfg.scenarios.n_scenarios
+    ctx = Context(0, stream=torch.cuda.current_stream().cuda_stream)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    O = cfg.dataset.n_opt_ids
+    dopt = torch.empty(S * O * OPT_SCORE_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    dscn = torch.empty(S * SCN_SCORE_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    ctx.evaluate(0, S, out=dict(opt=dopt, scn=dscn))
+    torch.cuda.synchronize()
+    opt = dopt.cpu().numpy().view(OPT_SCORE_DTYPE).reshape(S, O)
+    scn = dscn.cpu().numpy().view(SCN_SCORE_DTYPE)
+    ctx.close()
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.r_[0, S - 1, rng.integers(0, S, size=300)])
+    ref_opt, ref_scn = [], []
+    for s in idx:
+        r = oracle.evaluate(cfg.dataset, cfg.scenarios, int(s), 1, n_threads=1)
+        ref_opt.append(r["opt"])
+        ref_scn.append(r["scn"])
+    st = compare(dict(opt=opt[idx], scn=scn[idx]),
+                 dict(opt=np.concatenate(ref_opt), scn=np.concatenate(ref_scn)))
+    print("C3 full sampled", st)
+    # properties at full size: counts conservation of the 2^6 lattice
+    assert (opt["n_test"].sum(1) <= 6 * 64).all()
+    assert (scn["n_rec"] <= 3 * 128).all()
+
+
+def test_errors_name_the_entity(Context):
+    from paper_1910_07776_b200 import SpeedrecError, default_params
+    from paper_1910_07776_b200 import speedrec as S
+    cfg = gen.make_config("C1")
+    ctx = Context(0)
+    with pytest.raises(SpeedrecError) as e:
+        ctx.evaluate(0, 1)
+    assert e.value.status == S.SR_E_STATE or ctx.shape is None
+    ds = cfg.dataset
+    bad = ds.cycles.copy()
+    bad[17] = 0.0
+    with pytest.raises(SpeedrecError) as e:
+        ctx.load_dataset(1, 1, 1, ds.n_counters, ds.n_opt_ids, ds.counters, bad, ds.runtime_ms, ds.opt_bit)
+    assert e.value.status == S.SR_E_DATA and "slot 17" in str(e.value)
+    ob = ds.opt_bit.copy()
+    ob[0, 1] = ob[0, 0]
+    with pytest.raises(SpeedrecError) as e:
+        ctx.load_dataset(1, 1, 1, ds.n_counters, ds.n_opt_ids, ds.counters, ds.cycles, ds.runtime_ms, ob)
+    assert e.value.status == S.SR_E_LATTICE
+    ctx.load(ds)
+    ctx.define_scenarios(cfg.scenarios)
+    with pytest.raises(SpeedrecError) as e:
+        ctx.evaluate(60, 10)
+    assert e.value.status == S.SR_E_ARG
+    with pytest.raises(SpeedrecError) as e:
+        ctx.evaluate(0, 1, params=default_params(learner=1))
+    assert e.value.status == S.SR_E_UNSUPPORTED
+    r = ctx.evaluate(0, 0)                           # empty batch is valid
+    assert r["opt"].shape[0] == 0
+    ctx.close()
