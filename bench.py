@@ -33,15 +33,19 @@ FP64_FMA_PER_CLK_PER_SM = 64   # inferred from the measured DMMA 
 def fit_flops(n: np.ndarray, t: np.ndarray, d: int, refine: int = 2) -> float:
     """Algorithmic FP64 flops of the fits a batch performed:
     per fit with n training pairs, t test cases and d active features,
-      dual   (n-1 < d): n(n+1)/2*d + n^3/6 + refine*(2nd + n^2) + nd + td   FMA
-      primal (else)   : n*d(d+1)/2 + d^3/6 + nd + refine*(2nd + d^2) + td  FMA
-    flop = 2 * FMA.  Fits with n == 0 or t == 0 do no work."""
+      dual   (n-1 < d): n(n+1)/2*d + n^3/6 + n^2 + R*(2nd + n^2) + nd + td   FMA
+      primal (else)   : n*d(d+1)/2 + d^3/6 + nd + d^2 + R*(2nd + d^2) + td   FMA
+    R = refine when the fit's conditioning rule asks for it (dual: 2(n-1) >= d,
+    primal: n-1 < 2d), else 0.  flop = 2 * FMA.  Fits with
+    n == 0 or t == 0 do no work."""
     n = n.astype(np.float64)
     t = t.astype(np.float64)
     live = (n > 0) & (t > 0)
     dual = (n - 1) < d
-    fd = n * (n + 1) / 2 * d + n ** 3 / 6 + refine * (2 * n * d + n ** 2) + n * d + t * d
-    fp = n * d * (d + 1) / 2 + d ** 3 / 6 + n * d + refine * (2 * n * d + d ** 2) + t * d
+    rd = np.where(2 * (n - 1) >= d, refine, 0)
+    rp = np.where((n - 1) < 2 * d, refine, 0)
+    fd = n * (n + 1) / 2 * d + n ** 3 / 6 + n ** 2 + rd * (2 * n * d + n ** 2) + n * d + t * d
+    fp = n * d * (d + 1) / 2 + d ** 3 / 6 + n * d + d ** 2 + rp * (2 * n * d + d ** 2) + t * d
     return float(2.0 * np.where(live, np.where(dual, fd, fp), 0.0).sum())
 
 
@@ -167,7 +171,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1910_07776_b200 import Context
     from paper_1910_07776_b200.speedrec import OPT_SCORE_DTYPE, SCN_SCORE_DTYPE
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=local)      # one explicit stream for the library and the events
+    torch.cuda.set_stream(stream)
     ctx = Context(local, stream=stream.cuda_stream)
     ds = cfg.dataset
     ctx.load(ds)

@@ -147,6 +147,8 @@ typedef struct {
   double threshold;      /* recommend iff EX >= threshold, 1.05 (reading R8) */
   double clamp_floor;    /* EX <= 0 -> clamp_floor, 0.01 */
   double guard_tol;      /* guard band for n_guard, 1e-9 (reading R21) */
+  int32_t top_k;         /* masks kept by the mask ranking, 64, <= 512 */
+  int32_t pad_;
 } sr_params;
 
 void sr_default_params(sr_params* out);
@@ -173,6 +175,11 @@ typedef struct {
   int32_t n_guard;     /* decisions within guard_tol of a boundary (reading R21) */
 } sr_scn_score;      /* 16 bytes */
 
+/* Per feature mask, summed over all folds (splits) of the mask (A7, C5). */
+typedef struct {
+  int32_t n_correct, n_test, n_rec, n_rec_hit;
+} sr_mask_score;     /* 16 bytes */
+
 typedef struct {
   sr_opt_score* opt_scores; /* required: [count][O] */
   sr_scn_score* scn_scores; /* required: [count] */
@@ -181,6 +188,11 @@ typedef struct {
   int64_t* totals;          /* optional: [4] pooled over the range (A7 "per config"):
                                sum n_correct, sum n_test, sum n_rec, sum n_rec_hit;
                                pooled sign accuracy = 100 * totals[0] / totals[1] (Table 3) */
+  sr_mask_score* mask_scores; /* optional: [count / n_splits] per feature mask, summed over its folds */
+  int64_t* top_masks;       /* optional: [params.top_k] mask ids ranked by (sum n_correct desc, id asc),
+                               -1 padded.  Either of these two switches
+                               the call to mask aggregation: first and count must then be multiples of
+                               n_splits, and opt_scores / scn_scores may be NULL (not materialised). */
   int32_t on_device;        /* 0: host buffers (copied back, call is synchronous); 1: device buffers */
 } sr_outputs;
 

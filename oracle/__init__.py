@@ -151,6 +151,31 @@ def sign_correct(ex: float, ac: float) -> bool:
     return bool(lib().or_sign_correct(ex, ac))
 
 
+MASK_SCORE_DTYPE = np.dtype([("n_correct", "<i4"), ("n_test", "<i4"), ("n_rec", "<i4"),
+                             ("n_rec_hit", "<i4")])
+
+
+def aggregate_masks(opt, scn, n_folds: int, first_mask: int = 0, top_k: int = 64):
+    """C5 scoring (SURVEY §8(a) A7 "C5: per mask, sum over folds; rank masks by
+    (sum correct desc, mask asc) and keep the top-K").
+
+    opt/scn: per-scenario rows of whole masks (scenario s = mask*n_folds + fold).
+    Returns (rows [n_masks] MASK_SCORE_DTYPE, top [<=top_k] int64 mask ids).
+    """
+    n_masks = len(scn) // n_folds
+    assert n_masks * n_folds == len(scn)
+    rows = np.zeros(n_masks, dtype=MASK_SCORE_DTYPE)
+    o = opt.reshape(n_masks, n_folds, -1)
+    s = scn.reshape(n_masks, n_folds)
+    rows["n_correct"] = o["n_correct"].astype(np.int64).sum(axis=(1, 2))
+    rows["n_test"] = o["n_test"].astype(np.int64).sum(axis=(1, 2))
+    rows["n_rec"] = s["n_rec"].astype(np.int64).sum(axis=1)
+    rows["n_rec_hit"] = s["n_rec_hit"].astype(np.int64).sum(axis=1)
+    ids = np.arange(first_mask, first_mask + n_masks, dtype=np.int64)
+    order = np.lexsort((ids, -rows["n_correct"].astype(np.int64)))   # primary: correct desc; then id asc
+    return rows, ids[order[:top_k]]
+
+
 # ---------------------------------------------------------------- batch
 DEFAULT_PARAMS = dict(ridge=1e-8, threshold=1.05, clamp_floor=0.01, guard_tol=1e-9, max_count=3)
 

@@ -3,6 +3,7 @@
 // refinement) are argued in DESIGN.md §5.3.
 #pragma once
 #include "kernels.cuh"
+#include "fit_fast.cuh"
 
 namespace speedrec {
 
@@ -132,7 +133,7 @@ __device__ __forceinline__ double row_dot_u(const FitView& f, const double* xrow
 }
 
 template <int CMAX>
-__global__ void __launch_bounds__(512, 1) k_eval_warp(const EvalArgs A) {
+__global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, 1) k_eval_warp(const EvalArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const WarpLayout& L = A.L;
   int8_t* obit = reinterpret_cast<int8_t*>(smem);
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(512, 1) k_eval_warp(const EvalArgs A) {
   double* v3 = reinterpret_cast<double*>(slab + L.off_v3);
   double* invd = reinterpret_cast<double*>(slab + L.off_invd);
   double* Msm = reinterpret_cast<double*>(slab + L.off_M);
+  double* ufull = reinterpret_cast<double*>(slab + L.off_ufull);
 
   const long long gwarp = (long long)blockIdx.x * A.warps_per_block + warp;
   const long long nwarps = (long long)gridDim.x * A.warps_per_block;
@@ -180,7 +182,14 @@ __global__ void __launch_bounds__(512, 1) k_eval_warp(const EvalArgs A) {
   const int G = A.G, O = A.O, C = A.C;
   unsigned long long tot_corr = 0, tot_test = 0, tot_rec = 0, tot_hit = 0;  // lane 0
 
-  for (long long sl = gwarp; sl < A.count; sl += nwarps) {
+  // Work item = one scenario, or (C5 aggregation) one feature mask with all
+  // its folds, whose per-mask sums are reduced in registers (A7).
+  const long long n_items = A.agg ? A.count / A.n_splits : A.count;
+  const long long n_inner = A.agg ? A.n_splits : 1;
+  for (long long item = gwarp; item < n_items; item += nwarps) {
+  int m_corr = 0, m_test = 0, m_rec = 0, m_hit = 0;
+  for (long long inner = 0; inner < n_inner; ++inner) {
+    const long long sl = A.agg ? item * A.n_splits + inner : item;
     const long long s = A.first + sl;
     const long long split = s % A.n_splits, fidx = s / A.n_splits;
 
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(512, 1) k_eval_warp(const EvalArgs A) {
       row.sum_ratio = row.min_ratio = row.max_ratio = 0.0;
       row.fp_train = row.fp_test = 0ull;
       if (!((om >> o) & 1u)) {
-        if (lane == 0) A.opt_out[sl * O + o] = row;
+        if (lane == 0 && A.opt_out) A.opt_out[sl * O + o] = row;
         continue;
       }
       const int my_oi = oi++;
@@ -305,12 +314,12 @@ __global__ void __launch_bounds__(512, 1) k_eval_warp(const EvalArgs A) {
       __syncwarp();
       if (n == 0) {                      // untrained (reading R18)
         untrained += nt;
-        if (lane == 0) A.opt_out[sl * O + o] = row;
+        if (lane == 0 && A.opt_out) A.opt_out[sl * O + o] = row;
         continue;
       }
       trained |= 1u << o;
       if (nt == 0) {
-        if (lane == 0) A.opt_out[sl * O + o] = row;
+        if (lane == 0 && A.opt_out) A.opt_out[sl * O + o] = row;
         continue;
       }
 
@@ -341,29 +350,42 @@ __global__ void __launch_bounds__(512, 1) k_eval_warp(const EvalArgs A) {
         }
         deff += __popc(bm);
       }
+      {  // zero padding read by the fast-path fragment loads
+        const int pad_end = max(32, (deff + 3) & ~3);
+        for (int p = deff + lane; p < pad_end; p += 32) {
+          col[p] = 0;
+          xb[p] = 0.0;
+          sv[p] = 0.0;
+        }
+      }
       double ysum = 0.0;
       for (int i = lane; i < n; i += 32) ysum += tr_y[i];
       const double ybar = warp_sum(ysum) / (double)n;
+      for (int i = lane; i < n; i += 32) v3[i] = tr_y[i] - ybar;
       __syncwarp();
 
-      // ---- A3/A4: centred normal equations, dual or primal ----
-      FitView f{X, ldx, trs, n, col, xb, sv, deff};
+      // ---- A3/A4: centred normal equations, dual or primal (DESIGN §5.3) ----
       const bool dual = (n - 1) < deff;
       const int m = dual ? n : deff;
-      double* M = (m <= L.mcap) ? Msm : Mgl;
+      // refinement only where the conditioning needs it
+      const int nref = (dual ? 2 * (n - 1) >= deff : (n - 1) < 2 * deff) ? A.refine : 0;
       bool ok = true;
-      if (m > 0) {
+      if (m > 0 && m <= (L.mcap < 32 ? L.mcap : 32)) {
+        const FastView fv{X, ldx, trs, n, col, xb, sv, deff};
+        ok = dual ? fit_fast<true>(fv, v3, A.lambda, nref, Msm, v2, uv, wv, lane)
+                  : fit_fast<false>(fv, v3, A.lambda, nref, Msm, v2, uv, wv, lane);
+      } else if (m > 0) {
+        FitView f{X, ldx, trs, n, col, xb, sv, deff};
+        double* M = (m <= L.mcap) ? Msm : Mgl;
         if (dual) build_gram<true>(M, m, deff, f, A.lambda, lane);
         else build_gram<false>(M, m, n, f, A.lambda, lane);
         ok = chol_packed(M, invd, m, lane);
-      }
-      if (m > 0 && ok) {
-        if (dual) {
+        if (ok && dual) {
           // alpha = (K + lambda I)^{-1} yc ;  w' = Xtilde^T alpha
-          for (int i = lane; i < n; i += 32) { v3[i] = tr_y[i] - ybar; v1[i] = v3[i]; }
+          for (int i = lane; i < n; i += 32) v1[i] = v3[i];
           __syncwarp();
           chol_solve(M, invd, v1, m, lane);
-          for (int it = 0; it < A.refine; ++it) {
+          for (int it = 0; it < nref; ++it) {
             xt_times(f, v1, wv, lane);
             for (int a = lane; a < deff; a += 32) uv[a] = wv[a] * sv[a];
             __syncwarp();
@@ -377,13 +399,11 @@ __global__ void __launch_bounds__(512, 1) k_eval_warp(const EvalArgs A) {
             __syncwarp();
           }
           xt_times(f, v1, wv, lane);
-        } else {
+        } else if (ok) {
           // w' = (G + lambda I)^{-1} Xtilde^T yc
-          for (int i = lane; i < n; i += 32) v3[i] = tr_y[i] - ybar;
-          __syncwarp();
           xt_times(f, v3, wv, lane);
           chol_solve(M, invd, wv, m, lane);
-          for (int it = 0; it < A.refine; ++it) {
+          for (int it = 0; it < nref; ++it) {
             for (int a = lane; a < deff; a += 32) uv[a] = wv[a] * sv[a];
             __syncwarp();
             for (int i = lane; i < n; i += 32) {
@@ -399,18 +419,35 @@ __global__ void __launch_bounds__(512, 1) k_eval_warp(const EvalArgs A) {
             __syncwarp();
           }
         }
-        for (int a = lane; a < deff; a += 32) uv[a] = wv[a] * sv[a];
-        __syncwarp();
       }
       if (!ok) guard += 1000000;  // unreachable for lambda > 0; poisons the row
+      // weights on raw counters: EX = c0 + sum_c x_c * ufull[c]
+      for (int c = lane; c < C; c += 32) ufull[c] = 0.0;
+      __syncwarp();
+      double cpart = 0.0;
+      if (m > 0 && ok)
+        for (int a = lane; a < deff; a += 32) {
+          const double u = wv[a] * sv[a];
+          ufull[col[a]] = u;
+          cpart = fma(xb[a], u, cpart);
+        }
+      const double c0 = ybar - warp_sum(cpart);
+      __syncwarp();
 
       // ---- A5: predict + clamp; A7 per-(s,o) scores ----
       const int oiex = my_oi * exs;
       int ncorr = 0, ncl = 0;
       double rsum = 0.0, rmin = INFINITY, rmax = -INFINITY;
       for (int j = lane; j < nt; j += 32) {
-        double e = ybar;
-        if (m > 0) e += row_dot_u(f, X + (long long)tes[j] * ldx, uv);
+        const double* xr = X + (long long)tes[j] * ldx;
+        double e0 = 0.0, e1 = 0.0;
+        int c = 0;
+        for (; c + 1 < C; c += 2) {
+          e0 = fma(xr[c], ufull[c], e0);
+          e1 = fma(xr[c + 1], ufull[c + 1], e1);
+        }
+        if (c < C) e0 = fma(xr[c], ufull[c], e0);
+        double e = c0 + (e0 + e1);
         if (near_tol(e, 0.0, A.guard_tol) || near_tol(e, 1.0, A.guard_tol)) ++guard;
         uint8_t cl = 0;
         if (e <= 0.0) { e = A.clamp_floor; cl = 1; ++ncl; }
@@ -433,7 +470,9 @@ __global__ void __launch_bounds__(512, 1) k_eval_warp(const EvalArgs A) {
       row.max_ratio = warp_max(rmax);
       tot_corr += row.n_correct;
       tot_test += nt;
-      if (lane == 0) A.opt_out[sl * O + o] = row;
+      m_corr += row.n_correct;
+      m_test += nt;
+      if (lane == 0 && A.opt_out) A.opt_out[sl * O + o] = row;
       __syncwarp();
     }
 
@@ -500,9 +539,19 @@ __global__ void __launch_bounds__(512, 1) k_eval_warp(const EvalArgs A) {
     sr.n_guard = warp_isum(guard);
     tot_rec += sr.n_rec;
     tot_hit += sr.n_rec_hit;
-    if (lane == 0) A.scn_out[sl] = sr;
+    m_rec += sr.n_rec;
+    m_hit += sr.n_rec_hit;
+    if (lane == 0 && A.scn_out) A.scn_out[sl] = sr;
     __syncwarp();
+  }  // inner (folds)
+  if (A.agg && lane == 0) {
+    const long long mask_id = A.first / A.n_splits + item;
+    MaskScore ms{m_corr, m_test, m_rec, m_hit};
+    if (A.mask_out) A.mask_out[item] = ms;
+    // top-K key: more correct first, then smaller mask id (O8)
+    A.keys_out[item] = ((unsigned long long)(unsigned)m_corr << 32) | (0xFFFFFFFFull - (unsigned long long)mask_id);
   }
+  }  // items
   if (A.totals && lane == 0 && (tot_test | tot_rec)) {
     atomicAdd(&A.totals[0], tot_corr);
     atomicAdd(&A.totals[1], tot_test);

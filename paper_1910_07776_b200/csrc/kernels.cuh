@@ -26,6 +26,7 @@ constexpr int kMaxOpt = 16;
 constexpr int kMaxGroups = 64;
 constexpr int kMaxCounters = 128;
 constexpr int kMaxRec = 8;
+constexpr int kMaxWarpsPerBlock = 12;  // 384 threads -> up to 170 registers per thread
 
 struct OptScore {
   int32_t n_train, n_test, n_correct, n_clamped;
@@ -34,6 +35,9 @@ struct OptScore {
 };
 struct ScnScore {
   int32_t n_rec, n_rec_hit, n_untrained, n_guard;
+};
+struct MaskScore {
+  int32_t n_correct, n_test, n_rec, n_rec_hit;
 };
 
 // Per-warp shared-memory layout (byte offsets inside the warp's slab).
@@ -61,6 +65,8 @@ struct WarpLayout {
   int vmax;
   int off_M;            // double [mcap(mcap+1)/2] packed Cholesky factor
   int mcap;
+  int off_colbuf;       // double [32] column broadcast of the register Cholesky
+  int off_ufull;        // double [C] weights on raw counters
 };
 
 struct EvalArgs {
@@ -94,6 +100,9 @@ struct EvalArgs {
   double* ex_out;
   int8_t* rec_out;
   unsigned long long* totals;  // [4] or null
+  int agg;                     // 1: work item = mask (all folds), C5 aggregation
+  MaskScore* mask_out;         // [count / n_splits] or null
+  unsigned long long* keys_out;  // [count / n_splits] top-K keys (agg only)
   // workspace
   WarpLayout L;
   int warps_per_block;
@@ -177,6 +186,43 @@ __global__ void k_labels(const double* __restrict__ rt, const int8_t* __restrict
       y = rt[g * 64 + v] / rt[g * 64 + (v | (1 << b))];
     }
     ylab[i] = y;
+  }
+}
+
+// Mask ranking: keys = (sum correct << 32) | (2^32-1 - mask);
+// each 1024-thread block bitonic-sorts up to 1024 keys in shared memory
+// (descending) and keeps its first K.  Launched repeatedly (n -> n/1024*K)
+// until one block remains.  Integer keys => exact and order-independent.
+__global__ void __launch_bounds__(1024) k_topk_keys(const unsigned long long* __restrict__ in, long long n,
+                                                    unsigned long long* __restrict__ out, int K) {
+  __shared__ unsigned long long sk[1024];
+  const long long base = (long long)blockIdx.x * 1024;
+  const int t = threadIdx.x;
+  sk[t] = (base + t < n) ? in[base + t] : 0ull;
+  __syncthreads();
+  for (int size = 2; size <= 1024; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const int p = t ^ stride;
+      if (p > t) {
+        const bool desc = (t & size) == 0;
+        const unsigned long long a = sk[t], b = sk[p];
+        if (desc ? (a < b) : (a > b)) {
+          sk[t] = b;
+          sk[p] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (t < K) out[(long long)blockIdx.x * K + t] = sk[t];
+}
+
+// keys -> mask ids (-1 for padding), first K of a descending-sorted list.
+__global__ void k_decode_top(const unsigned long long* __restrict__ keys, long long n, int64_t* __restrict__ ids,
+                             int K) {
+  for (int t = threadIdx.x; t < K; t += blockDim.x) {
+    const unsigned long long k = t < n ? keys[t] : 0ull;
+    ids[t] = k ? (int64_t)(0xFFFFFFFFull - (k & 0xFFFFFFFFull)) : (int64_t)-1;
   }
 }
 

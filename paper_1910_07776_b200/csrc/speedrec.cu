@@ -22,6 +22,7 @@ using namespace speedrec;
 static_assert(sizeof(sr_opt_score) == 56, "sr_opt_score layout");
 static_assert(sizeof(OptScore) == sizeof(sr_opt_score), "OptScore layout");
 static_assert(sizeof(ScnScore) == sizeof(sr_scn_score), "ScnScore layout");
+static_assert(sizeof(MaskScore) == sizeof(sr_mask_score), "MaskScore layout");
 
 namespace {
 
@@ -60,7 +61,7 @@ struct sr_ctx {
   std::vector<int32_t> h_pool;
   int dmax = 0, np_tr = 0, np_te = 0, n_tg = 0, n_os = 0;
   // scratch + outputs
-  DevBuf gscratch, out_opt, out_scn, out_ex, out_rec, out_tot;
+  DevBuf gscratch, out_opt, out_scn, out_ex, out_rec, out_tot, out_mask, out_top, keys_a, keys_b;
   // accounting
   bool timing = false;
   std::vector<KStat> kstats;
@@ -216,7 +217,8 @@ void sr_destroy(sr_ctx* c) {
   collect_timing(c);
   for (DevBuf* b : {&c->counters, &c->cycles, &c->runtime, &c->opt_bit, &c->x, &c->ylab, &c->bad,
                     &c->train_g, &c->test_g, &c->split_om, &c->pool_list, &c->fmasks, &c->gscratch,
-                    &c->out_opt, &c->out_scn, &c->out_ex, &c->out_rec, &c->out_tot})
+                    &c->out_opt, &c->out_scn, &c->out_ex, &c->out_rec, &c->out_tot, &c->out_mask,
+                    &c->out_top, &c->keys_a, &c->keys_b})
     release(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -235,6 +237,8 @@ void sr_default_params(sr_params* p) {
   p->threshold = 1.05;
   p->clamp_floor = 0.01;
   p->guard_tol = 1e-9;
+  p->top_k = 64;
+  p->pad_ = 0;
 }
 
 sr_status sr_load_dataset(sr_ctx* c, const sr_dataset* d) {
@@ -433,9 +437,10 @@ WarpLayout plan_layout(const sr_ctx* c, int mcap) {
   L.off_tes = take(4 * c->np_te);
   L.off_tek = take(4 * c->np_te);
   L.off_tey = take(8 * c->np_te);
-  L.off_col = take(2 * d);
-  L.off_xb = take(8 * d);
-  L.off_s = take(8 * d);
+  const int dpad = std::max(d, 32) + 4;  // zero-padded for the fast-path fragment loads
+  L.off_col = take(2 * dpad);
+  L.off_xb = take(8 * dpad);
+  L.off_s = take(8 * dpad);
   L.off_w = take(8 * d);
   L.off_u = take(8 * d);
   L.vmax = vmax;
@@ -445,6 +450,8 @@ WarpLayout plan_layout(const sr_ctx* c, int mcap) {
   L.off_invd = take(8 * vmax);
   L.mcap = mcap;
   L.off_M = take(8 * (mcap * (mcap + 1) / 2));
+  L.off_colbuf = take(8 * 32);
+  L.off_ufull = take(8 * c->C);
   L.bytes = align16(off);
   return L;
 }
@@ -455,11 +462,18 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   if (!c) return SR_E_ARG;
   c->err.clear();
   if (!c->have_ds || !c->have_sc) return fail(c, SR_E_STATE, "evaluate: dataset and scenarios must be defined first");
-  if (!prm || !out || !out->opt_scores || !out->scn_scores) return fail(c, SR_E_ARG, "evaluate: null pointer");
+  if (!prm || !out) return fail(c, SR_E_ARG, "evaluate: null pointer");
+  const bool agg = out->mask_scores || out->top_masks;
+  if (!agg && (!out->opt_scores || !out->scn_scores))
+    return fail(c, SR_E_ARG, "evaluate: opt_scores and scn_scores are required without mask aggregation");
   const long long total = c->sc.n_splits * c->sc.n_masks;
   if (first < 0 || count < 0 || first + count > total)
     return fail(c, SR_E_ARG, "evaluate: range [%lld, %lld) outside [0, %lld)", (long long)first,
                 (long long)(first + count), total);
+  if (agg && (first % c->sc.n_splits || count % c->sc.n_splits))
+    return fail(c, SR_E_ARG, "evaluate: mask aggregation needs first/count multiples of n_splits=%lld",
+                (long long)c->sc.n_splits);
+  if (agg && (prm->top_k < 1 || prm->top_k > 512)) return fail(c, SR_E_ARG, "evaluate: top_k=%d", prm->top_k);
   if (prm->learner != SR_LINREG) return fail(c, SR_E_UNSUPPORTED, "evaluate: learner %d (IBK is NEXT-1)", prm->learner);
   if (prm->max_count < 1 || prm->max_count > kMaxRec) return fail(c, SR_E_ARG, "evaluate: max_count=%d", prm->max_count);
   if (prm->refine_steps < 0 || prm->refine_steps > 8) return fail(c, SR_E_ARG, "evaluate: refine_steps=%d", prm->refine_steps);
@@ -496,16 +510,16 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   if (prm->debug_mcap > 0) mcap = std::min(mcap, prm->debug_mcap);
   WarpLayout L = plan_layout(c, mcap);
   int avail = budget - head - (stage ? align16((int)stage_bytes) : 0);
-  int wpb = std::min(16, avail / std::max(L.bytes, 1));
+  int wpb = std::min(kMaxWarpsPerBlock, avail / std::max(L.bytes, 1));
   while (wpb < 4 && mcap > 8 && prm->debug_mcap == 0) {
     mcap /= 2;
     L = plan_layout(c, mcap);
-    wpb = std::min(16, avail / L.bytes);
+    wpb = std::min(kMaxWarpsPerBlock, avail / L.bytes);
   }
   if (wpb < 1 && stage) {
     stage = 0;
     avail = budget - head;
-    wpb = std::min(16, avail / L.bytes);
+    wpb = std::min(kMaxWarpsPerBlock, avail / L.bytes);
   }
   if (wpb < 1) return fail(c, SR_E_UNSUPPORTED, "evaluate: per-warp workspace %d B exceeds shared memory", L.bytes);
   const long long mscr = (mmax > mcap) ? (long long)mmax * (mmax + 1) / 2 : 0;
@@ -553,7 +567,8 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   int per_sm = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem));
   per_sm = std::max(per_sm, 1);
-  long long blocks = std::min<long long>((long long)c->sm_count * per_sm, (count + wpb - 1) / wpb);
+  const long long items = agg ? count / c->sc.n_splits : count;
+  long long blocks = std::min<long long>((long long)c->sm_count * per_sm, (items + wpb - 1) / wpb);
   blocks = std::max(1LL, blocks);
   const long long nwarps = blocks * wpb;
   if (mscr > 0) {
@@ -565,16 +580,36 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   // ---- outputs ----
   const size_t b_opt = (size_t)count * O * sizeof(sr_opt_score), b_scn = (size_t)count * sizeof(sr_scn_score);
   const size_t b_ex = (size_t)count * O * G * 32 * 8, b_rec = (size_t)count * N * prm->max_count;
+  const long long nm = agg ? count / c->sc.n_splits : 0;
+  const int K = prm->top_k;
+  if (agg) {
+    A.agg = 1;
+    const long long nk2 = (nm + 1023) / 1024 * K;
+    if ((st = ensure(c, c->keys_a, (size_t)std::max(nm, 1LL) * 8)) ||
+        (st = ensure(c, c->keys_b, (size_t)std::max(nk2, (long long)K) * 8)))
+      return st;
+    A.keys_out = (unsigned long long*)c->keys_a.p;
+  }
   if (out->on_device) {
     A.opt_out = (OptScore*)out->opt_scores;
     A.scn_out = (ScnScore*)out->scn_scores;
     A.ex_out = out->ex;
     A.rec_out = out->recs;
     A.totals = (unsigned long long*)out->totals;
+    A.mask_out = (MaskScore*)out->mask_scores;
   } else {
-    if ((st = ensure(c, c->out_opt, b_opt)) || (st = ensure(c, c->out_scn, b_scn))) return st;
-    A.opt_out = (OptScore*)c->out_opt.p;
-    A.scn_out = (ScnScore*)c->out_scn.p;
+    if (out->opt_scores) {
+      if ((st = ensure(c, c->out_opt, b_opt))) return st;
+      A.opt_out = (OptScore*)c->out_opt.p;
+    }
+    if (out->scn_scores) {
+      if ((st = ensure(c, c->out_scn, b_scn))) return st;
+      A.scn_out = (ScnScore*)c->out_scn.p;
+    }
+    if (out->mask_scores) {
+      if ((st = ensure(c, c->out_mask, (size_t)nm * sizeof(sr_mask_score)))) return st;
+      A.mask_out = (MaskScore*)c->out_mask.p;
+    }
     if (out->ex) {
       if ((st = ensure(c, c->out_ex, b_ex))) return st;
       A.ex_out = (double*)c->out_ex.p;
@@ -593,9 +628,36 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
          kern<<<(unsigned)blocks, wpb * 32, smem, c->stream>>>(A);
        })))
     return st;
+  if (agg && out->top_masks) {
+    // iterated block top-K over the mask keys (O8)
+    unsigned long long* src = (unsigned long long*)c->keys_a.p;
+    unsigned long long* dst = (unsigned long long*)c->keys_b.p;
+    long long n = nm;
+    do {
+      const long long nb = (n + 1023) / 1024;
+      if ((st = launch(c, "k_topk_keys", [&] { k_topk_keys<<<(unsigned)nb, 1024, 0, c->stream>>>(src, n, dst, K); })))
+        return st;
+      n = nb * K;
+      std::swap(src, dst);
+    } while (n > K);
+    int64_t* tm = out->on_device ? out->top_masks : nullptr;
+    if (!tm) {
+      if ((st = ensure(c, c->out_top, (size_t)K * 8))) return st;
+      tm = (int64_t*)c->out_top.p;
+    }
+    if ((st = launch(c, "k_decode_top", [&] { k_decode_top<<<1, 512, 0, c->stream>>>(src, n, tm, K); })))
+      return st;
+    if (!out->on_device)
+      CU(cudaMemcpyAsync(out->top_masks, tm, (size_t)K * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
   if (!out->on_device) {
-    CU(cudaMemcpyAsync(out->opt_scores, c->out_opt.p, b_opt, cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaMemcpyAsync(out->scn_scores, c->out_scn.p, b_scn, cudaMemcpyDeviceToHost, c->stream));
+    if (out->opt_scores)
+      CU(cudaMemcpyAsync(out->opt_scores, c->out_opt.p, b_opt, cudaMemcpyDeviceToHost, c->stream));
+    if (out->scn_scores)
+      CU(cudaMemcpyAsync(out->scn_scores, c->out_scn.p, b_scn, cudaMemcpyDeviceToHost, c->stream));
+    if (out->mask_scores)
+      CU(cudaMemcpyAsync(out->mask_scores, c->out_mask.p, (size_t)nm * sizeof(sr_mask_score),
+                         cudaMemcpyDeviceToHost, c->stream));
     if (out->ex) CU(cudaMemcpyAsync(out->ex, c->out_ex.p, b_ex, cudaMemcpyDeviceToHost, c->stream));
     if (out->recs) CU(cudaMemcpyAsync(out->recs, c->out_rec.p, b_rec, cudaMemcpyDeviceToHost, c->stream));
     if (out->totals) CU(cudaMemcpyAsync(out->totals, c->out_tot.p, 32, cudaMemcpyDeviceToHost, c->stream));

@@ -54,12 +54,18 @@ class sr_scenarios(ct.Structure):
 class sr_params(ct.Structure):
     _fields_ = [("learner", ct.c_int32), ("max_count", ct.c_int32), ("refine_steps", ct.c_int32),
                 ("debug_mcap", ct.c_int32), ("ridge", ct.c_double), ("threshold", ct.c_double),
-                ("clamp_floor", ct.c_double), ("guard_tol", ct.c_double)]
+                ("clamp_floor", ct.c_double), ("guard_tol", ct.c_double), ("top_k", ct.c_int32),
+                ("pad_", ct.c_int32)]
 
 
 class sr_outputs(ct.Structure):
     _fields_ = [("opt_scores", ct.c_void_p), ("scn_scores", ct.c_void_p), ("ex", ct.c_void_p),
-                ("recs", ct.c_void_p), ("totals", ct.c_void_p), ("on_device", ct.c_int32)]
+                ("recs", ct.c_void_p), ("totals", ct.c_void_p), ("mask_scores", ct.c_void_p),
+                ("top_masks", ct.c_void_p), ("on_device", ct.c_int32)]
+
+
+MASK_SCORE_DTYPE = np.dtype([("n_correct", "<i4"), ("n_test", "<i4"), ("n_rec", "<i4"),
+                             ("n_rec_hit", "<i4")])
 
 
 # Every symbol include/speedrec.h declares (checked by tests/test_boundary.py).
@@ -199,31 +205,37 @@ class Context:
 
     # ------------------------------------------------------------ compute
     def evaluate(self, first: int = 0, count: Optional[int] = None, params: Optional[sr_params] = None,
-                 want_ex: bool = False, want_recs: bool = False, out: Optional[dict] = None):
+                 want_ex: bool = False, want_recs: bool = False, out: Optional[dict] = None,
+                 want_masks: bool = False, per_scenario: bool = True, n_folds: Optional[int] = None):
         """Run the fused path on scenarios [first, first+count).
 
         out=None: host numpy outputs (synchronous).  out=dict of torch CUDA
-        tensors {opt, scn[, ex, recs]}: device outputs, asynchronous on the
-        context stream.
+        tensors {opt, scn[, ex, recs, totals, masks, top]}: device outputs,
+        asynchronous on the context stream.  want_masks: per-mask sums over
+        the folds + top-k mask ids (C5); per_scenario=False skips the rows.
         """
         if count is None:
             count = self.n_scenarios - first
         p = params or default_params()
         if self.shape is None:      # let the library report the call-order error
-            o = sr_outputs(None, None, None, None, None, 0)
+            o = sr_outputs()
             self._check(lib().sr_evaluate(self._h, ct.byref(p), first, count, ct.byref(o)))
         O, G = self.shape["O"], self.shape["G"]
         if out is None:
-            opt = np.zeros((count, O), dtype=OPT_SCORE_DTYPE)
-            scn = np.zeros(count, dtype=SCN_SCORE_DTYPE)
+            opt = np.zeros((count, O), dtype=OPT_SCORE_DTYPE) if per_scenario else None
+            scn = np.zeros(count, dtype=SCN_SCORE_DTYPE) if per_scenario else None
             ex = np.zeros((count, O, G * 32)) if want_ex else None
             recs = np.zeros((count, G * 64, p.max_count), dtype=np.int8) if want_recs else None
             tot = np.zeros(4, dtype=np.int64)
-            o = sr_outputs(_ptr(opt), _ptr(scn), _ptr(ex), _ptr(recs), _ptr(tot), 0)
+            masks = top = None
+            if want_masks:
+                masks = np.zeros(count // n_folds, dtype=MASK_SCORE_DTYPE)
+                top = np.zeros(p.top_k, dtype=np.int64)
+            o = sr_outputs(_ptr(opt), _ptr(scn), _ptr(ex), _ptr(recs), _ptr(tot), _ptr(masks), _ptr(top), 0)
             self._check(lib().sr_evaluate(self._h, ct.byref(p), first, count, ct.byref(o)))
-            return dict(opt=opt, scn=scn, ex=ex, recs=recs, totals=tot)
-        o = sr_outputs(_ptr(out["opt"]), _ptr(out["scn"]), _ptr(out.get("ex")), _ptr(out.get("recs")),
-                       _ptr(out.get("totals")), 1)
+            return dict(opt=opt, scn=scn, ex=ex, recs=recs, totals=tot, masks=masks, top=top)
+        o = sr_outputs(_ptr(out.get("opt")), _ptr(out.get("scn")), _ptr(out.get("ex")), _ptr(out.get("recs")),
+                       _ptr(out.get("totals")), _ptr(out.get("masks")), _ptr(out.get("top")), 1)
         self._check(lib().sr_evaluate(self._h, ct.byref(p), first, count, ct.byref(o)))
         return out
 

@@ -1,0 +1,74 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the sharding and exchange
+logic the N-GPU bench uses (paper_1910_07776_b200/dist.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1910_07776_b200 import dist as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # pooled totals: exact integer sums
+        tot = torch.tensor([10 + rank, 20, 3 * rank, 1], dtype=torch.int64)
+        red = D.reduce_totals(tot, dist)
+        # timing: max over ranks
+        mx = D.max_over_ranks(1.5 + rank, dist)
+        # top-k merge: rank 0 owns masks 0..3, rank 1 masks 4..7
+        correct = {0: 5, 1: 9, 2: 9, 3: 1, 4: 9, 5: 2, 6: 7, 7: 9}
+        mine = [m for m in correct if (m < 4) == (rank == 0)]
+        mine.sort(key=lambda m: (-correct[m], m))
+        ids = mine[:3]
+        top = D.merge_top_masks(ids + [-1], [correct[m] for m in ids] + [0], 4, dist)
+        q.put((rank, red.tolist(), mx, top.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_exchange():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, red, mx, top in res:
+        assert red == [21, 40, 3, 2]
+        assert mx == 2.5
+        assert top == [1, 2, 4, 7]          # ties on 9 correct broken by mask id (O8)
+
+
+def test_shard_ranges_partition():
+    for total, world, align in ((1000, 2, 1), (1003, 4, 1), (128 * 1024, 8, 128), (64, 8, 1)):
+        seen = []
+        for r in range(world):
+            a, n = D.strong_range(total, r, world, align)
+            assert a % align == 0 and n % align == 0
+            seen.extend(range(a, a + n))
+        assert seen == list(range(total // align * align))
+    assert D.weak_range(1000, 3) == (3000, 1000)
+
+
+def test_topk_key_order_matches_rule():
+    keys = [D.topk_key(c, m) for c, m in ((5, 3), (9, 7), (9, 2), (0, 0))]
+    order = np.argsort(keys)[::-1]
+    assert list(order) == [2, 1, 0, 3]

@@ -54,7 +54,10 @@ def test_c2_all_table2(Context):
     cfg = gen.make_config("C2")
     got, ref = _run(Context, cfg, 0, 240)
     st = compare(got, ref, max_guard_frac=0.05)
-    print("C2", st)
+    from tests.parity import rel_err
+    e = rel_err(got["ex"], ref["ex"]).reshape(240, -1).max(axis=1)
+    per_exp = {int(x): float(e[cfg.scenarios.experiment == x].max()) for x in range(1, 7)}
+    print("C2", st, "worst EX rel err per experiment", per_exp)
 
 
 def test_c3_small_ragged(Context):
@@ -70,6 +73,38 @@ def test_c5_small_masks(Context):
     n = cfg.scenarios.n_scenarios
     got, ref = _run(Context, cfg, 0, n)
     print("C5k5", compare(got, ref))
+
+
+def test_c5_mask_aggregation_and_top_k(Context):
+    """A7 for C5: per-mask sums over the 128 LOO folds and the mask ranking
+    (sum correct desc, id asc), fused in the kernel, per-scenario rows not
+    materialised; exact integers vs the oracle's aggregation."""
+    from paper_1910_07776_b200 import default_params
+    cfg = gen.make_config("C5", n_masks_k=7)        # 128 masks x 128 folds
+    folds = cfg.scenarios.n_splits
+    n = cfg.scenarios.n_scenarios
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    for k in (5, 64, 200):
+        p = default_params(top_k=k)
+        got = ctx.evaluate(0, n, params=p, want_masks=True, per_scenario=False, n_folds=folds)
+        ref = oracle.evaluate(cfg.dataset, cfg.scenarios, 0, n)
+        assert ref["scn"]["n_guard"].sum() == 0
+        rows, top = oracle.aggregate_masks(ref["opt"], ref["scn"], folds, top_k=k)
+        for f in rows.dtype.names:
+            assert np.array_equal(got["masks"][f], rows[f]), f
+        assert list(got["top"][:len(top)]) == list(top)
+        assert (got["top"][len(top):] == -1).all()
+        assert got["totals"][1] == rows["n_test"].sum()
+    # sub-range of whole masks, plus per-scenario rows in the same call
+    got = ctx.evaluate(32 * folds, 16 * folds, params=default_params(top_k=4), want_masks=True, n_folds=folds)
+    ref = oracle.evaluate(cfg.dataset, cfg.scenarios, 32 * folds, 16 * folds)
+    rows, top = oracle.aggregate_masks(ref["opt"], ref["scn"], folds, first_mask=32, top_k=4)
+    assert np.array_equal(got["masks"]["n_correct"], rows["n_correct"])
+    assert list(got["top"]) == list(top)
+    compare(got, ref)
+    ctx.close()
 
 
 def test_global_scratch_path(Context):

@@ -384,3 +384,20 @@ def test_pipeline_recommendation_rule():
             assert list(recs) == [0, -1, -1]
     assert r["scn"]["n_rec"].sum() == 32 and r["scn"]["n_rec_hit"].sum() == 32
     assert (r["opt"][:, 0]["n_correct"] == r["opt"][:, 0]["n_test"]).all()
+
+
+def test_mask_aggregation_ranking_rule():
+    # O8: per-mask sums over folds; rank by (sum correct desc, mask id asc).
+    n_masks, folds, O = 5, 3, 2
+    opt = np.zeros((n_masks * folds, O), dtype=oracle.OPT_SCORE_DTYPE)
+    scn = np.zeros(n_masks * folds, dtype=oracle.SCN_SCORE_DTYPE)
+    correct = {0: 4, 1: 7, 2: 7, 3: 1, 4: 9}
+    for m, c in correct.items():
+        for f in range(folds):
+            opt[m * folds + f, 0]["n_correct"] = c if f == 0 else 0
+            opt[m * folds + f, :]["n_test"] = 2
+            scn[m * folds + f]["n_rec"] = 1
+    rows, top = oracle.aggregate_masks(opt, scn, folds, first_mask=10, top_k=3)
+    assert list(rows["n_correct"]) == [4, 7, 7, 1, 9]
+    assert (rows["n_test"] == 12).all() and (rows["n_rec"] == 3).all()
+    assert list(top) == [14, 11, 12]
