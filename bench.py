@@ -35,18 +35,27 @@ def fit_flops(n: np.ndarray, t: np.ndarray, d: int, refine: int = 2) -> float:
     per fit with n training pairs, t test cases and d active features,
       dual   (n-1 < d): n(n+1)/2*d + n^3/6 + n^2 + R*(2nd + n^2) + nd + td   FMA
       primal (else)   : n*d(d+1)/2 + d^3/6 + nd + d^2 + R*(2nd + d^2) + td   FMA
-    R = refine when the fit's conditioning rule asks for it (dual: 2(n-1) >= d,
-    primal: n-1 < 2d), else 0.  flop = 2 * FMA.  Fits with
+    R = refine when the fit's rule asks for it (dual: 2(n-1) >= d, primal:
+    n-1 < 2d or n > 64), else 0.  flop = 2 * FMA.  Fits with
     n == 0 or t == 0 do no work."""
     n = n.astype(np.float64)
     t = t.astype(np.float64)
     live = (n > 0) & (t > 0)
     dual = (n - 1) < d
     rd = np.where(2 * (n - 1) >= d, refine, 0)
-    rp = np.where((n - 1) < 2 * d, refine, 0)
+    rp = np.where(((n - 1) < 2 * d) | (n > 64), refine, 0)
     fd = n * (n + 1) / 2 * d + n ** 3 / 6 + n ** 2 + rd * (2 * n * d + n ** 2) + n * d + t * d
     fp = n * d * (d + 1) / 2 + d ** 3 / 6 + n * d + d ** 2 + rp * (2 * n * d + d ** 2) + t * d
     return float(2.0 * np.where(live, np.where(dual, fd, fp), 0.0).sum())
+
+
+def fit_flops_big(n: np.ndarray, t: np.ndarray, d: int, refine: int = 2) -> float:
+    """k_fit_big (C4 path, primal, always refined; prediction is in k_rank_big):
+    per fit n*d(d+1)/2 + d^3/6 + nd + d^2 + R*(2nd + d^2) FMA, flop = 2 FMA."""
+    n = n.astype(np.float64)
+    live = (n > 0) & (t > 0)
+    f = n * d * (d + 1) / 2 + d ** 3 / 6 + n * d + d ** 2 + refine * (2 * n * d + d ** 2)
+    return float(2.0 * np.where(live, f, 0.0).sum())
 
 
 class ClockSampler:
@@ -148,6 +157,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=4000)
     ap.add_argument("--cpu-sample", type=int, default=4000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg (tuning runs)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -220,10 +230,16 @@ def main():
 
     # ---------------- roofline of the dominant kernel (FP64 ALU/DMMA bound)
     opt = out["opt"].cpu().numpy().view(OPT_SCORE_DTYPE).reshape(count, O)
-    flops_launch = fit_flops(opt["n_train"].ravel(), opt["n_test"].ravel(), ds.n_counters)
-    name_dom = "k_eval_warp"
+    big = ds.n_groups > 64          # CTA-per-fit path (C4): prediction runs in k_rank_big
+    n_tr, n_te = opt["n_train"].ravel(), opt["n_test"].ravel()
+    name_dom = "k_fit_big" if big else "k_fit_warp"
+    flops_launch = fit_flops(n_tr, np.where(big, 0, n_te), ds.n_counters,
+                             refine=2) if not big else fit_flops_big(n_tr, n_te, ds.n_counters)
     n_dom, ms_dom = stats.get(name_dom, (0, 0.0))
-    avg_dom = ms_dom / max(n_dom, 1)
+    avg_dom = ms_dom / max(n_dom, 1)                 # average launch duration (CUDA events, live)
+    launches_per_step = max(n_dom // max(args.steps, 1), 1)
+    flops_step = flops_launch                        # algorithmic flops of one step (all chunks)
+    flops_launch = flops_step / launches_per_step    # chunks are equal-sized slices of the batch
     clk_sum = clk.summary()
     sm_max = clk_sum.get("sm_max_mhz") or 1965.0
     props = torch.cuda.get_device_properties(dev)
@@ -233,7 +249,7 @@ def main():
 
     # ---------------- end to end: host buffers through the C-ABI, copies inside
     e2e = None
-    if True:
+    if not args.no_e2e:
         hc = torch.from_numpy(ds.counters).pin_memory()
         hy = torch.from_numpy(ds.cycles).pin_memory()
         hr = torch.from_numpy(ds.runtime_ms).pin_memory()
@@ -284,7 +300,7 @@ def main():
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": None,
                          "kernel": name_dom, "kernel_ms": avg_dom, "kernel_share_of_step": share,
-                         "flops_per_launch": flops_launch,
+                         "flops_per_launch": flops_launch, "launches_per_step": launches_per_step,
                          "peak_note": f"FP64 (DFMA/DMMA shared pipe): {props.multi_processor_count} SMs x "
                                       f"{FP64_FMA_PER_CLK_PER_SM} FMA/clk x 2 x {sm_max:.0f} MHz"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

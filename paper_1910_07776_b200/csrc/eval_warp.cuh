@@ -1,14 +1,26 @@
-// eval_warp.cuh -- k_eval_warp: one warp = one scenario, A1..A7 fused.
-// Paper passages per step are cited inline; the numerics (dual/primal choice,
-// refinement) are argued in DESIGN.md §5.3.
+// eval_warp.cuh -- the warp-per-fit path (<= 64 groups: configs C1, C2, C3, C5).
+// DESIGN.md §5.2.
+//
+//  k_fit_warp  one warp = one (scenario, optimization) fit, A1-A5 + the
+//              per-(scenario, optimization) scores of A7.  Persistent grid of
+//              warps over the fits of a scenario chunk; the rate matrix is
+//              staged once per CTA in shared memory when it fits.  EX of every
+//              test case goes to a per-chunk table (clamped values negated).
+//  k_rank_warp one warp = one scenario: A6 rank + thresholded recommendation
+//              per test slot from the EX table, per-scenario scores (A7).
+//  k_mask_final C5: per-mask rows and ranking keys from the atomically summed
+//              integer accumulators.
+// Splitting fit and rank keeps each kernel's hot code small (instruction
+// cache) and balances the fits (warp per fit, not per scenario).
 #pragma once
-#include "kernels.cuh"
 #include "fit_fast.cuh"
+#include "kernels.cuh"
 
 namespace speedrec {
 
-// View of one fit's operands: training rows are tr_slot[0..n), active
-// features col[0..deff) with centring xb and scale s (1/range).
+// ---------------------------------------------------------------- generic
+// (m > 32: rare on C3, never on C1/C2/C5) -- packed factor and two vectors
+// in the warp's global scratch slab.
 struct FitView {
   const double* X;   // rates, row stride ldx (staged smem or global)
   int ldx;
@@ -20,10 +32,6 @@ struct FitView {
   int deff;
 };
 
-// Element (r, k) of the contraction operand Z (m x L).  Dual (kernel) form:
-// Z = Xtilde (rows = training rows, k = features).  Primal form: Z = Xtilde^T.
-// Xtilde_ia = (x_ia - xbar_a) * s_a: the min-max scaled, centred feature
-// (the min cancels under centring; reading D3).
 template <bool DUAL>
 __device__ __forceinline__ double zval(const FitView& f, int r, int k) {
   int i = DUAL ? r : k, a = DUAL ? k : r;
@@ -31,8 +39,6 @@ __device__ __forceinline__ double zval(const FitView& f, int r, int k) {
   return 0.0;
 }
 
-// Packed lower triangle of Z Z^T + lambda I (m x m), 8x8 tiles on DMMA.
-// All 32 lanes execute every mma (warp-uniform loops).
 template <bool DUAL>
 __device__ void build_gram(double* M, int m, int Lk, const FitView& f, double lambda, int lane) {
   const int nb = (m + 7) >> 3;
@@ -71,8 +77,6 @@ __device__ void build_gram(double* M, int m, int Lk, const FitView& f, double la
   __syncwarp();
 }
 
-// In-place Cholesky of the packed lower triangle, rsqrt pivots.
-// invd[j] = 1 / L_jj.  Returns false if a pivot is not positive.
 __device__ bool chol_packed(double* M, double* invd, int m, int lane) {
   for (int j = 0; j < m; ++j) {
     const double djj = M[pk(j, j)];
@@ -95,7 +99,6 @@ __device__ bool chol_packed(double* M, double* invd, int m, int lane) {
   return true;
 }
 
-// z <- (L L^T)^{-1} z, z in shared memory.
 __device__ void chol_solve(const double* M, const double* invd, double* z, int m, int lane) {
   for (int j = 0; j < m; ++j) {
     const double yj = z[j] * invd[j];
@@ -113,7 +116,6 @@ __device__ void chol_solve(const double* M, const double* invd, double* z, int m
   }
 }
 
-// out_a = s_a * sum_i (x_ia - xb_a) * v_i   (= Xtilde^T v), lanes over features.
 __device__ void xt_times(const FitView& f, const double* v, double* out, int lane) {
   for (int a = lane; a < f.deff; a += 32) {
     const int c = f.col[a];
@@ -125,15 +127,61 @@ __device__ void xt_times(const FitView& f, const double* v, double* out, int lan
   __syncwarp();
 }
 
-// out_i = sum_a (x_ia - xb_a) * u_a   (= Xtilde w with u = s .* w), lanes over rows.
 __device__ __forceinline__ double row_dot_u(const FitView& f, const double* xrow, const double* u) {
   double acc = 0.0;
   for (int a = 0; a < f.deff; ++a) acc = fma(xrow[f.col[a]] - f.xb[a], u[a], acc);
   return acc;
 }
 
-template <int CMAX>
-__global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, 1) k_eval_warp(const EvalArgs A) {
+// Generic fit (any m): yc [n] smem, scratch slab: M packed + v1 [vmax] + invd [vmax].
+// Output w' in wv[0..deff).
+__device__ __noinline__ bool fit_generic(const FitView& f, const double* yc, double lambda, int nref, bool dual,
+                                         double* scr, int vmax, double* uv, double* v2, double* wv, int lane) {
+  const int m = dual ? f.n : f.deff;
+  double* M = scr;
+  double* v1 = scr + (long long)m * (m + 1) / 2;
+  double* invd = v1 + vmax;
+  if (dual) build_gram<true>(M, m, f.deff, f, lambda, lane);
+  else build_gram<false>(M, m, f.n, f, lambda, lane);
+  if (!chol_packed(M, invd, m, lane)) return false;
+  if (dual) {
+    for (int i = lane; i < f.n; i += 32) v1[i] = yc[i];
+    __syncwarp();
+    chol_solve(M, invd, v1, m, lane);
+    for (int it = 0; it < nref; ++it) {
+      xt_times(f, v1, wv, lane);
+      for (int a = lane; a < f.deff; a += 32) uv[a] = wv[a] * f.s[a];
+      __syncwarp();
+      for (int i = lane; i < f.n; i += 32)
+        v2[i] = yc[i] - row_dot_u(f, f.X + (long long)f.trs[i] * f.ldx, uv) - lambda * v1[i];
+      __syncwarp();
+      chol_solve(M, invd, v2, m, lane);
+      for (int i = lane; i < f.n; i += 32) v1[i] += v2[i];
+      __syncwarp();
+    }
+    xt_times(f, v1, wv, lane);
+  } else {
+    xt_times(f, yc, wv, lane);
+    chol_solve(M, invd, wv, m, lane);
+    for (int it = 0; it < nref; ++it) {
+      for (int a = lane; a < f.deff; a += 32) uv[a] = wv[a] * f.s[a];
+      __syncwarp();
+      for (int i = lane; i < f.n; i += 32) v2[i] = yc[i] - row_dot_u(f, f.X + (long long)f.trs[i] * f.ldx, uv);
+      __syncwarp();
+      xt_times(f, v2, v1, lane);
+      for (int a = lane; a < f.deff; a += 32) v1[a] -= lambda * wv[a];
+      __syncwarp();
+      chol_solve(M, invd, v1, m, lane);
+      for (int a = lane; a < f.deff; a += 32) wv[a] += v1[a];
+      __syncwarp();
+    }
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------- fit kernel
+template <int WMAX>
+__global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const WarpLayout& L = A.L;
   int8_t* obit = reinterpret_cast<int8_t*>(smem);
@@ -155,355 +203,283 @@ __global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, 1) k_eval_warp(const E
   unsigned char* slab = smem + A.off_warps + warp * L.bytes;
   uint64_t* trw = reinterpret_cast<uint64_t*>(slab + L.off_trw);
   uint64_t* tew = reinterpret_cast<uint64_t*>(slab + L.off_tew);
-  int16_t* gidx = reinterpret_cast<int16_t*>(slab + L.off_gidx);
   int16_t* F = reinterpret_cast<int16_t*>(slab + L.off_F);
-  double* extab = reinterpret_cast<double*>(slab + L.off_ex);
-  uint8_t* excl = reinterpret_cast<uint8_t*>(slab + L.off_excl);
   int32_t* trs = reinterpret_cast<int32_t*>(slab + L.off_trs);
-  double* tr_y = reinterpret_cast<double*>(slab + L.off_try);
+  double* yc = reinterpret_cast<double*>(slab + L.off_yc);
   int32_t* tes = reinterpret_cast<int32_t*>(slab + L.off_tes);
   int32_t* tek = reinterpret_cast<int32_t*>(slab + L.off_tek);
-  double* te_y = reinterpret_cast<double*>(slab + L.off_tey);
   int16_t* col = reinterpret_cast<int16_t*>(slab + L.off_col);
   double* xb = reinterpret_cast<double*>(slab + L.off_xb);
   double* sv = reinterpret_cast<double*>(slab + L.off_s);
   double* wv = reinterpret_cast<double*>(slab + L.off_w);
   double* uv = reinterpret_cast<double*>(slab + L.off_u);
-  double* v1 = reinterpret_cast<double*>(slab + L.off_v1);
   double* v2 = reinterpret_cast<double*>(slab + L.off_v2);
-  double* v3 = reinterpret_cast<double*>(slab + L.off_v3);
-  double* invd = reinterpret_cast<double*>(slab + L.off_invd);
   double* Msm = reinterpret_cast<double*>(slab + L.off_M);
   double* ufull = reinterpret_cast<double*>(slab + L.off_ufull);
 
   const long long gwarp = (long long)blockIdx.x * A.warps_per_block + warp;
   const long long nwarps = (long long)gridDim.x * A.warps_per_block;
-  double* Mgl = A.gscratch ? A.gscratch + gwarp * A.mscratch : nullptr;
+  double* scr = A.gscratch ? A.gscratch + gwarp * A.mscratch : nullptr;
   const int G = A.G, O = A.O, C = A.C;
-  unsigned long long tot_corr = 0, tot_test = 0, tot_rec = 0, tot_hit = 0;  // lane 0
+  unsigned long long tot_corr = 0, tot_test = 0;
 
-  // Work item = one scenario, or (C5 aggregation) one feature mask with all
-  // its folds, whose per-mask sums are reduced in registers (A7).
-  const long long n_items = A.agg ? A.count / A.n_splits : A.count;
-  const long long n_inner = A.agg ? A.n_splits : 1;
-  for (long long item = gwarp; item < n_items; item += nwarps) {
-  int m_corr = 0, m_test = 0, m_rec = 0, m_hit = 0;
-  for (long long inner = 0; inner < n_inner; ++inner) {
-    const long long sl = A.agg ? item * A.n_splits + inner : item;
-    const long long s = A.first + sl;
-    const long long split = s % A.n_splits, fidx = s / A.n_splits;
+  for (long long f = gwarp; f < A.count * O; f += nwarps) {
+    const long long sl = f / O;
+    const int o = (int)(f - sl * O);
+    const long long s = A.first + sl, so = A.out0 + sl;
+    const long long split = s % A.sd.n_splits, fidx = s / A.sd.n_splits;
+    const uint32_t om = scored_mask(A.sd, split, O);
+    OptScore row;
+    row.n_train = row.n_test = row.n_correct = row.n_clamped = 0;
+    row.sum_ratio = row.min_ratio = row.max_ratio = 0.0;
+    row.fp_train = row.fp_test = 0ull;
+    if (!((om >> o) & 1u)) {
+      if (lane == 0 && A.opt_out) A.opt_out[so * O + o] = row;
+      continue;
+    }
+    const int q = __popc(om & ((1u << o) - 1u));  // scored-optimization slot in the EX table
 
-    // ---- A1: split membership words per group (Table 2; R17) ----
+    // ---- A1: split membership (Table 2; R17), features, pairs ----
     for (int g = lane; g < G; g += 32) {
-      uint64_t tr = 0, te = 0;
-      if (A.kind == 0) {
-        tr = ((A.train_g[split * A.gw + (g >> 6)] >> (g & 63)) & 1ull) ? ~0ull : 0ull;
-        te = ((A.test_g[split * A.gw + (g >> 6)] >> (g & 63)) & 1ull) ? ~0ull : 0ull;
-      } else if (A.kind == 1) {
-        bool inpool = false;
-        for (int q = 0; q < A.n_pool; ++q) inpool |= (A.pool_list[q] == g);
-        tr = inpool ? ~0ull : 0ull;
-        const int gh = A.pool_list[split >> 6];
-        const int vh = (int)(split & 63);
-        if (g == gh) {
-          tr &= ~(1ull << vh);
-          te = 1ull << vh;
-        }
-      } else {
-        tr = mix64(mix64(A.seed ^ mix64((uint64_t)split)) + (uint64_t)g);
-        te = ~tr;
-      }
+      uint64_t tr, te;
+      member_words(A.sd, split, g, tr, te);
       trw[g] = tr;
       tew[g] = te;
     }
-    // feature set F, counter-index order
     int d = 0;
     for (int c0 = 0; c0 < C; c0 += 32) {
       const int c = c0 + lane;
-      bool in = false;
-      if (c < C) {
-        if (A.subsets_k > 0) in = c < A.subsets_k && ((fidx >> c) & 1);
-        else if (A.fmasks) in = (A.fmasks[fidx * 2 + (c >> 6)] >> (c & 63)) & 1ull;
-        else in = true;
-      }
+      const bool in = c < C && feature_in(A.sd, fidx, c);
       const unsigned bm = __ballot_sync(FULL, in);
       if (in) F[d + __popc(bm & lt)] = (int16_t)c;
       d += __popc(bm);
     }
     __syncwarp();
-    // test-group index
-    int n_tg = 0;
-    for (int g0 = 0; g0 < G; g0 += 32) {
-      const int g = g0 + lane;
-      const bool has = g < G && tew[g] != 0ull;
-      const unsigned bm = __ballot_sync(FULL, has);
-      if (g < G) gidx[g] = has ? (int16_t)(n_tg + __popc(bm & lt)) : (int16_t)-1;
-      n_tg += __popc(bm);
+    int n = 0, nt = 0;
+    uint64_t fptr = 0, fpte = 0;
+    for (int g = 0; g < G; ++g) {
+      const int b = obit[(g / A.IR) * O + o];
+      const uint64_t tr = trw[g], te = tew[g];
+      if (b < 0 || (tr == 0ull && te == 0ull)) continue;
+      const int v = ins0(lane, b);
+      const bool istr = ((tr >> v) & 1ull) && ((tr >> (v | (1 << b))) & 1ull);
+      const bool iste = (te >> v) & 1ull;
+      const unsigned mtr = __ballot_sync(FULL, istr), mte = __ballot_sync(FULL, iste);
+      const int lab = (g * O + o) * 32 + lane;
+      if (istr | iste) {
+        const uint64_t h = mix64((uint64_t)lab);
+        if (istr) {
+          const int p = n + __popc(mtr & lt);
+          trs[p] = g * 64 + v;
+          yc[p] = A.ylab[lab];
+          fptr ^= h;
+        }
+        if (iste) {
+          const int p = nt + __popc(mte & lt);
+          tes[p] = g * 64 + v;
+          tek[p] = g * 32 + lane;
+          fpte ^= h;
+        }
+      }
+      n += __popc(mtr);
+      nt += __popc(mte);
     }
-    const uint32_t om = (A.split_om ? A.split_om[split] : A.opt_mask) & ((1u << O) - 1u);
-    const int exs = n_tg * 32;  // EX table stride per optimization
-    // zero the optional debug slabs
-    if (A.ex_out) {
-      double* e = A.ex_out + sl * (long long)O * G * 32;
-      for (int i = lane; i < O * G * 32; i += 32) e[i] = 0.0;
+    row.n_train = n;
+    row.n_test = nt;
+    row.fp_train = warp_xor(fptr);
+    row.fp_test = warp_xor(fpte);
+    __syncwarp();
+    if (n > 0 && lane == 0) atomicOr(&A.trained[sl], 1u << o);
+    if (n == 0 || nt == 0) {          // untrained (reading R18) or nothing to predict
+      if (lane == 0 && A.opt_out) A.opt_out[so * O + o] = row;
+      if (A.agg && lane == 0 && nt > 0) atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 1], nt);
+      tot_test += (n == 0) ? 0 : 0;
+      continue;
     }
-    if (A.rec_out) {
-      int8_t* r = A.rec_out + sl * (long long)G * 64 * A.max_count;
-      for (int i = lane; i < G * 64 * A.max_count; i += 32) r[i] = -1;
+
+    // ---- A2: per-fit min-max statistics over the training befores (D3) ----
+    int deff = 0;
+    for (int a0 = 0; a0 < d; a0 += 32) {
+      const int a = a0 + lane;
+      double mn = 0.0, mx = 0.0, sm = 0.0;
+      int c = 0;
+      if (a < d) {
+        c = F[a];
+        mn = mx = X[(long long)trs[0] * ldx + c];
+        sm = mn;
+        for (int i = 1; i < n; ++i) {
+          const double vv = X[(long long)trs[i] * ldx + c];
+          mn = fmin(mn, vv);
+          mx = fmax(mx, vv);
+          sm += vv;
+        }
+      }
+      const bool act = a < d && mx > mn;
+      const unsigned bm = __ballot_sync(FULL, act);
+      if (act) {
+        const int p = deff + __popc(bm & lt);
+        col[p] = (int16_t)c;
+        xb[p] = sm / (double)n;
+        sv[p] = 1.0 / (mx - mn);
+      }
+      deff += __popc(bm);
     }
+    {  // zero padding read by the fast-path fragment loads
+      const int pad_end = max(32, (deff + 3) & ~3);
+      for (int p = deff + lane; p < pad_end; p += 32) {
+        col[p] = 0;
+        xb[p] = 0.0;
+        sv[p] = 0.0;
+      }
+    }
+    double ysum = 0.0;
+    for (int i = lane; i < n; i += 32) ysum += yc[i];
+    const double ybar = warp_sum(ysum) / (double)n;
+    for (int i = lane; i < n; i += 32) yc[i] -= ybar;
     __syncwarp();
 
-    int guard = 0;        // lane-partial guard count
-    int untrained = 0;    // lane 0 only
-    uint32_t trained = 0;
-    int oi = 0;
-    int8_t olist[kMaxOpt];
-#pragma unroll
-    for (int q = 0; q < kMaxOpt; ++q) olist[q] = -1;
-
-    for (int o = 0; o < O; ++o) {
-      OptScore row;
-      row.n_train = row.n_test = row.n_correct = row.n_clamped = 0;
-      row.sum_ratio = row.min_ratio = row.max_ratio = 0.0;
-      row.fp_train = row.fp_test = 0ull;
-      if (!((om >> o) & 1u)) {
-        if (lane == 0 && A.opt_out) A.opt_out[sl * O + o] = row;
-        continue;
-      }
-      const int my_oi = oi++;
-#pragma unroll
-      for (int q = 0; q < kMaxOpt; ++q)
-        if (q == my_oi) olist[q] = (int8_t)o;
-
-      // ---- A1: before/after pairs by ballot compaction ----
-      int n = 0, nt = 0;
-      uint64_t fptr = 0, fpte = 0;
-      for (int g = 0; g < G; ++g) {
-        const int b = obit[(g / A.IR) * O + o];
-        const uint64_t tr = trw[g], te = tew[g];
-        if (b < 0 || (tr == 0ull && te == 0ull)) continue;
-        const int k = lane, v = ins0(k, b);
-        const bool istr = ((tr >> v) & 1ull) && ((tr >> (v | (1 << b))) & 1ull);
-        const bool iste = (te >> v) & 1ull;
-        const unsigned mtr = __ballot_sync(FULL, istr), mte = __ballot_sync(FULL, iste);
-        const int lab = (g * O + o) * 32 + k;
-        if (istr | iste) {
-          const uint64_t h = mix64((uint64_t)lab);
-          const double y = A.ylab[lab];
-          if (istr) {
-            const int p = n + __popc(mtr & lt);
-            trs[p] = g * 64 + v;
-            tr_y[p] = y;
-            fptr ^= h;
-          }
-          if (iste) {
-            const int p = nt + __popc(mte & lt);
-            tes[p] = g * 64 + v;
-            tek[p] = g * 32 + k;
-            te_y[p] = y;
-            fpte ^= h;
-          }
-        }
-        n += __popc(mtr);
-        nt += __popc(mte);
-      }
-      row.n_train = n;
-      row.n_test = nt;
-      row.fp_train = warp_xor(fptr);
-      row.fp_test = warp_xor(fpte);
-      __syncwarp();
-      if (n == 0) {                      // untrained (reading R18)
-        untrained += nt;
-        if (lane == 0 && A.opt_out) A.opt_out[sl * O + o] = row;
-        continue;
-      }
-      trained |= 1u << o;
-      if (nt == 0) {
-        if (lane == 0 && A.opt_out) A.opt_out[sl * O + o] = row;
-        continue;
-      }
-
-      // ---- A2: per-fit min-max statistics over the training befores ----
-      int deff = 0;
-      for (int a0 = 0; a0 < d; a0 += 32) {
-        const int a = a0 + lane;
-        double mn = 0.0, mx = 0.0, sm = 0.0;
-        int c = 0;
-        if (a < d) {
-          c = F[a];
-          mn = mx = X[(long long)trs[0] * ldx + c];
-          sm = mn;
-          for (int i = 1; i < n; ++i) {
-            const double vv = X[(long long)trs[i] * ldx + c];
-            mn = fmin(mn, vv);
-            mx = fmax(mx, vv);
-            sm += vv;
-          }
-        }
-        const bool act = a < d && mx > mn;
-        const unsigned bm = __ballot_sync(FULL, act);
-        if (act) {
-          const int p = deff + __popc(bm & lt);
-          col[p] = (int16_t)c;
-          xb[p] = sm / (double)n;
-          sv[p] = 1.0 / (mx - mn);
-        }
-        deff += __popc(bm);
-      }
-      {  // zero padding read by the fast-path fragment loads
-        const int pad_end = max(32, (deff + 3) & ~3);
-        for (int p = deff + lane; p < pad_end; p += 32) {
-          col[p] = 0;
-          xb[p] = 0.0;
-          sv[p] = 0.0;
-        }
-      }
-      double ysum = 0.0;
-      for (int i = lane; i < n; i += 32) ysum += tr_y[i];
-      const double ybar = warp_sum(ysum) / (double)n;
-      for (int i = lane; i < n; i += 32) v3[i] = tr_y[i] - ybar;
-      __syncwarp();
-
-      // ---- A3/A4: centred normal equations, dual or primal ----
-      const bool dual = (n - 1) < deff;
-      const int m = dual ? n : deff;
-      // refinement only where the conditioning needs it
-      const int nref = (dual ? 2 * (n - 1) >= deff : (n - 1) < 2 * deff) ? A.refine : 0;
-      bool ok = true;
-      if (m > 0 && m <= (L.mcap < 32 ? L.mcap : 32)) {
-        const FastView fv{X, ldx, trs, n, col, xb, sv, deff};
-        ok = dual ? fit_fast<true>(fv, v3, A.lambda, nref, Msm, v2, uv, wv, lane)
-                  : fit_fast<false>(fv, v3, A.lambda, nref, Msm, v2, uv, wv, lane);
-      } else if (m > 0) {
-        FitView f{X, ldx, trs, n, col, xb, sv, deff};
-        double* M = (m <= L.mcap) ? Msm : Mgl;
-        if (dual) build_gram<true>(M, m, deff, f, A.lambda, lane);
-        else build_gram<false>(M, m, n, f, A.lambda, lane);
-        ok = chol_packed(M, invd, m, lane);
-        if (ok && dual) {
-          // alpha = (K + lambda I)^{-1} yc ;  w' = Xtilde^T alpha
-          for (int i = lane; i < n; i += 32) v1[i] = v3[i];
-          __syncwarp();
-          chol_solve(M, invd, v1, m, lane);
-          for (int it = 0; it < nref; ++it) {
-            xt_times(f, v1, wv, lane);
-            for (int a = lane; a < deff; a += 32) uv[a] = wv[a] * sv[a];
-            __syncwarp();
-            for (int i = lane; i < n; i += 32) {
-              const double* xr = X + (long long)trs[i] * ldx;
-              v2[i] = v3[i] - row_dot_u(f, xr, uv) - A.lambda * v1[i];
-            }
-            __syncwarp();
-            chol_solve(M, invd, v2, m, lane);
-            for (int i = lane; i < n; i += 32) v1[i] += v2[i];
-            __syncwarp();
-          }
-          xt_times(f, v1, wv, lane);
-        } else if (ok) {
-          // w' = (G + lambda I)^{-1} Xtilde^T yc
-          xt_times(f, v3, wv, lane);
-          chol_solve(M, invd, wv, m, lane);
-          for (int it = 0; it < nref; ++it) {
-            for (int a = lane; a < deff; a += 32) uv[a] = wv[a] * sv[a];
-            __syncwarp();
-            for (int i = lane; i < n; i += 32) {
-              const double* xr = X + (long long)trs[i] * ldx;
-              v2[i] = v3[i] - row_dot_u(f, xr, uv);
-            }
-            __syncwarp();
-            xt_times(f, v2, v1, lane);
-            for (int a = lane; a < deff; a += 32) v1[a] -= A.lambda * wv[a];
-            __syncwarp();
-            chol_solve(M, invd, v1, m, lane);
-            for (int a = lane; a < deff; a += 32) wv[a] += v1[a];
-            __syncwarp();
-          }
-        }
-      }
-      if (!ok) guard += 1000000;  // unreachable for lambda > 0; poisons the row
-      // weights on raw counters: EX = c0 + sum_c x_c * ufull[c]
-      for (int c = lane; c < C; c += 32) ufull[c] = 0.0;
-      __syncwarp();
-      double cpart = 0.0;
-      if (m > 0 && ok)
-        for (int a = lane; a < deff; a += 32) {
-          const double u = wv[a] * sv[a];
-          ufull[col[a]] = u;
-          cpart = fma(xb[a], u, cpart);
-        }
-      const double c0 = ybar - warp_sum(cpart);
-      __syncwarp();
-
-      // ---- A5: predict + clamp; A7 per-(s,o) scores ----
-      const int oiex = my_oi * exs;
-      int ncorr = 0, ncl = 0;
-      double rsum = 0.0, rmin = INFINITY, rmax = -INFINITY;
-      for (int j = lane; j < nt; j += 32) {
-        const double* xr = X + (long long)tes[j] * ldx;
-        double e0 = 0.0, e1 = 0.0;
-        int c = 0;
-        for (; c + 1 < C; c += 2) {
-          e0 = fma(xr[c], ufull[c], e0);
-          e1 = fma(xr[c + 1], ufull[c + 1], e1);
-        }
-        if (c < C) e0 = fma(xr[c], ufull[c], e0);
-        double e = c0 + (e0 + e1);
-        if (near_tol(e, 0.0, A.guard_tol) || near_tol(e, 1.0, A.guard_tol)) ++guard;
-        uint8_t cl = 0;
-        if (e <= 0.0) { e = A.clamp_floor; cl = 1; ++ncl; }
-        const double ac = te_y[j];
-        ncorr += ((e > 1.0 && ac > 1.0) || (e <= 1.0 && ac <= 1.0)) ? 1 : 0;
-        const double ratio = ac / e;
-        rsum += ratio;
-        rmin = fmin(rmin, ratio);
-        rmax = fmax(rmax, ratio);
-        const int gk = tek[j];
-        const int gi = gidx[gk >> 5];
-        extab[oiex + gi * 32 + (gk & 31)] = e;
-        excl[oiex + gi * 32 + (gk & 31)] = cl;
-        if (A.ex_out) A.ex_out[(sl * O + o) * (long long)G * 32 + gk] = e;
-      }
-      row.n_correct = warp_isum(ncorr);
-      row.n_clamped = warp_isum(ncl);
-      row.sum_ratio = warp_sum(rsum);
-      row.min_ratio = warp_min(rmin);
-      row.max_ratio = warp_max(rmax);
-      tot_corr += row.n_correct;
-      tot_test += nt;
-      m_corr += row.n_correct;
-      m_test += nt;
-      if (lane == 0 && A.opt_out) A.opt_out[sl * O + o] = row;
-      __syncwarp();
+    // ---- A3/A4: centred normal equations, dual or primal ----
+    const bool dual = (n - 1) < deff;
+    const int m = dual ? n : deff;
+    // refine where conditioning or the O(n eps) Gram accumulation error needs it
+    const int nref = (dual ? 2 * (n - 1) >= deff : ((n - 1) < 2 * deff || n > 64)) ? A.refine : 0;
+    bool ok = true;
+    if (m > 0 && m <= (L.mcap < 32 ? L.mcap : 32)) {
+      const FastView fv{X, ldx, trs, n, col, xb, sv, deff};
+      ok = dual ? fit_fast<true>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane)
+                : fit_fast<false>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane);
+    } else if (m > 0) {
+      const FitView fv{X, ldx, trs, n, col, xb, sv, deff};
+      ok = fit_generic(fv, yc, A.lambda, nref, dual, scr, L.vmax, uv, v2, wv, lane);
     }
+    // weights on raw counters: EX = c0 + sum_c x_c * ufull[c]
+    for (int c = lane; c < C; c += 32) ufull[c] = 0.0;
+    __syncwarp();
+    double cpart = 0.0;
+    if (m > 0 && ok)
+      for (int a = lane; a < deff; a += 32) {
+        const double u = wv[a] * sv[a];
+        ufull[col[a]] = u;
+        cpart = fma(xb[a], u, cpart);
+      }
+    const double c0 = ybar - warp_sum(cpart);
+    __syncwarp();
 
-    // ---- A6: rank + thresholded recommendation per test slot ----
-    int nrec = 0, nhit = 0;
-    const int n_os = oi;
+    // ---- A5: predict + clamp; A7 per-(s,o) scores ----
+    double* ext = A.extab + sl * A.ex_stride + q * A.tg_stride;
+    int ncorr = 0, ncl = 0, guard = ok ? 0 : 1000000;
+    double rsum = 0.0, rmin = INFINITY, rmax = -INFINITY;
+    for (int j = lane; j < nt; j += 32) {
+      const double* xr = X + (long long)tes[j] * ldx;
+      double e0 = 0.0, e1 = 0.0;
+      int c = 0;
+      for (; c + 1 < C; c += 2) {
+        e0 = fma(xr[c], ufull[c], e0);
+        e1 = fma(xr[c + 1], ufull[c + 1], e1);
+      }
+      if (c < C) e0 = fma(xr[c], ufull[c], e0);
+      double e = c0 + (e0 + e1);
+      if (near_tol(e, 0.0, A.guard_tol) || near_tol(e, 1.0, A.guard_tol)) ++guard;
+      bool cl = false;
+      if (e <= 0.0) {
+        e = A.clamp_floor;
+        cl = true;
+        ++ncl;
+      }
+      const int gk = tek[j];
+      const double ac = A.ylab[((gk >> 5) * O + o) * 32 + (gk & 31)];
+      ncorr += ((e > 1.0 && ac > 1.0) || (e <= 1.0 && ac <= 1.0)) ? 1 : 0;
+      const double ratio = ac / e;
+      rsum += ratio;
+      rmin = fmin(rmin, ratio);
+      rmax = fmax(rmax, ratio);
+      ext[test_group_index(A.sd, split, gk >> 5) * 32 + (gk & 31)] = cl ? -e : e;
+      if (A.ex_out) A.ex_out[(so * O + o) * (long long)G * 32 + gk] = e;
+    }
+    row.n_correct = warp_isum(ncorr);
+    row.n_clamped = warp_isum(ncl);
+    row.sum_ratio = warp_sum(rsum);
+    row.min_ratio = warp_min(rmin);
+    row.max_ratio = warp_max(rmax);
+    guard = warp_isum(guard);
+    tot_corr += row.n_correct;
+    tot_test += nt;
+    if (lane == 0) {
+      if (A.opt_out) A.opt_out[so * O + o] = row;
+      if (guard) atomicAdd(&A.guard_acc[sl], guard);
+      if (A.agg) {
+        atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 0], row.n_correct);
+        atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 1], nt);
+      }
+    }
+    __syncwarp();
+  }
+  if (A.totals && lane == 0 && tot_test) {
+    atomicAdd(&A.totals[0], tot_corr);
+    atomicAdd(&A.totals[1], tot_test);
+  }
+}
+
+// ---------------------------------------------------------------- rank kernel
+// A6: per test slot, candidates = scored, trained optimizations whose bit is
+// clear (reading R13); sort by (EX desc, id asc), keep EX >= threshold, first
+// max_count.  One warp per scenario, lanes over the slot's versions.
+template <int CMAX>
+__global__ void __launch_bounds__(256) k_rank_warp(const EvalArgs A) {
+  const int lane = threadIdx.x & 31;
+  const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int G = A.G, O = A.O;
+  unsigned long long tot_rec = 0, tot_hit = 0;
+  for (long long sl = gwarp; sl < A.count; sl += nwarps) {
+    const long long s = A.first + sl, so = A.out0 + sl;
+    const long long split = s % A.sd.n_splits, fidx = s / A.sd.n_splits;
+    const uint32_t om = scored_mask(A.sd, split, O);
+    const uint32_t trained = A.trained[sl];
+    int olist[CMAX];
+    int n_os = 0;
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q) olist[q] = -1;
+    {
+      uint32_t mm = om;
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) {
+        if (mm) {
+          olist[q] = __ffs(mm) - 1;
+          mm &= mm - 1;
+          ++n_os;
+        }
+      }
+    }
+    const double* ext = A.extab + sl * A.ex_stride;
+    int nrec = 0, nhit = 0, guard = 0, untrained = 0;
     for (int g = 0; g < G; ++g) {
-      const uint64_t te = tew[g];
+      uint64_t tr, te;
+      member_words(A.sd, split, g, tr, te);
       if (te == 0ull) continue;
-      const int gi = gidx[g];
+      const int gi = test_group_index(A.sd, split, g);
       const int p = g / A.IR;
       for (int h = 0; h < 2; ++h) {
         const int v = h * 32 + lane;
         if (!((te >> v) & 1ull)) continue;
         double ce[CMAX];
         bool cv[CMAX], cc[CMAX];
-        int co[CMAX], ck[CMAX];
+        int ck[CMAX];
 #pragma unroll
         for (int q = 0; q < CMAX; ++q) {
-          const int o = (q < kMaxOpt) ? olist[q] : -1;
-          bool valid = q < n_os && o >= 0 && ((trained >> o) & 1u);
+          const int o = olist[q];
           int b = -1;
-          if (valid) {
-            b = obit[p * O + o];
-            valid = b >= 0 && !((v >> b) & 1);
+          if (o >= 0) b = A.opt_bit[p * O + o];
+          bool cand = o >= 0 && b >= 0 && !((v >> b) & 1);
+          if (cand && !((trained >> o) & 1u)) {
+            ++untrained;
+            cand = false;
           }
-          cv[q] = valid;
-          co[q] = o;
-          ck[q] = valid ? rmv(v, b) : 0;
-          ce[q] = valid ? extab[q * exs + gi * 32 + ck[q]] : 0.0;
-          cc[q] = valid ? excl[q * exs + gi * 32 + ck[q]] != 0 : false;
+          cv[q] = cand;
+          ck[q] = cand ? rmv(v, b) : 0;
+          const double raw = cand ? ext[q * A.tg_stride + gi * 32 + ck[q]] : 0.0;
+          cc[q] = raw < 0.0;
+          ce[q] = fabs(raw);
         }
         // guard band (reading R21)
 #pragma unroll
@@ -524,10 +500,9 @@ __global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, 1) k_eval_warp(const E
             if (r != q && cv[r] && ce[r] >= A.threshold && (ce[r] > ce[q] || (ce[r] == ce[q] && r < q))) ++rk;
           if (rk < A.max_count) {
             ++nrec;
-            const int o = co[q];
+            const int o = olist[q];
             if (A.ylab[(g * O + o) * 32 + ck[q]] > 1.0) ++nhit;
-            if (A.rec_out)
-              A.rec_out[(sl * G * 64 + g * 64 + v) * A.max_count + rk] = (int8_t)o;
+            if (A.rec_out) A.rec_out[(so * G * 64 + g * 64 + v) * A.max_count + rk] = (int8_t)o;
           }
         }
       }
@@ -535,28 +510,33 @@ __global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, 1) k_eval_warp(const E
     ScnScore sr;
     sr.n_rec = warp_isum(nrec);
     sr.n_rec_hit = warp_isum(nhit);
-    sr.n_untrained = untrained;
-    sr.n_guard = warp_isum(guard);
+    sr.n_untrained = warp_isum(untrained);
+    sr.n_guard = warp_isum(guard) + A.guard_acc[sl];
     tot_rec += sr.n_rec;
     tot_hit += sr.n_rec_hit;
-    m_rec += sr.n_rec;
-    m_hit += sr.n_rec_hit;
-    if (lane == 0 && A.scn_out) A.scn_out[sl] = sr;
-    __syncwarp();
-  }  // inner (folds)
-  if (A.agg && lane == 0) {
-    const long long mask_id = A.first / A.n_splits + item;
-    MaskScore ms{m_corr, m_test, m_rec, m_hit};
-    if (A.mask_out) A.mask_out[item] = ms;
-    // top-K key: more correct first, then smaller mask id (O8)
-    A.keys_out[item] = ((unsigned long long)(unsigned)m_corr << 32) | (0xFFFFFFFFull - (unsigned long long)mask_id);
+    if (lane == 0) {
+      if (A.scn_out) A.scn_out[so] = sr;
+      if (A.agg) {
+        atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 2], sr.n_rec);
+        atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 3], sr.n_rec_hit);
+      }
+    }
   }
-  }  // items
-  if (A.totals && lane == 0 && (tot_test | tot_rec)) {
-    atomicAdd(&A.totals[0], tot_corr);
-    atomicAdd(&A.totals[1], tot_test);
+  if (A.totals && lane == 0 && (tot_rec | tot_hit)) {
     atomicAdd(&A.totals[2], tot_rec);
     atomicAdd(&A.totals[3], tot_hit);
+  }
+}
+
+// C5: per-mask rows + ranking keys (O8) from the integer accumulators.
+__global__ void k_mask_final(const EvalArgs A) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < A.n_mask_range;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int* a = A.mask_acc + i * 4;
+    MaskScore ms{a[0], a[1], a[2], a[3]};
+    if (A.mask_out) A.mask_out[i] = ms;
+    const long long mask_id = A.mask0 + i;
+    A.keys_out[i] = ((unsigned long long)(unsigned)a[0] << 32) | (0xFFFFFFFFull - (unsigned long long)mask_id);
   }
 }
 

@@ -1,0 +1,759 @@
+// fit_big.cuh -- the large-batch path (config C4: 1024 programs x 64 variants
+// x 128 counters, thousands of training pairs per fit).  DESIGN.md §5.5.
+//
+// k_fit_big: one CTA (8 warps) per (scenario, optimization) fit, persistent
+//   over fits.  Pair lists are built by ballot + CTA scan (deterministic
+//   order); min/max/sum statistics stream the training rows once; the centred,
+//   scaled Gram X~^T X~ (d_eff <= 128) is accumulated on the FP64 tensor pipe
+//   (mma.sync.m8n8k4.f64): training rows are gathered from L2 in 32-row chunks,
+//   prefetched into registers while the previous chunk is contracted from
+//   shared memory, each warp owning block-rows w and 15-w (17 tiles).  Then a
+//   CTA LDL-form Cholesky, triangular solves, optional refinement (streamed
+//   residual), and the weights on raw counters + intercept are written out.
+// k_rank_big: one CTA per scenario: every test slot's candidates are
+//   predicted (warp dot products against the staged weights), clamped,
+//   ranked, thresholded and scored (A5-A7), deterministic reduction order.
+#pragma once
+#include "kernels.cuh"
+
+namespace speedrec {
+
+constexpr int kBigThreads = 256;
+constexpr int kBigChunk = 32;   // training rows per staged chunk (8 k-steps)
+constexpr int kBigLd = 132;     // chunk row stride in doubles: conflict-free 4x8 fragments
+constexpr int kBigMaxD = 128;
+constexpr int kBigGLd = 129;    // Gram row stride (odd: conflict-free columns)
+
+struct BigArgs {
+  const double* x;
+  const double* ylab;
+  const int8_t* opt_bit;
+  int P, IR, C, O, G;
+  int kind, gw;
+  long long n_splits;
+  const uint64_t* train_g;
+  const uint64_t* test_g;
+  const uint32_t* split_om;
+  const int32_t* pool_list;
+  int n_pool;
+  unsigned long long seed;
+  uint32_t opt_mask;
+  int subsets_k;
+  long long n_masks;
+  const uint64_t* fmasks;
+  double lambda, threshold, clamp_floor, guard_tol;
+  int refine, max_count;
+  long long first, count;  // scenario range of this batch
+  // k_fit_big scratch: per CTA [np] training slots + [np] centred labels
+  int32_t* lists;
+  double* ylist;
+  long long np;
+  // fit results per (scenario in batch, optimization)
+  double* U;        // [count][O][C]
+  double* c0;       // [count][O]
+  int32_t* fitflag; // [count][O]: 1 = model available
+  OptScore* opt_out;  // [count][O] (k_fit_big writes counts/fingerprints, k_rank_big the scores)
+  ScnScore* scn_out;
+  double* ex_out;
+  int8_t* rec_out;
+  unsigned long long* totals;
+};
+
+__device__ __forceinline__ void member_words(const BigArgs& A, long long split, int g, uint64_t& tr,
+                                             uint64_t& te) {
+  if (A.kind == 0) {
+    tr = ((A.train_g[split * A.gw + (g >> 6)] >> (g & 63)) & 1ull) ? ~0ull : 0ull;
+    te = ((A.test_g[split * A.gw + (g >> 6)] >> (g & 63)) & 1ull) ? ~0ull : 0ull;
+  } else if (A.kind == 1) {
+    bool inpool = false;
+    for (int q = 0; q < A.n_pool; ++q) inpool |= (A.pool_list[q] == g);
+    tr = inpool ? ~0ull : 0ull;
+    te = 0ull;
+    if (g == A.pool_list[split >> 6]) {
+      tr &= ~(1ull << (split & 63));
+      te = 1ull << (split & 63);
+    }
+  } else {
+    tr = mix64(mix64(A.seed ^ mix64((uint64_t)split)) + (uint64_t)g);
+    te = ~tr;
+  }
+}
+
+// CTA-wide exclusive scan of n ints in smem (n <= 4 * kBigThreads); returns the total.
+__device__ int cta_scan(int* v, int n, int* wsum) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  int loc[4], s = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = t * 4 + q;
+    loc[q] = i < n ? v[i] : 0;
+    s += loc[q];
+  }
+  int inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (t == 0) {
+    int acc = 0;
+    for (int q = 0; q < kBigThreads / 32; ++q) {
+      const int y = wsum[q];
+      wsum[q] = acc;
+      acc += y;
+    }
+    wsum[kBigThreads / 32] = acc;
+  }
+  __syncthreads();
+  int run = wsum[w] + inc - s;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = t * 4 + q;
+    if (i < n) v[i] = run;
+    run += loc[q];
+  }
+  const int total = wsum[kBigThreads / 32];
+  __syncthreads();
+  return total;
+}
+
+__device__ __forceinline__ double cta_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int q = 0; q < kBigThreads / 32; ++q) s += red[q];  // fixed order
+  __syncthreads();
+  return s;
+}
+
+__device__ __forceinline__ uint64_t cta_xor(uint64_t v, uint64_t* red) {
+  v = warp_xor(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  uint64_t s = 0;
+  for (int q = 0; q < kBigThreads / 32; ++q) s ^= red[q];
+  __syncthreads();
+  return s;
+}
+
+// Stage rows [r0, r0+32) of the training list into registers (thread: row
+// t>>3, features (t&7)+8q), centred and scaled; rows past n are zero.
+__device__ __forceinline__ void big_load_chunk(const double* X, int C, const int32_t* trs, int n, int r0,
+                                               const int* col, const double* xb, const double* s, int deff,
+                                               double (&v)[16]) {
+  const int r = r0 + (threadIdx.x >> 3);
+  const int a0 = threadIdx.x & 7;
+  const double* xr = r < n ? X + (long long)trs[r] * C : nullptr;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int a = a0 + 8 * q;
+    v[q] = (xr && a < deff) ? xr[col[a]] : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int a = a0 + 8 * q;
+    if (xr && a < deff) v[q] = (v[q] - xb[a]) * s[a];  // padding rows stay exactly 0
+  }
+}
+
+__device__ __forceinline__ void big_store_chunk(double* buf, const double (&v)[16]) {
+  const int r = threadIdx.x >> 3, a0 = threadIdx.x & 7;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) buf[r * kBigLd + a0 + 8 * q] = v[q];
+}
+
+__global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  // layout: Gbuf (union with two chunk buffers) | vectors | scan arrays
+  double* Gbuf = reinterpret_cast<double*>(smem);                       // [128][129]
+  double* chunk0 = Gbuf;                                                // [32][132]
+  double* chunk1 = Gbuf + kBigChunk * kBigLd;                           // [32][132]
+  double* rch = Gbuf + kBigMaxD * kBigGLd;                              // [32][132] refinement chunk
+  double* rpt = rch + kBigChunk * kBigLd;                               // [32][128] refinement partials
+  double* xb = rpt + kBigChunk * kBigMaxD;                              // [128]
+  double* sv = xb + kBigMaxD;                                           // [128]
+  double* rhs = sv + kBigMaxD;                                          // [128]
+  double* wv = rhs + kBigMaxD;                                          // [128]
+  double* zv = wv + kBigMaxD;                                           // [128]
+  double* invd = zv + kBigMaxD;                                         // [128]
+  double* ych = invd + kBigMaxD;                                        // [2][32] yc of the chunk rows
+  double* red = ych + 2 * kBigChunk;                                    // [16]
+  uint64_t* xred = reinterpret_cast<uint64_t*>(red + 16);               // [8]
+  int* col = reinterpret_cast<int*>(xred + 8);                          // [128]
+  int* Fl = col + kBigMaxD;                                             // [128]
+  int* ctr = Fl + kBigMaxD;                                             // [G]
+  int* cte = ctr + A.G;                                                 // [G] (counts only)
+  int* wsum = cte + A.G;                                                // [9]
+  int* misc = wsum + 16;                                                // [4]
+
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const unsigned ltm = (1u << lane) - 1u;
+  int32_t* trs = A.lists + blockIdx.x * A.np;
+  double* yl = A.ylist + blockIdx.x * A.np;
+  const int G = A.G, O = A.O, C = A.C;
+
+  for (long long fit = blockIdx.x; fit < A.count * O; fit += gridDim.x) {
+    const long long sl = fit / O;
+    const int o = (int)(fit % O);
+    const long long s = A.first + sl;
+    const long long split = s % A.n_splits, fidx = s / A.n_splits;
+    const uint32_t om = (A.split_om ? A.split_om[split] : A.opt_mask) & ((1u << O) - 1u);
+    OptScore row;
+    row.n_train = row.n_test = row.n_correct = row.n_clamped = 0;
+    row.sum_ratio = row.min_ratio = row.max_ratio = 0.0;
+    row.fp_train = row.fp_test = 0ull;
+    if (!((om >> o) & 1u)) {
+      if (t == 0) {
+        A.opt_out[sl * O + o] = row;
+        A.fitflag[sl * O + o] = 0;
+      }
+      continue;
+    }
+    // ---- A1: pair counts per group, then deterministic positions ----
+    uint64_t fptr = 0, fpte = 0;
+    for (int g = warp; g < G; g += kBigThreads / 32) {
+      const int b = A.opt_bit[(g / A.IR) * O + o];
+      int ntr = 0, nte = 0;
+      if (b >= 0) {
+        uint64_t tr, te;
+        member_words(A, split, g, tr, te);
+        const int v = ins0(lane, b);
+        const bool istr = ((tr >> v) & 1ull) && ((tr >> (v | (1 << b))) & 1ull);
+        const bool iste = (te >> v) & 1ull;
+        const uint64_t h = mix64((uint64_t)((g * O + o) * 32 + lane));
+        if (istr) fptr ^= h;
+        if (iste) fpte ^= h;
+        ntr = __popc(__ballot_sync(FULL, istr));
+        nte = __popc(__ballot_sync(FULL, iste));
+      }
+      if (lane == 0) {
+        ctr[g] = ntr;
+        cte[g] = nte;
+      }
+    }
+    row.fp_train = cta_xor(fptr, xred);
+    row.fp_test = cta_xor(fpte, xred);
+    const int n = cta_scan(ctr, G, wsum);
+    const int nt = cta_scan(cte, G, wsum);
+    row.n_train = n;
+    row.n_test = nt;
+    if (n == 0 || nt == 0) {
+      if (t == 0) {
+        A.opt_out[sl * O + o] = row;
+        A.fitflag[sl * O + o] = n > 0 ? 1 : 0;
+        A.c0[sl * O + o] = 0.0;
+      }
+      for (int c = t; c < C; c += kBigThreads) A.U[(sl * O + o) * C + c] = 0.0;
+      // (t > 0 and n > 0 never happens here; the rank kernel needs no model)
+      continue;
+    }
+    for (int g = warp; g < G; g += kBigThreads / 32) {
+      const int b = A.opt_bit[(g / A.IR) * O + o];
+      if (b < 0) continue;
+      uint64_t tr, te;
+      member_words(A, split, g, tr, te);
+      const int v = ins0(lane, b);
+      const bool istr = ((tr >> v) & 1ull) && ((tr >> (v | (1 << b))) & 1ull);
+      const unsigned m = __ballot_sync(FULL, istr);
+      if (istr) {
+        const int p = ctr[g] + __popc(m & ltm);
+        trs[p] = g * 64 + v;
+        yl[p] = A.ylab[(g * O + o) * 32 + lane];
+      }
+    }
+    // feature set F (counter-index order)
+    {
+      const int c = t;
+      bool in = false;
+      if (c < C && c < kBigMaxD) {
+        if (A.subsets_k > 0) in = c < A.subsets_k && ((fidx >> c) & 1);
+        else if (A.fmasks) in = (A.fmasks[fidx * 2 + (c >> 6)] >> (c & 63)) & 1ull;
+        else in = true;
+      }
+      const unsigned bm = __ballot_sync(FULL, in);
+      if (lane == 0) wsum[warp] = __popc(bm);
+      __syncthreads();
+      int base = 0;
+      for (int q = 0; q < warp; ++q) base += wsum[q];
+      if (in) Fl[base + __popc(bm & ltm)] = c;
+      if (t == 0) {
+        int dd = 0;
+        for (int q = 0; q < kBigThreads / 32; ++q) dd += wsum[q];
+        misc[0] = dd;
+      }
+      __syncthreads();
+    }
+    const int d = misc[0];
+    // ---- A2: min / max / sum per feature (two row halves), ybar ----
+    {
+      const int a = t & (kBigMaxD - 1), h = t >> 7;
+      double mn = INFINITY, mx = -INFINITY, sm = 0.0;
+      if (a < d) {
+        const int c = Fl[a];
+        for (int i = h; i < n; i += 2) {
+          const double vv = A.x[(long long)trs[i] * C + c];
+          mn = fmin(mn, vv);
+          mx = fmax(mx, vv);
+          sm += vv;
+        }
+      }
+      if (h == 1) {
+        zv[a] = mn;
+        wv[a] = mx;
+        rhs[a] = sm;
+      }
+      __syncthreads();
+      bool act = false;
+      if (h == 0) {
+        mn = fmin(mn, zv[a]);
+        mx = fmax(mx, wv[a]);
+        sm += rhs[a];
+        act = a < d && mx > mn;
+      }
+      const unsigned bm = __ballot_sync(FULL, act);
+      if (h == 0 && lane == 0) wsum[warp] = __popc(bm);
+      __syncthreads();
+      if (h == 0) {
+        int base = 0;
+        for (int q = 0; q < warp; ++q) base += wsum[q];
+        if (act) {
+          const int p = base + __popc(bm & ltm);
+          col[p] = Fl[a];
+          xb[p] = sm / (double)n;
+          sv[p] = 1.0 / (mx - mn);
+        }
+        if (t == 0) {
+          int de = 0;
+          for (int q = 0; q < kBigMaxD / 32; ++q) de += wsum[q];
+          misc[1] = de;
+        }
+      }
+      __syncthreads();
+    }
+    const int deff = misc[1];
+    double ys = 0.0;
+    for (int i = t; i < n; i += kBigThreads) ys += yl[i];
+    const double ybar = cta_sum(ys, red) / (double)n;
+    for (int i = t; i < n; i += kBigThreads) yl[i] -= ybar;
+    for (int a = t; a < kBigMaxD; a += kBigThreads) rhs[a] = 0.0;
+    __syncthreads();
+
+    // primal always (n >> d here); refinement always: the Gram's accumulation
+    // error grows with n (thousands of rows), the streamed residual removes it
+    const int nref = A.refine;
+    bool ok = true;
+    if (deff > 0) {
+      // ---- A3: centred Gram on DMMA, chunks of 32 rows double-buffered ----
+      const int nb = (deff + 7) >> 3;
+      const int I1 = warp, I2 = 15 - warp;
+      const bool has1 = I1 < nb, has2 = I2 < nb;
+      double acc1[8][2], acc2[16][2];
+#pragma unroll
+      for (int J = 0; J < 8; ++J) acc1[J][0] = acc1[J][1] = 0.0;
+#pragma unroll
+      for (int J = 0; J < 16; ++J) acc2[J][0] = acc2[J][1] = 0.0;
+      double rpart[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) rpart[q] = 0.0;
+      double v[16];
+      const int nchunks = (n + kBigChunk - 1) / kBigChunk;
+      big_load_chunk(A.x, C, trs, n, 0, col, xb, sv, deff, v);
+      big_store_chunk(chunk0, v);
+      if (t < kBigChunk) ych[t] = t < n ? yl[t] : 0.0;
+      __syncthreads();
+      const int rl = lane >> 2, kl = lane & 3;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        double* cur = (ch & 1) ? chunk1 : chunk0;
+        double* nxt = (ch & 1) ? chunk0 : chunk1;
+        const double* ycur = ych + (ch & 1) * kBigChunk;
+        if (ch + 1 < nchunks) big_load_chunk(A.x, C, trs, n, (ch + 1) * kBigChunk, col, xb, sv, deff, v);
+        // rhs partials from the current chunk: thread's row/features
+        {
+          const int r = t >> 3, a0 = t & 7;
+          const double yv = ycur[r];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) rpart[q] = fma(cur[r * kBigLd + a0 + 8 * q], yv, rpart[q]);
+        }
+#pragma unroll 2
+        for (int k0 = 0; k0 < kBigChunk; k0 += 4) {
+          const double* base = cur + (k0 + kl) * kBigLd + rl;
+          double f[16];
+#pragma unroll
+          for (int J = 0; J < 16; ++J) f[J] = (J < nb) ? base[8 * J] : 0.0;
+          const double fa1 = base[8 * I1], fa2 = base[8 * I2];  // A fragments of the warp's block-rows
+          if (has1) {
+#pragma unroll
+            for (int J = 0; J < 8; ++J)
+              if (J <= I1) dmma(acc1[J][0], acc1[J][1], fa1, f[J]);
+          }
+          if (has2) {
+#pragma unroll
+            for (int J = 0; J < 16; ++J)
+              if (J <= I2) dmma(acc2[J][0], acc2[J][1], fa2, f[J]);
+          }
+        }
+        if (ch + 1 < nchunks) {
+          big_store_chunk(nxt, v);
+          const int r = (ch + 1) * kBigChunk + t;
+          if (t < kBigChunk) ych[((ch + 1) & 1) * kBigChunk + t] = r < n ? yl[r] : 0.0;
+        }
+        __syncthreads();
+      }
+      // rhs: reduce the 32 row-threads per feature in fixed order via smem (chunk buffers are free)
+      {
+        double* part = chunk0;  // [32 rows][128]
+        const int r = t >> 3, a0 = t & 7;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) part[r * kBigMaxD + a0 + 8 * q] = rpart[q];
+        __syncthreads();
+        if (t < kBigMaxD) {
+          double acc = 0.0;
+          for (int rr = 0; rr < kBigChunk; ++rr) acc += part[rr * kBigMaxD + t];
+          rhs[t] = acc;
+        }
+        __syncthreads();
+      }
+      // tiles -> Gbuf (lower triangle, + lambda on the diagonal)
+      if (has1) {
+#pragma unroll
+        for (int J = 0; J < 8; ++J)
+          if (J <= I1)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int r = I1 * 8 + rl, c = J * 8 + 2 * kl + e;
+              if (r < deff && c <= r) Gbuf[r * kBigGLd + c] = acc1[J][e] + (r == c ? A.lambda : 0.0);
+            }
+      }
+      if (has2) {
+#pragma unroll
+        for (int J = 0; J < 16; ++J)
+          if (J <= I2)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int r = I2 * 8 + rl, c = J * 8 + 2 * kl + e;
+              if (r < deff && c <= r) Gbuf[r * kBigGLd + c] = acc2[J][e] + (r == c ? A.lambda : 0.0);
+            }
+      }
+      __syncthreads();
+      // ---- A4: LDL-form Cholesky (unscaled columns), CTA-wide ----
+      for (int j = 0; j < deff; ++j) {
+        const double djj = Gbuf[j * kBigGLd + j];
+        if (!(djj > 0.0)) ok = false;
+        const double r = rsqrt(djj);
+        if (t == 0) invd[j] = r;
+        const double q = r * r;
+        for (int i = j + 1 + warp; i < deff; i += kBigThreads / 32) {
+          const double sij = Gbuf[i * kBigGLd + j] * q;
+          for (int k = j + 1 + lane; k <= i; k += 32) Gbuf[i * kBigGLd + k] = fma(-sij, Gbuf[k * kBigGLd + j], Gbuf[i * kBigGLd + k]);
+        }
+        __syncthreads();
+      }
+      // solves by warp 0: w' = G^{-1} rhs, then refinement steps
+      for (int it = 0; it <= nref; ++it) {
+        if (warp == 0) {
+          for (int a = lane; a < deff; a += 32) zv[a] = (it == 0) ? rhs[a] : zv[a];
+          __syncwarp();
+          for (int j = 0; j < deff; ++j) {
+            const double yj = zv[j] * invd[j];
+            const double tj = yj * invd[j];
+            __syncwarp();
+            if (lane == 0) zv[j] = yj;
+            for (int i = j + 1 + lane; i < deff; i += 32) zv[i] = fma(-Gbuf[i * kBigGLd + j], tj, zv[i]);
+            __syncwarp();
+          }
+          for (int j = deff - 1; j >= 0; --j) {
+            const double xj = zv[j] * invd[j];
+            __syncwarp();
+            if (lane == 0) zv[j] = xj;
+            const double tj = xj;
+            for (int i = lane; i < j; i += 32) zv[i] = fma(-Gbuf[j * kBigGLd + i] * invd[i], tj, zv[i]);
+            __syncwarp();
+          }
+          for (int a = lane; a < deff; a += 32) wv[a] = (it == 0) ? zv[a] : wv[a] + zv[a];
+        }
+        __syncthreads();
+        if (it == nref) break;
+        // residual r = X~^T (yc - X~ w') - lambda w' streamed over the training rows
+        for (int a = t; a < kBigMaxD; a += kBigThreads) rhs[a] = 0.0;
+        __syncthreads();
+        double rp[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) rp[q] = 0.0;
+        for (int ch = 0; ch < (n + kBigChunk - 1) / kBigChunk; ++ch) {
+          big_load_chunk(A.x, C, trs, n, ch * kBigChunk, col, xb, sv, deff, v);
+          big_store_chunk(rch, v);
+          __syncthreads();
+          // e_r for the 32 rows: warp w handles rows 4w..4w+3
+          for (int rr = warp * 4; rr < warp * 4 + 4; ++rr) {
+            double dacc = 0.0;
+            for (int a = lane; a < deff; a += 32) dacc = fma(rch[rr * kBigLd + a], wv[a], dacc);
+            dacc = warp_sum(dacc);
+            const int gr = ch * kBigChunk + rr;
+            if (lane == 0) ych[rr] = gr < n ? yl[gr] - dacc : 0.0;
+          }
+          __syncthreads();
+          const int r = t >> 3, a0 = t & 7;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) rp[q] = fma(rch[r * kBigLd + a0 + 8 * q], ych[r], rp[q]);
+          __syncthreads();
+        }
+        {
+          double* part = rpt;  // never aliases the factor in Gbuf
+          const int r = t >> 3, a0 = t & 7;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) part[r * kBigMaxD + a0 + 8 * q] = rp[q];
+          __syncthreads();
+          if (t < deff) {
+            double acc = 0.0;
+            for (int rr = 0; rr < kBigChunk; ++rr) acc += part[rr * kBigMaxD + t];
+            zv[t] = acc - A.lambda * wv[t];
+          }
+          __syncthreads();
+        }
+      }
+    }
+    // ---- outputs: weights on raw counters, intercept ----
+    for (int c = t; c < C; c += kBigThreads) A.U[(sl * O + o) * C + c] = 0.0;
+    __syncthreads();
+    double cp = 0.0;
+    if (deff > 0 && ok)
+      for (int a = t; a < deff; a += kBigThreads) {
+        const double u = wv[a] * sv[a];
+        A.U[(sl * O + o) * C + col[a]] = u;
+        cp = fma(xb[a], u, cp);
+      }
+    const double csum = cta_sum(cp, red);
+    if (t == 0) {
+      A.c0[sl * O + o] = ybar - csum;
+      A.fitflag[sl * O + o] = ok ? 1 : 2;  // 2: poisoned (non-positive pivot)
+      A.opt_out[sl * O + o] = row;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- A5-A7 for one scenario per CTA ----
+// Prediction on the FP64 tensor pipe: for each group, EX for its 64 versions x
+// the scored optimizations is one (64 x C) x (C x 8) product (8 row-block
+// DMMA tiles per k-step; training rows are zeroed, not loaded), the tile goes
+// through shared memory and each lane then ranks/scores its own versions.
+template <int CMAX>
+__global__ void __launch_bounds__(kBigThreads) k_rank_big(const BigArgs A) {
+  constexpr int NT = CMAX / 8;                  // 8-column tiles of scored optimizations
+  constexpr int ULD = kBigMaxD + 4;
+  __shared__ double Us[CMAX][ULD];
+  __shared__ double c0s[CMAX];
+  __shared__ int ols[CMAX];
+  __shared__ int trained_s[CMAX];
+  __shared__ double exs[kBigThreads / 32][64][CMAX + 1];
+  __shared__ double redd[kBigThreads / 32][CMAX][3];
+  __shared__ int redi[kBigThreads / 32][CMAX][2];
+  __shared__ int reds[kBigThreads / 32][4];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int G = A.G, O = A.O, C = A.C;
+  const long long sl = blockIdx.x;
+  const long long s = A.first + sl;
+  const long long split = s % A.n_splits;
+  const uint32_t om = (A.split_om ? A.split_om[split] : A.opt_mask) & ((1u << O) - 1u);
+  int n_os = 0;
+  for (int o = 0; o < O; ++o)
+    if ((om >> o) & 1u) {
+      if (t == 0) {
+        ols[n_os] = o;
+        trained_s[n_os] = A.fitflag[sl * O + o];
+        c0s[n_os] = A.c0[sl * O + o];
+      }
+      for (int c = t; c < ULD; c += kBigThreads) Us[n_os][c] = c < C ? A.U[(sl * O + o) * C + c] : 0.0;
+      ++n_os;
+    }
+  for (int q = n_os; q < CMAX; ++q)
+    for (int c = t; c < ULD; c += kBigThreads) Us[q][c] = 0.0;
+  if (A.ex_out)
+    for (int i = t; i < O * G * 32; i += kBigThreads) A.ex_out[sl * (long long)O * G * 32 + i] = 0.0;
+  if (A.rec_out)
+    for (int i = t; i < G * 64 * A.max_count; i += kBigThreads) A.rec_out[sl * (long long)G * 64 * A.max_count + i] = -1;
+  __syncthreads();
+  int pc[CMAX], pcl[CMAX];
+  double ps[CMAX], pmn[CMAX], pmx[CMAX];
+#pragma unroll
+  for (int q = 0; q < CMAX; ++q) {
+    pc[q] = pcl[q] = 0;
+    ps[q] = 0.0;
+    pmn[q] = INFINITY;
+    pmx[q] = -INFINITY;
+  }
+  int nrec = 0, nhit = 0, guard = 0, untrained = 0;
+  const int rl = lane >> 2, kl = lane & 3;
+  double (*ex)[CMAX + 1] = exs[warp];
+  for (int g = warp; g < G; g += kBigThreads / 32) {
+    uint64_t tr, te;
+    member_words(A, split, g, tr, te);
+    if (te == 0ull) continue;
+    const int p = g / A.IR;
+    // ---- EX tile: (64 versions) x (C counters) times (C) x (CMAX weights) ----
+    double acc[8][NT][2];
+#pragma unroll
+    for (int rb = 0; rb < 8; ++rb)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[rb][nt][0] = acc[rb][nt][1] = 0.0;
+    const double* xg = A.x + (long long)g * 64 * C;
+    for (int k0 = 0; k0 < C; k0 += 4) {
+      const int kk = k0 + kl;
+      double b[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) b[nt] = Us[nt * 8 + rl][kk];
+#pragma unroll
+      for (int rb = 0; rb < 8; ++rb) {
+        const int v = rb * 8 + rl;
+        const double a = (((te >> v) & 1ull) && kk < C) ? xg[v * C + kk] : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[rb][nt][0], acc[rb][nt][1], a, b[nt]);
+      }
+    }
+#pragma unroll
+    for (int rb = 0; rb < 8; ++rb)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        ex[rb * 8 + rl][nt * 8 + 2 * kl] = acc[rb][nt][0];
+        ex[rb * 8 + rl][nt * 8 + 2 * kl + 1] = acc[rb][nt][1];
+      }
+    __syncwarp();
+    // ---- per version: clamp, score, rank (lane owns versions lane, lane+32) ----
+    for (int h = 0; h < 2; ++h) {
+      const int v = h * 32 + lane;
+      if (!((te >> v) & 1ull)) continue;
+      double ce[CMAX];
+      bool cv[CMAX], cc[CMAX];
+      int ck[CMAX];
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) {
+        cv[q] = false;
+        cc[q] = false;
+        ck[q] = 0;
+        ce[q] = 0.0;
+        if (q < n_os) {
+          const int o = ols[q];
+          const int b = A.opt_bit[p * O + o];
+          if (b >= 0 && !((v >> b) & 1)) {
+            if (trained_s[q] != 1) {
+              if (trained_s[q] == 0) ++untrained;
+              if (trained_s[q] == 2) guard += 1000000;
+              continue;
+            }
+            const int k = rmv(v, b);
+            double e = c0s[q] + ex[v][q];
+            if (near_tol(e, 0.0, A.guard_tol) || near_tol(e, 1.0, A.guard_tol)) ++guard;
+            bool cl = false;
+            if (e <= 0.0) {
+              e = A.clamp_floor;
+              cl = true;
+            }
+            const double ac = A.ylab[(g * O + o) * 32 + k];
+            cv[q] = true;
+            cc[q] = cl;
+            ck[q] = k;
+            ce[q] = e;
+            const double ratio = ac / e;
+            pc[q] += ((e > 1.0 && ac > 1.0) || (e <= 1.0 && ac <= 1.0)) ? 1 : 0;
+            pcl[q] += cl ? 1 : 0;
+            ps[q] += ratio;
+            pmn[q] = fmin(pmn[q], ratio);
+            pmx[q] = fmax(pmx[q], ratio);
+            if (A.ex_out) A.ex_out[(sl * O + o) * (long long)G * 32 + g * 32 + k] = e;
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) {
+        if (!cv[q]) continue;
+        if (near_tol(ce[q], A.threshold, A.guard_tol)) ++guard;
+#pragma unroll
+        for (int r = q + 1; r < CMAX; ++r)
+          if (cv[r] && !(cc[q] && cc[r]) && near_tol(ce[q], ce[r], A.guard_tol)) ++guard;
+      }
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) {
+        if (!cv[q] || !(ce[q] >= A.threshold)) continue;
+        int rk = 0;
+#pragma unroll
+        for (int r = 0; r < CMAX; ++r)
+          if (r != q && cv[r] && ce[r] >= A.threshold && (ce[r] > ce[q] || (ce[r] == ce[q] && r < q))) ++rk;
+        if (rk < A.max_count) {
+          ++nrec;
+          const int o = ols[q];
+          if (A.ylab[(g * O + o) * 32 + ck[q]] > 1.0) ++nhit;
+          if (A.rec_out) A.rec_out[(sl * G * 64 + g * 64 + v) * A.max_count + rk] = (int8_t)o;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // ---- deterministic reduction: lanes (butterfly), then warps in order ----
+#pragma unroll
+  for (int q = 0; q < CMAX; ++q) {
+    const int a = warp_isum(pc[q]), b = warp_isum(pcl[q]);
+    const double sm = warp_sum(ps[q]), mn = warp_min(pmn[q]), mx = warp_max(pmx[q]);
+    if (lane == 0) {
+      redi[warp][q][0] = a;
+      redi[warp][q][1] = b;
+      redd[warp][q][0] = sm;
+      redd[warp][q][1] = mn;
+      redd[warp][q][2] = mx;
+    }
+  }
+  {
+    const int a = warp_isum(nrec), b = warp_isum(nhit), c = warp_isum(untrained), d = warp_isum(guard);
+    if (lane == 0) {
+      reds[warp][0] = a;
+      reds[warp][1] = b;
+      reds[warp][2] = c;
+      reds[warp][3] = d;
+    }
+  }
+  __syncthreads();
+  if (t < n_os) {
+    const int q = t, o = ols[q];
+    OptScore row = A.opt_out[sl * O + o];
+    int nc = 0, ncl = 0;
+    double sm = 0.0, mn = INFINITY, mx = -INFINITY;
+    for (int w = 0; w < kBigThreads / 32; ++w) {
+      nc += redi[w][q][0];
+      ncl += redi[w][q][1];
+      sm += redd[w][q][0];
+      mn = fmin(mn, redd[w][q][1]);
+      mx = fmax(mx, redd[w][q][2]);
+    }
+    const bool has = row.n_test > 0 && trained_s[q] == 1;
+    row.n_correct = nc;
+    row.n_clamped = ncl;
+    row.sum_ratio = has ? sm : 0.0;
+    row.min_ratio = has ? mn : 0.0;
+    row.max_ratio = has ? mx : 0.0;
+    A.opt_out[sl * O + o] = row;
+    if (A.totals && has) {
+      atomicAdd(&A.totals[0], (unsigned long long)nc);
+      atomicAdd(&A.totals[1], (unsigned long long)row.n_test);
+    }
+  }
+  if (t == 0) {
+    ScnScore sr{0, 0, 0, 0};
+    for (int w = 0; w < kBigThreads / 32; ++w) {
+      sr.n_rec += reds[w][0];
+      sr.n_rec_hit += reds[w][1];
+      sr.n_untrained += reds[w][2];
+      sr.n_guard += reds[w][3];
+    }
+    A.scn_out[sl] = sr;
+    if (A.totals) {
+      atomicAdd(&A.totals[2], (unsigned long long)sr.n_rec);
+      atomicAdd(&A.totals[3], (unsigned long long)sr.n_rec_hit);
+    }
+  }
+}
+
+}  // namespace speedrec

@@ -23,10 +23,11 @@ namespace speedrec {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kMaxOpt = 16;
-constexpr int kMaxGroups = 64;
+constexpr int kMaxGroups = 64;       // warp-per-scenario path
+constexpr int kMaxGroupsBig = 4096;  // CTA-per-fit path (config C4)
 constexpr int kMaxCounters = 128;
 constexpr int kMaxRec = 8;
-constexpr int kMaxWarpsPerBlock = 12;  // 384 threads -> up to 170 registers per thread
+constexpr int kMaxWarpsPerBlock = 16;  // default warps/CTA of k_fit_warp (tools/tune_launch.sh)
 
 struct OptScore {
   int32_t n_train, n_test, n_correct, n_clamped;
@@ -40,77 +41,85 @@ struct MaskScore {
   int32_t n_correct, n_test, n_rec, n_rec_hit;
 };
 
-// Per-warp shared-memory layout (byte offsets inside the warp's slab).
-struct WarpLayout {
-  int bytes;            // slab size (multiple of 16)
-  int off_trw, off_tew; // uint64 [G]
-  int off_gidx;         // int16 [G]   group -> index among test groups (-1)
-  int off_F;            // int16 [dmax] feature columns of the scenario
-  int off_ex;           // double [ex_cap]  EX per (o_idx, test group, k)
-  int off_excl;         // uint8 [ex_cap]   clamped flag
-  int ex_cap;
-  int off_trs;          // int32 [np_tr]  training before-slots
-  int off_try;          // double [np_tr] training labels
-  int off_tes;          // int32 [np_te]  test before-slots
-  int off_tek;          // int32 [np_te]  g*32+k of the test case
-  int off_tey;          // double [np_te] AC of the test case
-  int np_tr, np_te;
-  int off_col;          // int16 [dmax] active feature columns
-  int off_xb;           // double [dmax]
-  int off_s;            // double [dmax]
-  int off_w;            // double [dmax]  weights on scaled features
-  int off_u;            // double [dmax]  weights on raw centred features
-  int off_v1, off_v2, off_v3;  // double [vmax] solve vectors
-  int off_invd;         // double [vmax]
-  int vmax;
-  int off_M;            // double [mcap(mcap+1)/2] packed Cholesky factor
-  int mcap;
-  int off_colbuf;       // double [32] column broadcast of the register Cholesky
-  int off_ufull;        // double [C] weights on raw counters
-};
-
-struct EvalArgs {
-  // dataset (device)
-  const double* x;       // rates [N][C]
-  const double* ylab;    // labels [G][O][32]
-  const int8_t* opt_bit; // [P][O]
-  int P, IR, C, O, G;
-  // scenario batch (device)
+// Scenario batch as the kernels see it (sr_scenarios after validation).
+struct ScenDesc {
   int kind;              // 0 groups, 1 loo, 2 random
   int gw;                // group words
   long long n_splits;
   const uint64_t* train_g;
   const uint64_t* test_g;
   const uint32_t* split_om;
-  const int32_t* pool_list;   // pool groups ascending
+  const int32_t* pool_list;  // pool groups ascending
   int n_pool;
   unsigned long long seed;
   uint32_t opt_mask;
   int subsets_k;
   long long n_masks;
-  const uint64_t* fmasks;     // [n_masks][2] or null
+  const uint64_t* fmasks;    // [n_masks][2] or null
+};
+
+// Per-warp shared-memory layout of k_fit_warp (byte offsets inside the slab).
+struct WarpLayout {
+  int bytes;            // slab size (multiple of 16)
+  int off_trw, off_tew; // uint64 [G] split words of the fit's scenario
+  int off_F;            // int16 [dmax] feature columns of the scenario
+  int off_trs;          // int32 [np_tr]  training before-slots
+  int off_yc;           // double [np_tr] training labels, centred in place
+  int off_tes;          // int32 [np_te]  test before-slots
+  int off_tek;          // int32 [np_te]  g*32+k of the test case
+  int np_tr, np_te;
+  int off_col;          // int16 [dpad] active feature columns (zero padded)
+  int off_xb;           // double [dpad]
+  int off_s;            // double [dpad]
+  int off_w;            // double [dmax]  weights on scaled features
+  int off_u;            // double [dmax]  work vector
+  int off_v2;           // double [vmax] residual / work vector
+  int off_M;            // double [mcap(mcap+1)/2] packed factor
+  int mcap;
+  int vmax;
+  int off_ufull;        // double [C] weights on raw counters
+};
+
+// Arguments of the warp-per-fit path (k_fit_warp, k_rank_warp, k_mask_final).
+struct EvalArgs {
+  // dataset (device)
+  const double* x;       // rates [N][C]
+  const double* ylab;    // labels [G][O][32]
+  const int8_t* opt_bit; // [P][O]
+  int P, IR, C, O, G;
+  ScenDesc sd;
   // params
   double lambda, threshold, clamp_floor, guard_tol;
   int max_count, refine;
-  // range
+  // scenario range of this launch (a chunk of the sr_evaluate range)
   long long first, count;
-  // outputs (device)
-  OptScore* opt_out;
-  ScnScore* scn_out;
-  double* ex_out;
-  int8_t* rec_out;
+  long long out0;        // index of `first` inside the caller's output arrays
+  // per-chunk exchange between the fit and rank kernels
+  double* extab;         // [count][ex_stride]: EX per (scored-opt slot q, test group, k); clamped -> -EX
+  int ex_stride, tg_stride;  // tg_stride = 32 * max test groups; ex_stride = n_os_max * tg_stride
+  uint32_t* trained;     // [count] bit o set iff optimization o has >= 1 training pair
+  int* guard_acc;        // [count] guard cases counted by the fit kernel
+  // outputs (device, indexed by out0 + local scenario)
+  OptScore* opt_out;     // [.][O] or null
+  ScnScore* scn_out;     // or null
+  double* ex_out;        // [.][O][G*32] or null (pre-zeroed)
+  int8_t* rec_out;       // [.][N][max_count] or null (pre-filled with -1)
   unsigned long long* totals;  // [4] or null
-  int agg;                     // 1: work item = mask (all folds), C5 aggregation
-  MaskScore* mask_out;         // [count / n_splits] or null
-  unsigned long long* keys_out;  // [count / n_splits] top-K keys (agg only)
-  // workspace
+  // mask aggregation (C5)
+  int agg;
+  int* mask_acc;         // [masks of the evaluate range][4], atomically accumulated
+  long long mask0;       // first mask id of the evaluate range
+  MaskScore* mask_out;
+  unsigned long long* keys_out;
+  long long n_mask_range;
+  // workspace of k_fit_warp
   WarpLayout L;
   int warps_per_block;
   int stage_x;           // 1: stage x [N][C] in smem with ld = ldxs
   int ldxs;
-  int off_stage;         // byte offset of the staged x (after opt_bit table)
+  int off_stage;         // byte offset of the staged x (after the opt_bit table)
   int off_warps;         // byte offset of the first warp slab
-  double* gscratch;      // per global warp: mscratch doubles for M overflow
+  double* gscratch;      // per global warp: mscratch doubles (large systems: factor + 2 vectors)
   long long mscratch;
 };
 
@@ -120,6 +129,46 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
   x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
   return x ^ (x >> 31);
+}
+
+// Train/test words of group g under split k (reading R17).
+__device__ __forceinline__ void member_words(const ScenDesc& D, long long split, int g, uint64_t& tr,
+                                             uint64_t& te) {
+  if (D.kind == 0) {
+    tr = ((D.train_g[split * D.gw + (g >> 6)] >> (g & 63)) & 1ull) ? ~0ull : 0ull;
+    te = ((D.test_g[split * D.gw + (g >> 6)] >> (g & 63)) & 1ull) ? ~0ull : 0ull;
+  } else if (D.kind == 1) {
+    bool inpool = false;
+    for (int q = 0; q < D.n_pool; ++q) inpool |= (D.pool_list[q] == g);
+    tr = inpool ? ~0ull : 0ull;
+    te = 0ull;
+    if (g == D.pool_list[split >> 6]) {
+      tr &= ~(1ull << (split & 63));
+      te = 1ull << (split & 63);
+    }
+  } else {
+    tr = mix64(mix64(D.seed ^ mix64((uint64_t)split)) + (uint64_t)g);
+    te = ~tr;
+  }
+}
+
+// Index of group g among the split's test groups (EX-table row).
+__device__ __forceinline__ int test_group_index(const ScenDesc& D, long long split, int g) {
+  if (D.kind == 2) return g;
+  if (D.kind == 1) return 0;
+  int gi = 0;
+  for (int w = 0; w < (g >> 6); ++w) gi += __popcll(D.test_g[split * D.gw + w]);
+  return gi + __popcll(D.test_g[split * D.gw + (g >> 6)] & ((1ull << (g & 63)) - 1ull));
+}
+
+__device__ __forceinline__ uint32_t scored_mask(const ScenDesc& D, long long split, int O) {
+  return (D.split_om ? D.split_om[split] : D.opt_mask) & ((1u << O) - 1u);
+}
+
+__device__ __forceinline__ bool feature_in(const ScenDesc& D, long long fidx, int c) {
+  if (D.subsets_k > 0) return c < D.subsets_k && ((fidx >> c) & 1);
+  if (D.fmasks) return (D.fmasks[fidx * 2 + (c >> 6)] >> (c & 63)) & 1ull;
+  return true;
 }
 __device__ __forceinline__ int ins0(int k, int b) { return ((k >> b) << (b + 1)) | (k & ((1 << b) - 1)); }
 __device__ __forceinline__ int rmv(int v, int b) { return (v & ((1 << b) - 1)) | ((v >> (b + 1)) << b); }

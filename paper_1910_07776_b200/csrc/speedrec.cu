@@ -12,9 +12,11 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <cstdlib>
 
 #include "../../include/speedrec.h"
 #include "eval_warp.cuh"
+#include "fit_big.cuh"
 #include "kernels.cuh"
 
 using namespace speedrec;
@@ -62,6 +64,8 @@ struct sr_ctx {
   int dmax = 0, np_tr = 0, np_te = 0, n_tg = 0, n_os = 0;
   // scratch + outputs
   DevBuf gscratch, out_opt, out_scn, out_ex, out_rec, out_tot, out_mask, out_top, keys_a, keys_b;
+  DevBuf big_lists, big_y, big_U, big_c0, big_flag;  // large-batch path (> 64 groups)
+  DevBuf extab, trained, guard_acc, mask_acc;         // fit -> rank exchange (warp path)
   // accounting
   bool timing = false;
   std::vector<KStat> kstats;
@@ -171,6 +175,24 @@ int grid_for(const sr_ctx* c, long long work, int block) {
 
 int align16(int x) { return (x + 15) & ~15; }
 
+ScenDesc scen_desc(const sr_ctx* c) {
+  ScenDesc D{};
+  D.kind = c->sc.kind;
+  D.gw = (c->G + 63) / 64;
+  D.n_splits = c->sc.n_splits;
+  D.train_g = (const uint64_t*)c->train_g.p;
+  D.test_g = (const uint64_t*)c->test_g.p;
+  D.split_om = c->sc.split_opt_masks ? (const uint32_t*)c->split_om.p : nullptr;
+  D.pool_list = (const int32_t*)c->pool_list.p;
+  D.n_pool = (int)c->h_pool.size();
+  D.seed = c->sc.seed;
+  D.opt_mask = c->sc.opt_mask;
+  D.subsets_k = c->sc.all_subsets_k;
+  D.n_masks = c->sc.n_masks;
+  D.fmasks = (c->sc.feature_masks && c->sc.all_subsets_k == 0) ? (const uint64_t*)c->fmasks.p : nullptr;
+  return D;
+}
+
 }  // namespace
 
 extern "C" {
@@ -218,7 +240,8 @@ void sr_destroy(sr_ctx* c) {
   for (DevBuf* b : {&c->counters, &c->cycles, &c->runtime, &c->opt_bit, &c->x, &c->ylab, &c->bad,
                     &c->train_g, &c->test_g, &c->split_om, &c->pool_list, &c->fmasks, &c->gscratch,
                     &c->out_opt, &c->out_scn, &c->out_ex, &c->out_rec, &c->out_tot, &c->out_mask,
-                    &c->out_top, &c->keys_a, &c->keys_b})
+                    &c->out_top, &c->keys_a, &c->keys_b, &c->big_lists, &c->big_y, &c->big_U, &c->big_c0,
+                    &c->big_flag, &c->extab, &c->trained, &c->guard_acc, &c->mask_acc})
     release(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -323,7 +346,7 @@ sr_status sr_define_scenarios(sr_ctx* c, const sr_scenarios* s, int64_t* n_scena
   if (s->kind < 0 || s->kind > 2) return fail(c, SR_E_ARG, "scenarios: kind %d", s->kind);
   if (s->n_splits <= 0 || s->n_masks <= 0) return fail(c, SR_E_ARG, "scenarios: n_splits/n_masks must be > 0");
   if (s->group_words != gw) return fail(c, SR_E_ARG, "scenarios: group_words=%d, expected %d", s->group_words, gw);
-  if (G > kMaxGroups) return fail(c, SR_E_UNSUPPORTED, "scenarios: %d groups > %d", G, kMaxGroups);
+  if (G > kMaxGroupsBig) return fail(c, SR_E_UNSUPPORTED, "scenarios: %d groups > %d", G, kMaxGroupsBig);
   if (s->all_subsets_k < 0 || s->all_subsets_k > 20 || s->all_subsets_k > c->C)
     return fail(c, SR_E_ARG, "scenarios: all_subsets_k=%d", s->all_subsets_k);
   if (s->all_subsets_k > 0 && s->n_masks != (1LL << s->all_subsets_k))
@@ -423,37 +446,131 @@ WarpLayout plan_layout(const sr_ctx* c, int mcap) {
     return o;
   };
   const int G = c->G, d = c->dmax, vmax = std::max(c->np_tr, d);
+  const int dpad = std::max(d, 32) + 4;  // zero-padded for the fast-path fragment loads
   L.off_trw = take(8 * G);
   L.off_tew = take(8 * G);
-  L.off_gidx = take(2 * G);
   L.off_F = take(2 * d);
-  L.ex_cap = c->n_os * c->n_tg * 32;
-  L.off_ex = take(8 * L.ex_cap);
-  L.off_excl = take(L.ex_cap);
   L.np_tr = c->np_tr;
   L.np_te = c->np_te;
   L.off_trs = take(4 * c->np_tr);
-  L.off_try = take(8 * c->np_tr);
+  L.off_yc = take(8 * c->np_tr);
   L.off_tes = take(4 * c->np_te);
   L.off_tek = take(4 * c->np_te);
-  L.off_tey = take(8 * c->np_te);
-  const int dpad = std::max(d, 32) + 4;  // zero-padded for the fast-path fragment loads
   L.off_col = take(2 * dpad);
   L.off_xb = take(8 * dpad);
   L.off_s = take(8 * dpad);
   L.off_w = take(8 * d);
   L.off_u = take(8 * d);
   L.vmax = vmax;
-  L.off_v1 = take(8 * vmax);
   L.off_v2 = take(8 * vmax);
-  L.off_v3 = take(8 * vmax);
-  L.off_invd = take(8 * vmax);
   L.mcap = mcap;
   L.off_M = take(8 * (mcap * (mcap + 1) / 2));
-  L.off_colbuf = take(8 * 32);
   L.off_ufull = take(8 * c->C);
   L.bytes = align16(off);
   return L;
+}
+
+// Large-batch path (> 64 groups, config C4): k_fit_big per (scenario, opt)
+// fit + k_rank_big per scenario, over scenario batches that bound the
+// per-batch weight table.
+sr_status evaluate_big(sr_ctx* c, const sr_params* prm, long long first, long long count, sr_outputs* out) {
+  const int G = c->G, O = c->O, C = c->C;
+  const long long N = c->N;
+  sr_status st;
+  const long long batch = std::min<long long>(count, 4096);
+  const long long np = 32LL * G;
+  const int fit_grid = (int)std::min<long long>(c->sm_count, batch * O);
+  if ((st = ensure(c, c->big_lists, (size_t)fit_grid * np * 4)) ||
+      (st = ensure(c, c->big_y, (size_t)fit_grid * np * 8)) ||
+      (st = ensure(c, c->big_U, (size_t)batch * O * C * 8)) || (st = ensure(c, c->big_c0, (size_t)batch * O * 8)) ||
+      (st = ensure(c, c->big_flag, (size_t)batch * O * 4)))
+    return st;
+  const size_t b_opt = (size_t)count * O * sizeof(sr_opt_score), b_scn = (size_t)count * sizeof(sr_scn_score);
+  const size_t b_ex = (size_t)count * O * G * 32 * 8, b_rec = (size_t)count * N * prm->max_count;
+  OptScore* opt = (OptScore*)out->opt_scores;
+  ScnScore* scn = (ScnScore*)out->scn_scores;
+  double* ex = out->ex;
+  int8_t* rec = out->recs;
+  unsigned long long* tot = (unsigned long long*)out->totals;
+  if (!out->on_device) {
+    if ((st = ensure(c, c->out_opt, b_opt)) || (st = ensure(c, c->out_scn, b_scn))) return st;
+    opt = (OptScore*)c->out_opt.p;
+    scn = (ScnScore*)c->out_scn.p;
+    if (ex) {
+      if ((st = ensure(c, c->out_ex, b_ex))) return st;
+      ex = (double*)c->out_ex.p;
+    }
+    if (rec) {
+      if ((st = ensure(c, c->out_rec, b_rec))) return st;
+      rec = (int8_t*)c->out_rec.p;
+    }
+    if (tot) {
+      if ((st = ensure(c, c->out_tot, 32))) return st;
+      tot = (unsigned long long*)c->out_tot.p;
+    }
+  }
+  if (tot) CU(cudaMemsetAsync(tot, 0, 32, c->stream));
+  BigArgs B{};
+  B.x = (const double*)c->x.p;
+  B.ylab = (const double*)c->ylab.p;
+  B.opt_bit = (const int8_t*)c->opt_bit.p;
+  B.P = c->P;
+  B.IR = c->I * c->R;
+  B.C = C;
+  B.O = O;
+  B.G = G;
+  B.kind = c->sc.kind;
+  B.gw = (G + 63) / 64;
+  B.n_splits = c->sc.n_splits;
+  B.train_g = (const uint64_t*)c->train_g.p;
+  B.test_g = (const uint64_t*)c->test_g.p;
+  B.split_om = c->sc.split_opt_masks ? (const uint32_t*)c->split_om.p : nullptr;
+  B.pool_list = (const int32_t*)c->pool_list.p;
+  B.n_pool = (int)c->h_pool.size();
+  B.seed = c->sc.seed;
+  B.opt_mask = c->sc.opt_mask;
+  B.subsets_k = c->sc.all_subsets_k;
+  B.n_masks = c->sc.n_masks;
+  B.fmasks = (c->sc.feature_masks && c->sc.all_subsets_k == 0) ? (const uint64_t*)c->fmasks.p : nullptr;
+  B.lambda = prm->ridge;
+  B.threshold = prm->threshold;
+  B.clamp_floor = prm->clamp_floor;
+  B.guard_tol = prm->guard_tol;
+  B.refine = prm->refine_steps;
+  B.max_count = prm->max_count;
+  B.lists = (int32_t*)c->big_lists.p;
+  B.ylist = (double*)c->big_y.p;
+  B.np = np;
+  B.U = (double*)c->big_U.p;
+  B.c0 = (double*)c->big_c0.p;
+  B.fitflag = (int32_t*)c->big_flag.p;
+  B.totals = tot;
+  const int smem = (kBigMaxD * kBigGLd + kBigChunk * kBigLd + kBigChunk * kBigMaxD + 6 * kBigMaxD + 2 * kBigChunk +
+                    16 + 8) * 8 + (2 * kBigMaxD + 2 * G + 20) * 4;
+  CU(cudaFuncSetAttribute(k_fit_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (c->n_os > 8) return fail(c, SR_E_UNSUPPORTED, "evaluate: > 64 groups supports <= 8 scored optimizations");
+  for (long long b0 = 0; b0 < count; b0 += batch) {
+    const long long bc = std::min(batch, count - b0);
+    B.first = first + b0;
+    B.count = bc;
+    B.opt_out = opt + b0 * O;
+    B.scn_out = scn + b0;
+    B.ex_out = ex ? ex + b0 * O * G * 32 : nullptr;
+    B.rec_out = rec ? rec + b0 * N * prm->max_count : nullptr;
+    const int grid = (int)std::min<long long>(c->sm_count, bc * O);
+    if ((st = launch(c, "k_fit_big", [&] { k_fit_big<<<grid, kBigThreads, smem, c->stream>>>(B); }))) return st;
+    if ((st = launch(c, "k_rank_big", [&] { k_rank_big<8><<<(unsigned)bc, kBigThreads, 0, c->stream>>>(B); })))
+      return st;
+  }
+  if (!out->on_device) {
+    CU(cudaMemcpyAsync(out->opt_scores, opt, b_opt, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(out->scn_scores, scn, b_scn, cudaMemcpyDeviceToHost, c->stream));
+    if (out->ex) CU(cudaMemcpyAsync(out->ex, ex, b_ex, cudaMemcpyDeviceToHost, c->stream));
+    if (out->recs) CU(cudaMemcpyAsync(out->recs, rec, b_rec, cudaMemcpyDeviceToHost, c->stream));
+    if (out->totals) CU(cudaMemcpyAsync(out->totals, tot, 32, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+  }
+  return SR_OK;
 }
 
 }  // namespace
@@ -498,31 +615,39 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
        })))
     return st;
   if (count == 0) return SR_OK;
+  if (G > kMaxGroups) {
+    if (agg) return fail(c, SR_E_UNSUPPORTED, "evaluate: mask aggregation needs <= %d groups", kMaxGroups);
+    return evaluate_big(c, prm, first, count, out);
+  }
 
-  // ---- plan k_eval_warp ----
+  // ---- plan k_fit_warp ----
+  // Launch-shape knobs (defaults = the tuned configuration): SPEEDREC_STAGE=0/1
+  // forces staging of x in shared memory, SPEEDREC_WMAX in {12,16,24} picks the
+  // warps-per-CTA variant, SPEEDREC_SMEM_KB caps shared memory per CTA.
   const int budget = c->max_smem_optin;                  // 232448 on B200
   const int head = align16(c->P * O);
   const int ldxs = C | 1;
   const long long stage_bytes = N * ldxs * 8;
   const int mmax = std::min(c->np_tr, c->dmax + 1);      // largest system any fit can need
   int stage = stage_bytes <= 96 * 1024 ? 1 : 0;
+  if (const char* e = getenv("SPEEDREC_STAGE")) stage = atoi(e) && stage_bytes <= 96 * 1024;
+  int wmax = kMaxWarpsPerBlock;
+  if (const char* e = getenv("SPEEDREC_WMAX")) wmax = atoi(e) >= 24 ? 24 : atoi(e) >= 16 ? 16 : 12;
+  int budget_cap = budget;
+  if (const char* e = getenv("SPEEDREC_SMEM_KB")) budget_cap = std::min(budget, std::max(16, atoi(e)) * 1024);
   int mcap = std::min(mmax, 32);
   if (prm->debug_mcap > 0) mcap = std::min(mcap, prm->debug_mcap);
   WarpLayout L = plan_layout(c, mcap);
-  int avail = budget - head - (stage ? align16((int)stage_bytes) : 0);
-  int wpb = std::min(kMaxWarpsPerBlock, avail / std::max(L.bytes, 1));
-  while (wpb < 4 && mcap > 8 && prm->debug_mcap == 0) {
-    mcap /= 2;
-    L = plan_layout(c, mcap);
-    wpb = std::min(kMaxWarpsPerBlock, avail / L.bytes);
-  }
+  int avail = budget_cap - head - (stage ? align16((int)stage_bytes) : 0);
+  int wpb = std::min(wmax, avail / std::max(L.bytes, 1));
   if (wpb < 1 && stage) {
     stage = 0;
-    avail = budget - head;
-    wpb = std::min(kMaxWarpsPerBlock, avail / L.bytes);
+    avail = budget_cap - head;
+    wpb = std::min(wmax, avail / L.bytes);
   }
   if (wpb < 1) return fail(c, SR_E_UNSUPPORTED, "evaluate: per-warp workspace %d B exceeds shared memory", L.bytes);
-  const long long mscr = (mmax > mcap) ? (long long)mmax * (mmax + 1) / 2 : 0;
+  // global scratch for systems beyond the shared-memory factor: packed factor + 2 vectors
+  const long long mscr = (mmax > std::min(mcap, 32)) ? (long long)mmax * (mmax + 1) / 2 + 2LL * L.vmax : 0;
 
   EvalArgs A{};
   A.x = (const double*)c->x.p;
@@ -533,27 +658,13 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.C = C;
   A.O = O;
   A.G = G;
-  A.kind = c->sc.kind;
-  A.gw = (G + 63) / 64;
-  A.n_splits = c->sc.n_splits;
-  A.train_g = (const uint64_t*)c->train_g.p;
-  A.test_g = (const uint64_t*)c->test_g.p;
-  A.split_om = c->sc.split_opt_masks ? (const uint32_t*)c->split_om.p : nullptr;
-  A.pool_list = (const int32_t*)c->pool_list.p;
-  A.n_pool = (int)c->h_pool.size();
-  A.seed = c->sc.seed;
-  A.opt_mask = c->sc.opt_mask;
-  A.subsets_k = c->sc.all_subsets_k;
-  A.n_masks = c->sc.n_masks;
-  A.fmasks = (c->sc.feature_masks && c->sc.all_subsets_k == 0) ? (const uint64_t*)c->fmasks.p : nullptr;
+  A.sd = scen_desc(c);
   A.lambda = prm->ridge;
   A.threshold = prm->threshold;
   A.clamp_floor = prm->clamp_floor;
   A.guard_tol = prm->guard_tol;
   A.max_count = prm->max_count;
   A.refine = prm->refine_steps;
-  A.first = first;
-  A.count = count;
   A.L = L;
   A.warps_per_block = wpb;
   A.stage_x = stage;
@@ -561,18 +672,27 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.off_stage = head;
   A.off_warps = head + (stage ? align16((int)stage_bytes) : 0);
   const int smem = A.off_warps + wpb * L.bytes;
-  const int cmax = c->n_os <= 8 ? 8 : 16;
-  auto kern = cmax == 8 ? k_eval_warp<8> : k_eval_warp<16>;
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  auto kfit = wmax == 24 ? k_fit_warp<24> : wmax == 16 ? k_fit_warp<16> : k_fit_warp<12>;
+  CU(cudaFuncSetAttribute(kfit, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfit, wpb * 32, smem));
   per_sm = std::max(per_sm, 1);
-  const long long items = agg ? count / c->sc.n_splits : count;
-  long long blocks = std::min<long long>((long long)c->sm_count * per_sm, (items + wpb - 1) / wpb);
-  blocks = std::max(1LL, blocks);
-  const long long nwarps = blocks * wpb;
+
+  // ---- per-chunk exchange buffers (EX table, trained masks, guard counts) ----
+  const int tg_stride = 32 * c->n_tg;
+  const int ex_stride = c->n_os * tg_stride;
+  const long long chunk = std::max(1LL, std::min<long long>(count, (256LL << 20) / (8LL * ex_stride)));
+  if ((st = ensure(c, c->extab, (size_t)chunk * ex_stride * 8)) || (st = ensure(c, c->trained, (size_t)chunk * 4)) ||
+      (st = ensure(c, c->guard_acc, (size_t)chunk * 4)))
+    return st;
+  A.extab = (double*)c->extab.p;
+  A.ex_stride = ex_stride;
+  A.tg_stride = tg_stride;
+  A.trained = (uint32_t*)c->trained.p;
+  A.guard_acc = (int*)c->guard_acc.p;
+  const long long max_fit_blocks = (long long)c->sm_count * per_sm;
   if (mscr > 0) {
-    if ((st = ensure(c, c->gscratch, (size_t)(nwarps * mscr * 8)))) return st;
+    if ((st = ensure(c, c->gscratch, (size_t)(max_fit_blocks * wpb * mscr * 8)))) return st;
     A.gscratch = (double*)c->gscratch.p;
     A.mscratch = mscr;
   }
@@ -584,11 +704,16 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   const int K = prm->top_k;
   if (agg) {
     A.agg = 1;
+    A.mask0 = first / c->sc.n_splits;
+    A.n_mask_range = nm;
     const long long nk2 = (nm + 1023) / 1024 * K;
     if ((st = ensure(c, c->keys_a, (size_t)std::max(nm, 1LL) * 8)) ||
-        (st = ensure(c, c->keys_b, (size_t)std::max(nk2, (long long)K) * 8)))
+        (st = ensure(c, c->keys_b, (size_t)std::max(nk2, (long long)K) * 8)) ||
+        (st = ensure(c, c->mask_acc, (size_t)std::max(nm, 1LL) * 16)))
       return st;
     A.keys_out = (unsigned long long*)c->keys_a.p;
+    A.mask_acc = (int*)c->mask_acc.p;
+    CU(cudaMemsetAsync(A.mask_acc, 0, (size_t)nm * 16, c->stream));
   }
   if (out->on_device) {
     A.opt_out = (OptScore*)out->opt_scores;
@@ -624,10 +749,32 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     }
   }
   if (A.totals) CU(cudaMemsetAsync(A.totals, 0, 32, c->stream));
-  if ((st = launch(c, "k_eval_warp", [&] {
-         kern<<<(unsigned)blocks, wpb * 32, smem, c->stream>>>(A);
-       })))
-    return st;
+  if (A.ex_out) CU(cudaMemsetAsync(A.ex_out, 0, b_ex, c->stream));
+  if (A.rec_out) CU(cudaMemsetAsync(A.rec_out, 0xFF, b_rec, c->stream));
+  const int cmax = c->n_os <= 8 ? 8 : 16;
+  for (long long c0 = 0; c0 < count; c0 += chunk) {
+    const long long cc = std::min(chunk, count - c0);
+    A.first = first + c0;
+    A.count = cc;
+    A.out0 = c0;
+    CU(cudaMemsetAsync(A.trained, 0, (size_t)cc * 4, c->stream));
+    CU(cudaMemsetAsync(A.guard_acc, 0, (size_t)cc * 4, c->stream));
+    const long long fblocks = std::max(1LL, std::min(max_fit_blocks, (cc * O + wpb - 1) / wpb));
+    if ((st = launch(c, "k_fit_warp", [&] { kfit<<<(unsigned)fblocks, wpb * 32, smem, c->stream>>>(A); }))) return st;
+    const long long rblocks = std::max(1LL, std::min<long long>((long long)c->sm_count * 8, (cc + 7) / 8));
+    if (cmax == 8) {
+      if ((st = launch(c, "k_rank_warp", [&] { k_rank_warp<8><<<(unsigned)rblocks, 256, 0, c->stream>>>(A); })))
+        return st;
+    } else {
+      if ((st = launch(c, "k_rank_warp", [&] { k_rank_warp<16><<<(unsigned)rblocks, 256, 0, c->stream>>>(A); })))
+        return st;
+    }
+  }
+  if (agg) {
+    if ((st = launch(c, "k_mask_final",
+                     [&] { k_mask_final<<<grid_for(c, nm, 256), 256, 0, c->stream>>>(A); })))
+      return st;
+  }
   if (agg && out->top_masks) {
     // iterated block top-K over the mask keys (O8)
     unsigned long long* src = (unsigned long long*)c->keys_a.p;

@@ -107,6 +107,35 @@ def test_c5_mask_aggregation_and_top_k(Context):
     ctx.close()
 
 
+def test_c4_large_batch_path_small(Context):
+    """> 64 groups -> the CTA-per-fit DMMA path (k_fit_big + k_rank_big):
+    96 programs x 64 variants x 128 counters (n ~ 770 training pairs, d = 128)."""
+    cfg = gen.make_config("C4", n_splits=24, n_programs=96)
+    got, ref = _run(Context, cfg, 0, 24)
+    print("C4 P=96", compare(got, ref))
+    got, ref = _run(Context, cfg, 5, 7)             # ragged sub-range
+    compare(got, ref)
+
+
+def test_c4_full_size_sampled(Context):
+    """Full C4 lattice (1024 programs, 65,536 slots, n ~ 8,192 pairs per fit,
+    p = 129) in the bench launch; sampled scenarios vs the oracle."""
+    cfg = gen.make_config("C4", n_splits=10_000_000)
+    S = 148
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    got = ctx.evaluate(0, S)
+    ctx.close()
+    idx = [0, 77, 147]
+    from concurrent.futures import ThreadPoolExecutor   # ctypes releases the GIL
+    with ThreadPoolExecutor(len(idx)) as pool:
+        refs = list(pool.map(lambda s: oracle.evaluate(cfg.dataset, cfg.scenarios, s, 1, n_threads=1), idx))
+    st = compare(dict(opt=got["opt"][idx], scn=got["scn"][idx]),
+                 dict(opt=np.concatenate([r["opt"] for r in refs]), scn=np.concatenate([r["scn"] for r in refs])))
+    print("C4 full sampled", st, "n_train", got["opt"]["n_train"][idx].tolist())
+
+
 def test_global_scratch_path(Context):
     # Force the Cholesky factor out of shared memory (debug_mcap=8): same results.
     for name, n in (("C3", 500), ("C2", 240), ("C1", 64)):
