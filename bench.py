@@ -174,11 +174,18 @@ def main():
         return run_reference(args, cfg, rank, world)
 
     import torch
+    from paper_1910_07776_b200 import dist as D
+    local = local % max(torch.cuda.device_count(), 1)   # (ranks > GPUs only for gloo smoke runs)
     torch.cuda.set_device(local)
     dist = None
+    backend = os.environ.get("SPEEDREC_DIST_BACKEND", "nccl")
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    xdev = "cpu" if backend != "nccl" else torch.device("cuda", local)   # device of exchanged tensors
     from paper_1910_07776_b200 import Context
     from paper_1910_07776_b200.speedrec import OPT_SCORE_DTYPE, SCN_SCORE_DTYPE
     stream = torch.cuda.Stream(device=local)      # one explicit stream for the library and the events
@@ -187,7 +194,7 @@ def main():
     ds = cfg.dataset
     ctx.load(ds)
     ctx.define_scenarios(cfg.scenarios)
-    first, count = rank * per_gpu, per_gpu
+    first, count = D.weak_range(per_gpu, rank)               # scenario shard of this rank
     O = ds.n_opt_ids
     dev = torch.device("cuda", local)
     out = dict(opt=torch.empty(count * O * OPT_SCORE_DTYPE.itemsize, dtype=torch.uint8, device=dev),
@@ -220,12 +227,8 @@ def main():
     ctx.set_timing(False)
     launches = sum(v[0] for v in stats.values())
     my_ms = float(np.mean(step_ms))
-    t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
-    tot = out["totals"].clone()
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-    ms = float(t.item())
+    ms = D.max_over_ranks(my_ms, dist, device=xdev)           # max over ranks (device-timed)
+    tot = D.reduce_totals(out["totals"].to(xdev), dist)       # pooled A7 totals (exact)
     value = world * count / (ms / 1e3)
 
     # ---------------- roofline of the dominant kernel (FP64 ALU/DMMA bound)
@@ -275,10 +278,8 @@ def main():
             torch.cuda.synchronize()
             if k > 0:
                 e2e_ms.append(a.elapsed_time(b))
-        te = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
-        if dist:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * count / (te.item() / 1e3), "unit": "scenario_evals/s",
+        te = D.max_over_ranks(float(np.mean(e2e_ms)), dist, device=xdev)
+        e2e = {"value": world * count / (te / 1e3), "unit": "scenario_evals/s",
                "h2d_bytes_per_step": int(hc.numel() * 8 + hy.numel() * 8 + hr.numel() * 8 + hb.numel()),
                "d2h_bytes_per_step": int(hopt.numel() + hscn.numel() + 32)}
 

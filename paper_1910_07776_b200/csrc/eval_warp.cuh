@@ -299,30 +299,35 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
 
     // ---- A2: per-fit min-max statistics over the training befores (D3) ----
     int deff = 0;
-    for (int a0 = 0; a0 < d; a0 += 32) {
-      const int a = a0 + lane;
-      double mn = 0.0, mx = 0.0, sm = 0.0;
-      int c = 0;
-      if (a < d) {
-        c = F[a];
-        mn = mx = X[(long long)trs[0] * ldx + c];
-        sm = mn;
-        for (int i = 1; i < n; ++i) {
-          const double vv = X[(long long)trs[i] * ldx + c];
-          mn = fmin(mn, vv);
-          mx = fmax(mx, vv);
-          sm += vv;
+    for (int a0 = 0; a0 < d; a0 += 64) {       // two features per lane per row pass
+      const int a1 = a0 + lane, a2 = a0 + 32 + lane;
+      const int c1 = a1 < d ? F[a1] : 0, c2 = a2 < d ? F[a2] : 0;
+      const double* x0 = X + (long long)trs[0] * ldx;
+      double mn1 = x0[c1], mx1 = mn1, sm1 = mn1, mn2 = x0[c2], mx2 = mn2, sm2 = mn2;
+      for (int i = 1; i < n; ++i) {
+        const double* xr = X + (long long)trs[i] * ldx;
+        const double v1 = xr[c1], v2 = xr[c2];
+        mn1 = fmin(mn1, v1);
+        mx1 = fmax(mx1, v1);
+        sm1 += v1;
+        mn2 = fmin(mn2, v2);
+        mx2 = fmax(mx2, v2);
+        sm2 += v2;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = h ? a2 : a1;
+        const double mn = h ? mn2 : mn1, mx = h ? mx2 : mx1, sm = h ? sm2 : sm1;
+        const bool act = a < d && mx > mn;
+        const unsigned bm = __ballot_sync(FULL, act);
+        if (act) {
+          const int p = deff + __popc(bm & lt);
+          col[p] = (int16_t)(h ? c2 : c1);
+          xb[p] = sm / (double)n;
+          sv[p] = 1.0 / (mx - mn);
         }
+        deff += __popc(bm);
       }
-      const bool act = a < d && mx > mn;
-      const unsigned bm = __ballot_sync(FULL, act);
-      if (act) {
-        const int p = deff + __popc(bm & lt);
-        col[p] = (int16_t)c;
-        xb[p] = sm / (double)n;
-        sv[p] = 1.0 / (mx - mn);
-      }
-      deff += __popc(bm);
     }
     {  // zero padding read by the fast-path fragment loads
       const int pad_end = max(32, (deff + 3) & ~3);

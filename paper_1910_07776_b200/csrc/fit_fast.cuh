@@ -7,9 +7,9 @@
 //    hoisted) and every lower 8x8 tile is accumulated on DMMA.8x8x4 in
 //    registers (templated on NB only -- the rest is compact loop code, the
 //    kernel must stay inside the instruction cache).
-//  * Factorisation: right-looking LDL^T-form Cholesky in shared memory with
-//    unscaled columns: step j only reads column j (final) and rewrites the
-//    lane's own row, so one __syncwarp per pivot; rsqrt pivots.
+//  * Factorisation: left-looking (Crout) Cholesky in shared memory, rows
+//    16-byte aligned (rb2 layout) so the row-prefix dot products use 128-bit
+//    loads; one __syncwarp per pivot; rsqrt pivots.
 //  * Solves: vectors lane-owned (lane i holds element i), pivots broadcast by
 //    shuffle, factor entries read from shared memory.
 //  * Refinement (adaptive): residual from the data rows.
@@ -29,38 +29,28 @@ struct FastView {
   int deff;
 };
 
-// Packed lower triangle of Z Z^T + lambda I; Z = Xtilde (dual) or Xtilde^T.
-template <int NB, bool DUAL>
-__device__ __forceinline__ void gram_fast(const FastView& f, int m, double lambda, double* Mpk, int lane) {
-  constexpr int NT = NB * (NB + 1) / 2;
+// Lower triangle (rb2 row layout) of Z Z^T + lambda I; Z = Xtilde (dual) or
+// Xtilde^T (primal).  One code copy for every m <= 32: up to 4 block-rows,
+// tiles beyond nb = ceil(m/8) skipped by warp-uniform branches (code size
+// matters more than the template specialisation: instruction cache).
+template <bool DUAL>
+__device__ __noinline__ void gram_fast(const FastView f, int m, double lambda, double* Mpk, int lane) {
+  constexpr int NB = 4, NT = 10;
+  const int nb = (m + 7) >> 3;
   double acc[NT][2];
 #pragma unroll
   for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
   const int rl = lane >> 2, kl = lane & 3;
+  int so[NB];
+  int ca[NB];
+  double xba[NB], sa[NB];
   if (DUAL) {
-    int so[NB];
 #pragma unroll
     for (int I = 0; I < NB; ++I) {
       const int r = I * 8 + rl;
       so[I] = r < f.n ? f.trs[r] * f.ldx : -1;
     }
-#pragma unroll 2
-    for (int k0 = 0; k0 < f.deff; k0 += 4) {
-      const int ka = k0 + kl;
-      const int c = f.col[ka];
-      const double xbv = f.xb[ka], sv = f.s[ka];
-      double fr[NB];
-#pragma unroll
-      for (int I = 0; I < NB; ++I) fr[I] = so[I] >= 0 ? (f.X[so[I] + c] - xbv) * sv : 0.0;
-      int t = 0;
-#pragma unroll
-      for (int I = 0; I < NB; ++I)
-#pragma unroll
-        for (int J = 0; J <= I; ++J, ++t) dmma(acc[t][0], acc[t][1], fr[I], fr[J]);
-    }
   } else {
-    int ca[NB];
-    double xba[NB], sa[NB];
 #pragma unroll
     for (int I = 0; I < NB; ++I) {
       const int a = I * 8 + rl;
@@ -68,18 +58,38 @@ __device__ __forceinline__ void gram_fast(const FastView& f, int m, double lambd
       xba[I] = f.xb[a];
       sa[I] = f.s[a];
     }
-#pragma unroll 2
-    for (int i0 = 0; i0 < f.n; i0 += 4) {
-      const int ri = i0 + kl;
-      const int so = ri < f.n ? f.trs[ri] * f.ldx : -1;
-      double fr[NB];
+  }
+  const int kend = DUAL ? f.deff : f.n;
+#pragma unroll 1
+  for (int k0 = 0; k0 < kend; k0 += 4) {
+    double fr[NB];
+    if (DUAL) {
+      const int ka = k0 + kl;
+      const int c = f.col[ka];
+      const double xbv = f.xb[ka], sv = f.s[ka];
 #pragma unroll
-      for (int I = 0; I < NB; ++I) fr[I] = so >= 0 ? (f.X[so + ca[I]] - xba[I]) * sa[I] : 0.0;
-      int t = 0;
+      for (int I = 0; I < NB; ++I) fr[I] = (I < nb && so[I] >= 0) ? (f.X[so[I] + c] - xbv) * sv : 0.0;
+    } else {
+      const int ri = k0 + kl;
+      const int sr = ri < f.n ? f.trs[ri] * f.ldx : -1;
 #pragma unroll
-      for (int I = 0; I < NB; ++I)
-#pragma unroll
-        for (int J = 0; J <= I; ++J, ++t) dmma(acc[t][0], acc[t][1], fr[I], fr[J]);
+      for (int I = 0; I < NB; ++I) fr[I] = (I < nb && sr >= 0) ? (f.X[sr + ca[I]] - xba[I]) * sa[I] : 0.0;
+    }
+    dmma(acc[0][0], acc[0][1], fr[0], fr[0]);
+    if (nb > 1) {
+      dmma(acc[1][0], acc[1][1], fr[1], fr[0]);
+      dmma(acc[2][0], acc[2][1], fr[1], fr[1]);
+    }
+    if (nb > 2) {
+      dmma(acc[3][0], acc[3][1], fr[2], fr[0]);
+      dmma(acc[4][0], acc[4][1], fr[2], fr[1]);
+      dmma(acc[5][0], acc[5][1], fr[2], fr[2]);
+    }
+    if (nb > 3) {
+      dmma(acc[6][0], acc[6][1], fr[3], fr[0]);
+      dmma(acc[7][0], acc[7][1], fr[3], fr[1]);
+      dmma(acc[8][0], acc[8][1], fr[3], fr[2]);
+      dmma(acc[9][0], acc[9][1], fr[3], fr[3]);
     }
   }
   int t = 0;
@@ -91,63 +101,102 @@ __device__ __forceinline__ void gram_fast(const FastView& f, int m, double lambd
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = J * 8 + 2 * kl + e;
-        if (r < m && c <= r) Mpk[pk(r, c)] = acc[t][e] + (r == c ? lambda : 0.0);
+        if (r < m && c <= r) Mpk[rb2(r) + c] = acc[t][e] + (r == c ? lambda : 0.0);
       }
     }
   __syncwarp();
 }
 
-template <bool DUAL>
-__device__ __noinline__ void gram_fast_dispatch(const FastView& f, int m, double lambda, double* Mpk, int lane) {
-  if (m <= 8) gram_fast<1, DUAL>(f, m, lambda, Mpk, lane);
-  else if (m <= 16) gram_fast<2, DUAL>(f, m, lambda, Mpk, lane);
-  else if (m <= 24) gram_fast<3, DUAL>(f, m, lambda, Mpk, lane);
-  else gram_fast<4, DUAL>(f, m, lambda, Mpk, lane);
-}
-
-// LDL^T-form Cholesky of the packed lower triangle, m <= 32, unscaled columns:
-// on exit M[i][j] (i > j) = L_ij * L_jj, and the lane's 1/L_ii is returned in
-// myinv (lane i < m).  Lane i owns row i.  Returns false on a non-positive pivot.
-__device__ __noinline__ bool chol_ldl(double* M, int m, int lane, double& myinv) {
+#if SPEEDREC_CHOL_RL
+// A/B variant (compile with -DSPEEDREC_CHOL_RL=1): right-looking LDL^T form in
+// the same rb2 layout, unscaled columns; M[i][j] (i > j) = L_ij * L_jj.
+__device__ __noinline__ bool chol_rl(double* M, int m, int lane, double& myinv) {
   bool ok = true;
   myinv = 0.0;
-  const int rb = (lane * (lane + 1)) >> 1;
+  double* ri = M + rb2(lane < m ? lane : 0);
   for (int j = 0; j < m; ++j) {
-    const double djj = M[((j * (j + 1)) >> 1) + j];
+    const double djj = M[rb2(j) + j];
     ok = ok && djj > 0.0;
     const double r = rsqrt(djj);
     if (lane == j) myinv = r;
     if (lane > j && lane < m) {
-      const double sij = M[rb + j] * (r * r);
-      int k = j + 1;
-      for (; k + 1 <= lane; k += 2) {
-        const double a0 = M[((k * (k + 1)) >> 1) + j], a1 = M[(((k + 1) * (k + 2)) >> 1) + j];
-        M[rb + k] = fma(-sij, a0, M[rb + k]);
-        M[rb + k + 1] = fma(-sij, a1, M[rb + k + 1]);
-      }
-      if (k <= lane) M[rb + k] = fma(-sij, M[((k * (k + 1)) >> 1) + j], M[rb + k]);
+      const double sij = ri[j] * (r * r);
+      for (int k = j + 1; k <= lane; ++k) ri[k] = fma(-sij, M[rb2(k) + j], ri[k]);
+    }
+    __syncwarp();
+  }
+  return ok;
+}
+__device__ __noinline__ double solve_rl(const double* M, int m, int lane, double myinv, double z) {
+  const double* ri = M + rb2(lane < m ? lane : 0);
+  for (int j = 0; j < m; ++j) {
+    if (lane == j) z *= myinv;
+    const double t = __shfl_sync(FULL, z * myinv, j);
+    if (lane > j && lane < m) z = fma(-ri[j], t, z);
+  }
+  double acc = 0.0;
+  for (int j = m - 1; j >= 0; --j) {
+    if (lane == j) z = (z - myinv * acc) * myinv;
+    const double xj = __shfl_sync(FULL, z, j);
+    if (lane < j) acc = fma(M[rb2(j) + lane], xj, acc);
+  }
+  return z;
+}
+#define chol_ll chol_rl
+#define solve_ll solve_rl
+#else
+// Left-looking (Crout) Cholesky in the 16-byte-aligned row layout rb2(), m <= 32.
+// Step j: every lane i >= j forms sum_{k<j} L_ik L_jk from final row prefixes
+// (vectorised 16-byte loads, row j broadcast), lane j takes the rsqrt pivot,
+// lanes i > j scale.  One __syncwarp per pivot, no stores of partial updates.
+// On exit M holds L (scaled); myinv = 1/L_{lane,lane}.
+__device__ __noinline__ bool chol_ll(double* M, int m, int lane, double& myinv) {
+  bool ok = true;
+  myinv = 0.0;
+  const double* ri = M + rb2(lane < m ? lane : 0);
+  double* wi = M + rb2(lane < m ? lane : 0);
+  for (int j = 0; j < m; ++j) {
+    const double* rj = M + rb2(j);
+    double s0 = 0.0, s1 = 0.0;
+    int k = 0;
+    for (; k + 1 < j; k += 2) {
+      const double2 a = *reinterpret_cast<const double2*>(ri + k);
+      const double2 b = *reinterpret_cast<const double2*>(rj + k);
+      s0 = fma(a.x, b.x, s0);
+      s1 = fma(a.y, b.y, s1);
+    }
+    if (k < j) s0 = fma(ri[k], rj[k], s0);
+    const double v = ri[j] - (s0 + s1);          // lane j: pivot; lanes i > j: unscaled L_ij
+    const double r = __shfl_sync(FULL, rsqrt(v), j);
+    const double dj = __shfl_sync(FULL, v, j);
+    ok = ok && dj > 0.0;
+    if (lane == j) {
+      wi[j] = v * r;
+      myinv = r;
+    } else if (lane > j && lane < m) {
+      wi[j] = v * r;
     }
     __syncwarp();
   }
   return ok;
 }
 
-// z <- (L L^T)^{-1} z for the chol_ldl factor; z lane-owned, m <= 32.
-__device__ __noinline__ double solve_ldl(const double* M, int m, int lane, double myinv, double z) {
-  const int rb = (lane * (lane + 1)) >> 1;
+// z <- (L L^T)^{-1} z for the chol_ll factor; z lane-owned, m <= 32.
+__device__ __noinline__ double solve_ll(const double* M, int m, int lane, double myinv, double z) {
+  const double* ri = M + rb2(lane < m ? lane : 0);
   for (int j = 0; j < m; ++j) {                     // forward: L y = z
     if (lane == j) z *= myinv;
-    const double t = __shfl_sync(FULL, z * myinv, j);  // y_j / L_jj
-    if (lane > j && lane < m) z = fma(-M[rb + j], t, z);
+    const double yj = __shfl_sync(FULL, z, j);
+    if (lane > j && lane < m) z = fma(-ri[j], yj, z);
   }
-  double acc = 0.0;
   for (int j = m - 1; j >= 0; --j) {                // backward: L^T x = y
-    if (lane == j) z = (z - myinv * acc) * myinv;
+    if (lane == j) z *= myinv;
     const double xj = __shfl_sync(FULL, z, j);
-    if (lane < j) acc = fma(M[((j * (j + 1)) >> 1) + lane], xj, acc);
+    if (lane < j) z = fma(-M[rb2(j) + lane], xj, z);
   }
   return z;
 }
+#endif
 
 // w'_a = s_a * sum_i (x_ia - xb_a) * alpha_i, alpha lane-owned (n <= 32);
 // lanes over features, written to wout[0..deff).
@@ -183,19 +232,19 @@ template <bool DUAL>
 __device__ bool fit_fast(const FastView& f, const double* yc, double lambda, int refine, double* Mpk,
                          double* scratch, double* uwork, double* wout, int lane) {
   const int m = DUAL ? f.n : f.deff;
-  gram_fast_dispatch<DUAL>(f, m, lambda, Mpk, lane);
+  gram_fast<DUAL>(f, m, lambda, Mpk, lane);
   double myinv;
-  const bool ok = chol_ldl(Mpk, m, lane, myinv);
+  const bool ok = chol_ll(Mpk, m, lane, myinv);
   if (DUAL) {
     double alpha = lane < f.n ? yc[lane] : 0.0;
-    alpha = solve_ldl(Mpk, m, lane, myinv, alpha);
+    alpha = solve_ll(Mpk, m, lane, myinv, alpha);
     for (int it = 0; it < refine; ++it) {
       xt_alpha_lanes(f, alpha, wout, lane);
       for (int a = lane; a < f.deff; a += 32) uwork[a] = wout[a] * f.s[a];
       __syncwarp();
       double e = 0.0;
       if (lane < f.n) e = yc[lane] - xrow_dot(f, f.X + f.trs[lane] * f.ldx, uwork) - lambda * alpha;
-      alpha += solve_ldl(Mpk, m, lane, myinv, e);
+      alpha += solve_ll(Mpk, m, lane, myinv, e);
       __syncwarp();
     }
     xt_alpha_lanes(f, alpha, wout, lane);
@@ -208,7 +257,7 @@ __device__ bool fit_fast(const FastView& f, const double* yc, double lambda, int
       for (int i = 0; i < f.n; ++i) w = fma(f.X[f.trs[i] * f.ldx + c] - x0, yc[i], w);
       w *= f.s[lane];
     }
-    w = solve_ldl(Mpk, m, lane, myinv, w);
+    w = solve_ll(Mpk, m, lane, myinv, w);
     for (int it = 0; it < refine; ++it) {
       if (lane < f.deff) uwork[lane] = w * f.s[lane];
       __syncwarp();
@@ -221,7 +270,7 @@ __device__ bool fit_fast(const FastView& f, const double* yc, double lambda, int
         for (int i = 0; i < f.n; ++i) r = fma(f.X[f.trs[i] * f.ldx + c] - x0, scratch[i], r);
         r = r * f.s[lane] - lambda * w;
       }
-      w += solve_ldl(Mpk, m, lane, myinv, r);
+      w += solve_ll(Mpk, m, lane, myinv, r);
       __syncwarp();
     }
     if (lane < f.deff) wout[lane] = w;

@@ -173,6 +173,9 @@ __device__ __forceinline__ bool feature_in(const ScenDesc& D, long long fidx, in
 __device__ __forceinline__ int ins0(int k, int b) { return ((k >> b) << (b + 1)) | (k & ((1 << b) - 1)); }
 __device__ __forceinline__ int rmv(int v, int b) { return (v & ((1 << b) - 1)) | ((v >> (b + 1)) << b); }
 __device__ __forceinline__ int pk(int r, int c) { return ((r * (r + 1)) >> 1) + c; }
+// Row offset of a lower-triangular layout whose rows are padded to even
+// length (16-byte aligned rows): rb2(2p) = 2p(p+1), rb2(2p+1) = 2(p+1)^2.
+__host__ __device__ __forceinline__ int rb2(int i) { const int p = i >> 1; return (i & 1) ? 2 * (p + 1) * (p + 1) : 2 * p * (p + 1); }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -464,7 +464,7 @@ WarpLayout plan_layout(const sr_ctx* c, int mcap) {
   L.vmax = vmax;
   L.off_v2 = take(8 * vmax);
   L.mcap = mcap;
-  L.off_M = take(8 * (mcap * (mcap + 1) / 2));
+  L.off_M = take(8 * std::max(rb2(mcap), mcap * (mcap + 1) / 2));
   L.off_ufull = take(8 * c->C);
   L.bytes = align16(off);
   return L;

@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspeedrec.so")
+LIB_PATH = os.environ.get("SPEEDREC_LIB") or os.path.join(_HERE, "libspeedrec.so")  # env: A/B kernel variants
 
 SR_OK, SR_E_ARG, SR_E_DATA, SR_E_LATTICE, SR_E_EMPTY, SR_E_STATE, SR_E_OOM, SR_E_CUDA, SR_E_UNSUPPORTED = \
     0, -1, -2, -3, -4, -5, -6, -7, -8
