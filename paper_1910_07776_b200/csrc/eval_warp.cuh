@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
     __syncwarp();
     int n = 0, nt = 0;
     uint64_t fptr = 0, fpte = 0;
+    #pragma unroll 1
     for (int g = 0; g < G; ++g) {
       const int b = obit[(g / A.IR) * O + o];
       const uint64_t tr = trw[g], te = tew[g];
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
       const int c1 = a1 < d ? F[a1] : 0, c2 = a2 < d ? F[a2] : 0;
       const double* x0 = X + (long long)trs[0] * ldx;
       double mn1 = x0[c1], mx1 = mn1, sm1 = mn1, mn2 = x0[c2], mx2 = mn2, sm2 = mn2;
+      #pragma unroll 2
       for (int i = 1; i < n; ++i) {
         const double* xr = X + (long long)trs[i] * ldx;
         const double v1 = xr[c1], v2 = xr[c2];
@@ -338,6 +340,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
       }
     }
     double ysum = 0.0;
+    #pragma unroll 1
     for (int i = lane; i < n; i += 32) ysum += yc[i];
     const double ybar = warp_sum(ysum) / (double)n;
     for (int i = lane; i < n; i += 32) yc[i] -= ybar;
@@ -378,6 +381,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
       const double* xr = X + (long long)tes[j] * ldx;
       double e0 = 0.0, e1 = 0.0;
       int c = 0;
+      #pragma unroll 2
       for (; c + 1 < C; c += 2) {
         e0 = fma(xr[c], ufull[c], e0);
         e1 = fma(xr[c + 1], ufull[c + 1], e1);
@@ -458,6 +462,7 @@ __global__ void __launch_bounds__(256) k_rank_warp(const EvalArgs A) {
     }
     const double* ext = A.extab + sl * A.ex_stride;
     int nrec = 0, nhit = 0, guard = 0, untrained = 0;
+    #pragma unroll 1
     for (int g = 0; g < G; ++g) {
       uint64_t tr, te;
       member_words(A.sd, split, g, tr, te);

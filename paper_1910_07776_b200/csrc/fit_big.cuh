@@ -481,26 +481,32 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
         // residual r = X~^T (yc - X~ w') - lambda w' streamed over the training rows
         for (int a = t; a < kBigMaxD; a += kBigThreads) rhs[a] = 0.0;
         __syncthreads();
-        double rp[16];
+        // Register-only pass: thread (row t>>3, features (t&7)+8q) holds its 16
+        // centred values; the row's residual is a 3-step shuffle reduction over
+        // the 8 threads of the row (fixed order), next chunk prefetched.
+        double rp[16], wq[16], vn[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) rp[q] = 0.0;
-        for (int ch = 0; ch < (n + kBigChunk - 1) / kBigChunk; ++ch) {
-          big_load_chunk(A.x, C, trs, n, ch * kBigChunk, col, xb, sv, deff, v);
-          big_store_chunk(rch, v);
-          __syncthreads();
-          // e_r for the 32 rows: warp w handles rows 4w..4w+3
-          for (int rr = warp * 4; rr < warp * 4 + 4; ++rr) {
-            double dacc = 0.0;
-            for (int a = lane; a < deff; a += 32) dacc = fma(rch[rr * kBigLd + a], wv[a], dacc);
-            dacc = warp_sum(dacc);
-            const int gr = ch * kBigChunk + rr;
-            if (lane == 0) ych[rr] = gr < n ? yl[gr] - dacc : 0.0;
-          }
-          __syncthreads();
-          const int r = t >> 3, a0 = t & 7;
+        for (int q = 0; q < 16; ++q) {
+          rp[q] = 0.0;
+          const int a = (t & 7) + 8 * q;
+          wq[q] = a < deff ? wv[a] : 0.0;
+        }
+        const int nch = (n + kBigChunk - 1) / kBigChunk;
+        big_load_chunk(A.x, C, trs, n, 0, col, xb, sv, deff, v);
+        for (int ch = 0; ch < nch; ++ch) {
+          if (ch + 1 < nch) big_load_chunk(A.x, C, trs, n, (ch + 1) * kBigChunk, col, xb, sv, deff, vn);
+          double dot = 0.0;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) rp[q] = fma(rch[r * kBigLd + a0 + 8 * q], ych[r], rp[q]);
-          __syncthreads();
+          for (int q = 0; q < 16; ++q) dot = fma(v[q], wq[q], dot);
+          dot += __shfl_xor_sync(FULL, dot, 1);
+          dot += __shfl_xor_sync(FULL, dot, 2);
+          dot += __shfl_xor_sync(FULL, dot, 4);
+          const int gr = ch * kBigChunk + (t >> 3);
+          const double e = gr < n ? yl[gr] - dot : 0.0;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) rp[q] = fma(v[q], e, rp[q]);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] = vn[q];
         }
         {
           double* part = rpt;  // never aliases the factor in Gbuf

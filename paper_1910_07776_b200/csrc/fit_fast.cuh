@@ -114,6 +114,7 @@ __device__ __noinline__ bool chol_rl(double* M, int m, int lane, double& myinv) 
   bool ok = true;
   myinv = 0.0;
   double* ri = M + rb2(lane < m ? lane : 0);
+  #pragma unroll 1
   for (int j = 0; j < m; ++j) {
     const double djj = M[rb2(j) + j];
     ok = ok && djj > 0.0;
@@ -129,12 +130,14 @@ __device__ __noinline__ bool chol_rl(double* M, int m, int lane, double& myinv) 
 }
 __device__ __noinline__ double solve_rl(const double* M, int m, int lane, double myinv, double z) {
   const double* ri = M + rb2(lane < m ? lane : 0);
+  #pragma unroll 1
   for (int j = 0; j < m; ++j) {
     if (lane == j) z *= myinv;
     const double t = __shfl_sync(FULL, z * myinv, j);
     if (lane > j && lane < m) z = fma(-ri[j], t, z);
   }
   double acc = 0.0;
+  #pragma unroll 1
   for (int j = m - 1; j >= 0; --j) {
     if (lane == j) z = (z - myinv * acc) * myinv;
     const double xj = __shfl_sync(FULL, z, j);
@@ -155,10 +158,12 @@ __device__ __noinline__ bool chol_ll(double* M, int m, int lane, double& myinv) 
   myinv = 0.0;
   const double* ri = M + rb2(lane < m ? lane : 0);
   double* wi = M + rb2(lane < m ? lane : 0);
+  #pragma unroll 1
   for (int j = 0; j < m; ++j) {
     const double* rj = M + rb2(j);
     double s0 = 0.0, s1 = 0.0;
     int k = 0;
+    #pragma unroll 2
     for (; k + 1 < j; k += 2) {
       const double2 a = *reinterpret_cast<const double2*>(ri + k);
       const double2 b = *reinterpret_cast<const double2*>(rj + k);
@@ -184,11 +189,13 @@ __device__ __noinline__ bool chol_ll(double* M, int m, int lane, double& myinv) 
 // z <- (L L^T)^{-1} z for the chol_ll factor; z lane-owned, m <= 32.
 __device__ __noinline__ double solve_ll(const double* M, int m, int lane, double myinv, double z) {
   const double* ri = M + rb2(lane < m ? lane : 0);
+  #pragma unroll 1
   for (int j = 0; j < m; ++j) {                     // forward: L y = z
     if (lane == j) z *= myinv;
     const double yj = __shfl_sync(FULL, z, j);
     if (lane > j && lane < m) z = fma(-ri[j], yj, z);
   }
+  #pragma unroll 1
   for (int j = m - 1; j >= 0; --j) {                // backward: L^T x = y
     if (lane == j) z *= myinv;
     const double xj = __shfl_sync(FULL, z, j);
@@ -206,6 +213,7 @@ __device__ __noinline__ void xt_alpha_lanes(const FastView& f, double alpha, dou
     const int c1 = f.col[a1 < f.deff ? a1 : 0], c2 = f.col[a2 < f.deff ? a2 : 0];
     const double x1 = f.xb[a1 < f.deff ? a1 : 0], x2 = f.xb[a2 < f.deff ? a2 : 0];
     double acc1 = 0.0, acc2 = 0.0;
+    #pragma unroll 2
     for (int i = 0; i < f.n; ++i) {
       const double ai = __shfl_sync(FULL, alpha, i);
       const double* xr = f.X + f.trs[i] * f.ldx;
