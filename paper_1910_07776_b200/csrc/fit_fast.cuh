@@ -16,6 +16,14 @@
 #pragma once
 #include "kernels.cuh"
 
+// Fast-path helpers are inlined by default; -DSPEEDREC_NOINLINE_FAST=1 keeps
+// them out of line (A/B of code size vs call overhead, tools/ab_variants.sh).
+#if SPEEDREC_NOINLINE_FAST
+#define SR_FAST_FN __noinline__
+#else
+#define SR_FAST_FN __forceinline__
+#endif
+
 namespace speedrec {
 
 struct FastView {
@@ -34,7 +42,7 @@ struct FastView {
 // tiles beyond nb = ceil(m/8) skipped by warp-uniform branches (code size
 // matters more than the template specialisation: instruction cache).
 template <bool DUAL>
-__device__ __noinline__ void gram_fast(const FastView f, int m, double lambda, double* Mpk, int lane) {
+__device__ SR_FAST_FN void gram_fast(const FastView f, int m, double lambda, double* Mpk, int lane) {
   constexpr int NB = 4, NT = 10;
   const int nb = (m + 7) >> 3;
   double acc[NT][2];
@@ -110,7 +118,7 @@ __device__ __noinline__ void gram_fast(const FastView f, int m, double lambda, d
 #if SPEEDREC_CHOL_RL
 // A/B variant (compile with -DSPEEDREC_CHOL_RL=1): right-looking LDL^T form in
 // the same rb2 layout, unscaled columns; M[i][j] (i > j) = L_ij * L_jj.
-__device__ __noinline__ bool chol_rl(double* M, int m, int lane, double& myinv) {
+__device__ SR_FAST_FN bool chol_rl(double* M, int m, int lane, double& myinv) {
   bool ok = true;
   myinv = 0.0;
   double* ri = M + rb2(lane < m ? lane : 0);
@@ -128,7 +136,7 @@ __device__ __noinline__ bool chol_rl(double* M, int m, int lane, double& myinv) 
   }
   return ok;
 }
-__device__ __noinline__ double solve_rl(const double* M, int m, int lane, double myinv, double z) {
+__device__ SR_FAST_FN double solve_rl(const double* M, int m, int lane, double myinv, double z) {
   const double* ri = M + rb2(lane < m ? lane : 0);
   #pragma unroll 1
   for (int j = 0; j < m; ++j) {
@@ -153,14 +161,13 @@ __device__ __noinline__ double solve_rl(const double* M, int m, int lane, double
 // (vectorised 16-byte loads, row j broadcast), lane j takes the rsqrt pivot,
 // lanes i > j scale.  One __syncwarp per pivot, no stores of partial updates.
 // On exit M holds L (scaled); myinv = 1/L_{lane,lane}.
-__device__ __noinline__ bool chol_ll(double* M, int m, int lane, double& myinv) {
+__device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv) {
   bool ok = true;
   myinv = 0.0;
-  const double* ri = M + rb2(lane < m ? lane : 0);
-  double* wi = M + rb2(lane < m ? lane : 0);
+  double* ri = M + rb2(lane < m ? lane : 0);
+  const double* rj = M;                           // row j, advanced by its padded length
   #pragma unroll 1
   for (int j = 0; j < m; ++j) {
-    const double* rj = M + rb2(j);
     double s0 = 0.0, s1 = 0.0;
     int k = 0;
     #pragma unroll 2
@@ -172,22 +179,18 @@ __device__ __noinline__ bool chol_ll(double* M, int m, int lane, double& myinv) 
     }
     if (k < j) s0 = fma(ri[k], rj[k], s0);
     const double v = ri[j] - (s0 + s1);          // lane j: pivot; lanes i > j: unscaled L_ij
-    const double r = __shfl_sync(FULL, rsqrt(v), j);
-    const double dj = __shfl_sync(FULL, v, j);
-    ok = ok && dj > 0.0;
-    if (lane == j) {
-      wi[j] = v * r;
-      myinv = r;
-    } else if (lane > j && lane < m) {
-      wi[j] = v * r;
-    }
+    const double r = __shfl_sync(FULL, rsqrt(v), j);  // 1/L_jj (NaN/inf iff the pivot is not > 0)
+    ok = ok && r > 0.0 && r < INFINITY;
+    if (lane >= j && lane < m) ri[j] = v * r;
+    if (lane == j) myinv = r;
+    rj += (j + 2) & ~1;
     __syncwarp();
   }
   return ok;
 }
 
 // z <- (L L^T)^{-1} z for the chol_ll factor; z lane-owned, m <= 32.
-__device__ __noinline__ double solve_ll(const double* M, int m, int lane, double myinv, double z) {
+__device__ SR_FAST_FN double solve_ll(const double* M, int m, int lane, double myinv, double z) {
   const double* ri = M + rb2(lane < m ? lane : 0);
   #pragma unroll 1
   for (int j = 0; j < m; ++j) {                     // forward: L y = z
@@ -195,11 +198,13 @@ __device__ __noinline__ double solve_ll(const double* M, int m, int lane, double
     const double yj = __shfl_sync(FULL, z, j);
     if (lane > j && lane < m) z = fma(-ri[j], yj, z);
   }
+  const double* rj = M + rb2(m - 1) + lane;         // row j, column `lane`
   #pragma unroll 1
   for (int j = m - 1; j >= 0; --j) {                // backward: L^T x = y
     if (lane == j) z *= myinv;
     const double xj = __shfl_sync(FULL, z, j);
-    if (lane < j) z = fma(-M[rb2(j) + lane], xj, z);
+    if (lane < j) z = fma(-*rj, xj, z);
+    rj -= (j + 1) & ~1;                             // padded length of row j-1
   }
   return z;
 }
@@ -207,7 +212,10 @@ __device__ __noinline__ double solve_ll(const double* M, int m, int lane, double
 
 // w'_a = s_a * sum_i (x_ia - xb_a) * alpha_i, alpha lane-owned (n <= 32);
 // lanes over features, written to wout[0..deff).
-__device__ __noinline__ void xt_alpha_lanes(const FastView& f, double alpha, double* wout, int lane) {
+__device__ SR_FAST_FN void xt_alpha_lanes(const FastView& f, double alpha, double* wout, int lane,
+                                           double* abuf) {
+  if (lane < f.n) abuf[lane] = alpha;   // broadcast through shared memory (1 LDS per row, no shuffles)
+  __syncwarp();
   for (int a0 = 0; a0 < f.deff; a0 += 64) {
     const int a1 = a0 + lane, a2 = a0 + 32 + lane;
     const int c1 = f.col[a1 < f.deff ? a1 : 0], c2 = f.col[a2 < f.deff ? a2 : 0];
@@ -215,7 +223,7 @@ __device__ __noinline__ void xt_alpha_lanes(const FastView& f, double alpha, dou
     double acc1 = 0.0, acc2 = 0.0;
     #pragma unroll 2
     for (int i = 0; i < f.n; ++i) {
-      const double ai = __shfl_sync(FULL, alpha, i);
+      const double ai = abuf[i];
       const double* xr = f.X + f.trs[i] * f.ldx;
       acc1 = fma(xr[c1] - x1, ai, acc1);
       acc2 = fma(xr[c2] - x2, ai, acc2);
@@ -247,7 +255,7 @@ __device__ bool fit_fast(const FastView& f, const double* yc, double lambda, int
     double alpha = lane < f.n ? yc[lane] : 0.0;
     alpha = solve_ll(Mpk, m, lane, myinv, alpha);
     for (int it = 0; it < refine; ++it) {
-      xt_alpha_lanes(f, alpha, wout, lane);
+      xt_alpha_lanes(f, alpha, wout, lane, scratch);
       for (int a = lane; a < f.deff; a += 32) uwork[a] = wout[a] * f.s[a];
       __syncwarp();
       double e = 0.0;
@@ -255,7 +263,7 @@ __device__ bool fit_fast(const FastView& f, const double* yc, double lambda, int
       alpha += solve_ll(Mpk, m, lane, myinv, e);
       __syncwarp();
     }
-    xt_alpha_lanes(f, alpha, wout, lane);
+    xt_alpha_lanes(f, alpha, wout, lane, scratch);
   } else {
     // rhs_a = s_a * sum_i (x_ia - xb_a) * yc_i, lane a < deff <= 32
     double w = 0.0;

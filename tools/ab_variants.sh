@@ -3,7 +3,7 @@
 # bench workload under gpurun:   ./tools/ab_variants.sh build ; ./tools/ab_variants.sh run
 cd "$(dirname "$0")/.."
 NVCC="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -shared -Xcompiler -fPIC"
-declare -A V=( [base]="" [chol_rl]="-DSPEEDREC_CHOL_RL=1" )
+declare -A V=( [base]="" [noinline]="-DSPEEDREC_NOINLINE_FAST=1" [chol_rl]="-DSPEEDREC_CHOL_RL=1" )
 if [ "$1" = "build" ]; then
   mkdir -p build
   for k in "${!V[@]}"; do $NVCC ${V[$k]} -o build/libspeedrec_$k.so paper_1910_07776_b200/csrc/speedrec.cu || exit 1; done
