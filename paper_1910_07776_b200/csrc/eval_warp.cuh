@@ -379,15 +379,19 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
     double rsum = 0.0, rmin = INFINITY, rmax = -INFINITY;
     for (int j = lane; j < nt; j += 32) {
       const double* xr = X + (long long)tes[j] * ldx;
-      double e0 = 0.0, e1 = 0.0;
+      double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;   // 4 independent chains
       int c = 0;
-      #pragma unroll 2
-      for (; c + 1 < C; c += 2) {
-        e0 = fma(xr[c], ufull[c], e0);
-        e1 = fma(xr[c + 1], ufull[c + 1], e1);
+      #pragma unroll 1
+      for (; c + 3 < C; c += 4) {
+        const double2 u01 = *reinterpret_cast<const double2*>(ufull + c);
+        const double2 u23 = *reinterpret_cast<const double2*>(ufull + c + 2);
+        e0 = fma(xr[c], u01.x, e0);
+        e1 = fma(xr[c + 1], u01.y, e1);
+        e2 = fma(xr[c + 2], u23.x, e2);
+        e3 = fma(xr[c + 3], u23.y, e3);
       }
-      if (c < C) e0 = fma(xr[c], ufull[c], e0);
-      double e = c0 + (e0 + e1);
+      for (; c < C; ++c) e0 = fma(xr[c], ufull[c], e0);
+      double e = c0 + ((e0 + e1) + (e2 + e3));
       if (near_tol(e, 0.0, A.guard_tol) || near_tol(e, 1.0, A.guard_tol)) ++guard;
       bool cl = false;
       if (e <= 0.0) {

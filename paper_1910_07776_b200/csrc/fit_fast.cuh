@@ -180,12 +180,14 @@ __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv) {
     if (k < j) s0 = fma(ri[k], rj[k], s0);
     const double v = ri[j] - (s0 + s1);          // lane j: pivot; lanes i > j: unscaled L_ij
     const double r = __shfl_sync(FULL, rsqrt(v), j);  // 1/L_jj (NaN/inf iff the pivot is not > 0)
-    ok = ok && r > 0.0 && r < INFINITY;
     if (lane >= j && lane < m) ri[j] = v * r;
     if (lane == j) myinv = r;
     rj += (j + 2) & ~1;
     __syncwarp();
   }
+  // a non-positive pivot makes its 1/L_jj NaN or inf (and NaN propagates to
+  // later pivots): one vote at the end instead of a test per step
+  ok = __all_sync(FULL, lane >= m || (myinv > 0.0 && myinv < INFINITY));
   return ok;
 }
 
