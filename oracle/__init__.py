@@ -48,7 +48,8 @@ class OrScenarios(ct.Structure):
 
 class OrParams(ct.Structure):
     _fields_ = [("ridge", ct.c_double), ("threshold", ct.c_double), ("clamp_floor", ct.c_double),
-                ("guard_tol", ct.c_double), ("max_count", ct.c_int32)]
+                ("guard_tol", ct.c_double), ("max_count", ct.c_int32), ("learner", ct.c_int32),
+                ("k_nn", ct.c_int32)]
 
 
 OPT_SCORE_DTYPE = np.dtype([("n_train", "<i4"), ("n_test", "<i4"), ("n_correct", "<i4"),
@@ -76,6 +77,9 @@ def lib():
         _lib.or_fit_predict.argtypes = [ct.c_int32, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_void_p,
                                         ct.c_int32, ct.c_void_p, ct.c_double, ct.c_void_p, ct.c_void_p]
         _lib.or_rank.restype = ct.c_int32
+        _lib.or_knn_predict.restype = None
+        _lib.or_knn_predict.argtypes = [ct.c_int32, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_void_p,
+                                        ct.c_int32, ct.c_void_p, ct.c_int32, ct.c_void_p]
         _lib.or_rank.argtypes = [ct.c_int32, ct.c_void_p, ct.c_void_p, ct.c_double, ct.c_int32,
                                  ct.c_void_p, ct.c_void_p]
         _lib.or_sign_correct.restype = ct.c_int32
@@ -137,6 +141,18 @@ def fit_predict(Xs: np.ndarray, y: np.ndarray, Xts: np.ndarray, ridge: float = 1
     return ex, coef
 
 
+def knn_predict(Xs: np.ndarray, y: np.ndarray, Xts: np.ndarray, k: int = 10) -> np.ndarray:
+    """IBK on already-scaled features (see or_knn_predict for the exact form)."""
+    Xs = np.ascontiguousarray(Xs, dtype=np.float64)
+    n, d = Xs.shape
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    Xts = np.ascontiguousarray(Xts, dtype=np.float64).reshape(-1, d) if d else np.zeros((len(Xts), 0))
+    ex = np.zeros(Xts.shape[0])
+    lib().or_knn_predict(n, d, max(d, 1), _p(Xs) if d else _p(np.zeros(max(n, 1))), _p(y), Xts.shape[0],
+                         _p(Xts) if d else _p(np.zeros(max(len(ex), 1))), k, _p(ex))
+    return ex
+
+
 def rank(ex, ids, threshold: float = 1.05, max_count: int = 3):
     """Tier-3 rank-and-filter; returns (full order of ids, recommended ids)."""
     ex = np.ascontiguousarray(ex, dtype=np.float64)
@@ -177,7 +193,8 @@ def aggregate_masks(opt, scn, n_folds: int, first_mask: int = 0, top_k: int = 64
 
 
 # ---------------------------------------------------------------- batch
-DEFAULT_PARAMS = dict(ridge=1e-8, threshold=1.05, clamp_floor=0.01, guard_tol=1e-9, max_count=3)
+DEFAULT_PARAMS = dict(ridge=1e-8, threshold=1.05, clamp_floor=0.01, guard_tol=1e-9, max_count=3, learner=0,
+                      k_nn=10)
 
 
 def evaluate(ds, sc, first: int = 0, count: int | None = None, want_ex: bool = False,
@@ -216,7 +233,7 @@ def evaluate(ds, sc, first: int = 0, count: int | None = None, want_ex: bool = F
     s = OrScenarios(kind, sc.group_words, sc.n_splits, _p(tg), _p(eg), _p(om), _p(pg),
                     sc.seed, sc.opt_mask, sc.all_subsets_k, sc.n_masks, _p(fm))
     p = OrParams(prm["ridge"], prm["threshold"], prm["clamp_floor"], prm["guard_tol"],
-                 prm["max_count"])
+                 prm["max_count"], prm["learner"], prm["k_nn"])
     O = ds.n_opt_ids
     G = ds.n_programs * ds.n_inputs * ds.n_runs
     V = 1 << ds.n_opt_bits

@@ -66,6 +66,8 @@ typedef struct {
   double clamp_floor;              /* 0.01 */
   double guard_tol;                /* 1e-9 (reading R21) */
   int32_t max_count;               /* 3 */
+  int32_t learner;                 /* 0 ridge least squares (reading D1), 1 IBK k-NN */
+  int32_t k_nn;                    /* IBK k, 10 */
 } or_params;
 
 typedef struct {
@@ -219,6 +221,53 @@ int32_t or_fit_predict(int32_t n, int32_t d, int32_t ld, const double* Xs, const
 /* (EX desc, id asc), keep EX >= threshold (reading R8), first    */
 /* max_count (R9).  rec_out gets the kept ids; returns how many.          */
 /* ------------------------------------------------------------------ */
+/* ------------------------------------------------------------------ */
+/* IBK (NEXT-1; SPEC S:195-212 for the regression reading):   */
+/* "Similarity is measured by the Euclidean distance between the feature */
+/* vectors of the test and training instances ... k = 10".  Reading R19: */
+/* the label aggregate is the mean of the k nearest labels.  Exact form: */
+/*   D_i = sum_a (x'_ta - x'_ia)^2 accumulated in feature order with one */
+/*         fma per term (starting from 0), x' the min-max scaled features */
+/*         (inactive features contribute 0 and are skipped);              */
+/*   neighbours = the min(k, n) smallest (D_i, i) (ties -> lower stored   */
+/*         index);                                                 */
+/*   EX = (sum of their labels, added in neighbour order) / min(k, n).    */
+/* Every operation is a correctly rounded IEEE op, so the result is a     */
+/* pure function of the inputs (bit-exact target for the GPU path).       */
+/* ------------------------------------------------------------------ */
+void or_knn_predict(int32_t n, int32_t d, int32_t ld, const double* Xs, const double* y, int32_t t,
+                    const double* Xts, int32_t k, double* ex_out) {
+  int32_t kk = k < n ? k : n;
+  double* bd = (double*)malloc(sizeof(double) * (size_t)(kk > 0 ? kk : 1));
+  int32_t* bi = (int32_t*)malloc(sizeof(int32_t) * (size_t)(kk > 0 ? kk : 1));
+  for (int32_t j = 0; j < t; ++j) {
+    int32_t cnt = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      double D = 0.0;
+      for (int32_t a = 0; a < d; ++a) {
+        double dl = Xts[(int64_t)j * ld + a] - Xs[(int64_t)i * ld + a];
+        D = fma(dl, dl, D);
+      }
+      /* insert (D, i) into the sorted list of the best kk (i ascending => ties keep order) */
+      if (cnt < kk || D < bd[cnt - 1]) {
+        int32_t p = cnt < kk ? cnt++ : kk - 1;
+        while (p > 0 && bd[p - 1] > D) {
+          bd[p] = bd[p - 1];
+          bi[p] = bi[p - 1];
+          --p;
+        }
+        bd[p] = D;
+        bi[p] = i;
+      }
+    }
+    double s = 0.0;
+    for (int32_t q = 0; q < kk; ++q) s += y[bi[q]];
+    ex_out[j] = s / (double)kk;
+  }
+  free(bd);
+  free(bi);
+}
+
 int32_t or_rank(int32_t n_cand, const double* ex, const int32_t* ids, double threshold,
                 int32_t max_count, int32_t* order_out, int32_t* rec_out) {
   int32_t ord[64];
@@ -377,7 +426,9 @@ static void eval_scenario(const or_job* J, int64_t s, or_opt_score* orow, or_scn
     for (int32_t j = 0; j < nt; ++j)
       for (int32_t a = 0; a < d; ++a) Xtr[(int64_t)j * d + a] = J->x[(int64_t)te_before[j] * C + F[a]];
     int32_t d_eff = d > 0 ? or_scale(n, d, Xr, nt, Xtr, Xs, Xts, NULL) : 0;
-    if (or_fit_predict(n, d_eff, d > 0 ? d : 1, Xs, tr_y, nt, Xts, pr->ridge, te_ex, NULL) != 0) {
+    if (pr->learner == 1) {
+      or_knn_predict(n, d_eff, d > 0 ? d : 1, Xs, tr_y, nt, Xts, pr->k_nn, te_ex);
+    } else if (or_fit_predict(n, d_eff, d > 0 ? d : 1, Xs, tr_y, nt, Xts, pr->ridge, te_ex, NULL) != 0) {
       /* unreachable for lambda > 0 (G + lambda I is SPD); poison the row */
       srow->n_guard = -1000000;
     }

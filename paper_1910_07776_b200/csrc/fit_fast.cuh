@@ -70,48 +70,61 @@ __device__ SR_FAST_FN void gram_fast(const FastView f, int m, double lambda, dou
   const int kend = DUAL ? f.deff : f.n;
 #pragma unroll 1
   for (int k0 = 0; k0 < kend; k0 += 4) {
+    // fragments of block-rows >= nb are never formed (warp-uniform branches)
     double fr[NB];
+    int c = 0, sr = -1;
+    double xbv = 0.0, sv = 0.0;
     if (DUAL) {
       const int ka = k0 + kl;
-      const int c = f.col[ka];
-      const double xbv = f.xb[ka], sv = f.s[ka];
-#pragma unroll
-      for (int I = 0; I < NB; ++I) fr[I] = (I < nb && so[I] >= 0) ? (f.X[so[I] + c] - xbv) * sv : 0.0;
+      c = f.col[ka];
+      xbv = f.xb[ka];
+      sv = f.s[ka];
     } else {
       const int ri = k0 + kl;
-      const int sr = ri < f.n ? f.trs[ri] * f.ldx : -1;
-#pragma unroll
-      for (int I = 0; I < NB; ++I) fr[I] = (I < nb && sr >= 0) ? (f.X[sr + ca[I]] - xba[I]) * sa[I] : 0.0;
+      sr = ri < f.n ? f.trs[ri] * f.ldx : -1;
     }
+    auto frag = [&](int I) -> double {
+      if (DUAL) return so[I] >= 0 ? (f.X[so[I] + c] - xbv) * sv : 0.0;
+      return sr >= 0 ? (f.X[sr + ca[I]] - xba[I]) * sa[I] : 0.0;
+    };
+    fr[0] = frag(0);
     dmma(acc[0][0], acc[0][1], fr[0], fr[0]);
     if (nb > 1) {
+      fr[1] = frag(1);
       dmma(acc[1][0], acc[1][1], fr[1], fr[0]);
       dmma(acc[2][0], acc[2][1], fr[1], fr[1]);
-    }
-    if (nb > 2) {
-      dmma(acc[3][0], acc[3][1], fr[2], fr[0]);
-      dmma(acc[4][0], acc[4][1], fr[2], fr[1]);
-      dmma(acc[5][0], acc[5][1], fr[2], fr[2]);
-    }
-    if (nb > 3) {
-      dmma(acc[6][0], acc[6][1], fr[3], fr[0]);
-      dmma(acc[7][0], acc[7][1], fr[3], fr[1]);
-      dmma(acc[8][0], acc[8][1], fr[3], fr[2]);
-      dmma(acc[9][0], acc[9][1], fr[3], fr[3]);
+      if (nb > 2) {
+        fr[2] = frag(2);
+        dmma(acc[3][0], acc[3][1], fr[2], fr[0]);
+        dmma(acc[4][0], acc[4][1], fr[2], fr[1]);
+        dmma(acc[5][0], acc[5][1], fr[2], fr[2]);
+        if (nb > 3) {
+          fr[3] = frag(3);
+          dmma(acc[6][0], acc[6][1], fr[3], fr[0]);
+          dmma(acc[7][0], acc[7][1], fr[3], fr[1]);
+          dmma(acc[8][0], acc[8][1], fr[3], fr[2]);
+          dmma(acc[9][0], acc[9][1], fr[3], fr[3]);
+        }
+      }
     }
   }
   int t = 0;
 #pragma unroll
-  for (int I = 0; I < NB; ++I)
-#pragma unroll
-    for (int J = 0; J <= I; ++J, ++t) {
+  for (int I = 0; I < NB; ++I) {
+    if (I < nb) {
       const int r = I * 8 + rl;
+      double* Mr = Mpk + rb2(r);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = J * 8 + 2 * kl + e;
-        if (r < m && c <= r) Mpk[rb2(r) + c] = acc[t][e] + (r == c ? lambda : 0.0);
+      for (int J = 0; J <= I; ++J) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = J * 8 + 2 * kl + e;
+          if (r < m && c <= r) Mr[c] = acc[t + J][e] + (r == c ? lambda : 0.0);
+        }
       }
     }
+    t += I + 1;
+  }
   __syncwarp();
 }
 

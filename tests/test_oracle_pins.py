@@ -401,3 +401,73 @@ def test_mask_aggregation_ranking_rule():
     assert list(rows["n_correct"]) == [4, 7, 7, 1, 9]
     assert (rows["n_test"] == 12).all() and (rows["n_rec"] == 3).all()
     assert list(top) == [14, 11, 12]
+
+
+# ------------------------------------------------------------ IBK (NEXT-1)
+def _knn_brute(Xs, y, Xts, k):
+    """Independent brute force: exact rational distances, stable
+    sort by (distance, stored index), arithmetic mean of the k labels."""
+    out = []
+    for q in Xts:
+        D = [sum((Fraction(float(a)) - Fraction(float(b))) ** 2 for a, b in zip(q, row)) for row in Xs]
+        order = sorted(range(len(Xs)), key=lambda i: (D[i], i))[:min(k, len(Xs))]
+        out.append(float(sum(Fraction(float(y[i])) for i in order) / len(order)))
+    return np.array(out)
+
+
+def test_knn_spec_examples():
+    rng = np.random.default_rng(20)
+    X = rng.uniform(0, 1, (12, 5))
+    y = rng.uniform(0.5, 1.5, 12)
+    np.testing.assert_array_equal(oracle.knn_predict(X, y, X, k=1), y)           # S:210 identity, k=1
+    ex = oracle.knn_predict(X, y, rng.uniform(0, 1, (4, 5)), k=50)                # S:211 k >= n
+    np.testing.assert_allclose(ex, y.mean(), rtol=0, atol=1e-15)
+
+
+def test_knn_matches_bruteforce():
+    rng = np.random.default_rng(21)
+    for trial in range(120):
+        n, d = int(rng.integers(1, 51)), int(rng.integers(1, 9))
+        X = rng.uniform(0, 1, (n, d))
+        if trial % 4 == 0:
+            X[rng.integers(0, n, n // 2)] = X[0]                                   # duplicates -> ties
+        y = rng.uniform(0.5, 1.5, n)
+        Xt = rng.uniform(-0.2, 1.2, (3, d))
+        for k in (1, 3, 10):
+            np.testing.assert_allclose(oracle.knn_predict(X, y, Xt, k=k), _knn_brute(X, y, Xt, k),
+                                       rtol=0, atol=1e-9)
+
+
+def test_knn_permutation_and_shift_invariance():
+    rng = np.random.default_rng(22)
+    X = rng.uniform(0, 1, (30, 6))
+    y = rng.uniform(0.5, 1.5, 30)
+    Xt = rng.uniform(0, 1, (10, 6))
+    ex = oracle.knn_predict(X, y, Xt, k=10)
+    perm = rng.permutation(30)
+    np.testing.assert_allclose(oracle.knn_predict(X[perm], y[perm], Xt, k=10), ex, rtol=0, atol=1e-15)  # S:241
+    np.testing.assert_allclose(oracle.knn_predict(X, y + 0.25, Xt, k=10), ex + 0.25, rtol=0, atol=1e-14)  # S:246
+
+
+def test_knn_pipeline_exact_recall_exp1():
+    # SPEC acceptance #5 analogue (P:214 "IBK ... is therefore able to predict
+    # the speedup of the training data exactly"): Exp 1 tests the training run
+    # itself; with k = 1 every test case of the training group is its own
+    # nearest neighbour (distance 0), so EX == AC exactly there.
+    cfg = gen.make_config("C2")
+    sc = cfg.scenarios
+    r = oracle.evaluate(cfg.dataset, sc, 0, 24, want_ex=True, learner=1, k_nn=1)
+    ds = cfg.dataset
+    O, G = ds.n_opt_ids, ds.n_groups
+    V = 64
+    for s in range(24):                                   # Exp 1 instantiations
+        g_train = int(np.log2(int(sc.train_groups[s][0])))
+        p = g_train // (ds.n_inputs * ds.n_runs)
+        for o in range(O):
+            b = int(ds.opt_bit[p, o])
+            if b < 0:
+                continue
+            for k in range(32):
+                v = ((k >> b) << (b + 1)) | (k & ((1 << b) - 1))
+                ac = ds.runtime_ms[g_train * V + v] / ds.runtime_ms[g_train * V + (v | (1 << b))]
+                assert r["ex"][s, o, g_train * 32 + k] == ac
