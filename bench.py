@@ -103,10 +103,10 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def oracle_rate(cfg, first: int, count: int, threads: int):
+def oracle_rate(cfg, first: int, count: int, threads: int, learner: int = 0):
     import oracle
     t0 = time.perf_counter()
-    oracle.evaluate(cfg.dataset, cfg.scenarios, first, count, n_threads=threads)
+    oracle.evaluate(cfg.dataset, cfg.scenarios, first, count, n_threads=threads, learner=learner)
     return count / (time.perf_counter() - t0)
 
 
@@ -117,10 +117,10 @@ def run_reference(args, cfg, rank, world):
     threads = os.cpu_count() or 1
     sample = args.ref_sample
     for _ in range(args.warmup):
-        oracle_rate(cfg, 0, max(threads, sample // 10), threads)
+        oracle_rate(cfg, 0, max(threads, sample // 10), threads, LEARNERS[args.learner])
     rates = []
     for k in range(args.steps):
-        rates.append(oracle_rate(cfg, (k * sample) % cfg.scenarios.n_splits, sample, threads))
+        rates.append(oracle_rate(cfg, (k * sample) % cfg.scenarios.n_splits, sample, threads, LEARNERS[args.learner]))
     v = float(np.mean(rates))
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "scenario_evals/s", "n_gpus": args.gpus,
@@ -135,12 +135,23 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+LEARNERS = {"linreg": 0, "ibk": 1}
+
+
+def knn_flops(n: np.ndarray, t: np.ndarray, d: int) -> float:
+    """IBk (NEXT-1): per fit n*t*d distance terms, each a subtract and an FMA
+    (3 flop); the scaling divisions and the k-best inserts are not counted."""
+    n = n.astype(np.float64)
+    t = t.astype(np.float64)
+    return float(3.0 * np.where((n > 0) & (t > 0), n * t * d, 0.0).sum())
+
+
 METRIC = "train/test scenario evals/sec at 1/2/4/8 B200 (roofline frac) vs CPU oracle"
 
 
 def workload_config(cfg, args, per_gpu):
     ds = cfg.dataset
-    return {"workload": f"{cfg.name}: {cfg.description}", "splits_per_gpu": per_gpu,
+    return {"workload": f"{cfg.name}: {cfg.description}", "splits_per_gpu": per_gpu, "learner": args.learner,
             "programs": ds.n_programs, "variants": ds.n_slots, "counters": ds.n_counters,
             "optimizations": ds.n_opt_ids, "parallelism": f"scenario-sharded x{args.gpus}",
             "l2": "flushed between timed steps (256 MiB write); dataset 64 KiB is L2/smem resident by design"}
@@ -154,6 +165,8 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--splits", type=int, default=None, help="scenarios per GPU (default: config size)")
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
+    ap.add_argument("--learner", default="linreg", choices=list(LEARNERS),
+                    help="linreg = ridge LS (the paper's model); ibk = the NEXT-1 k-NN learner")
     ap.add_argument("--ref-sample", type=int, default=4000)
     ap.add_argument("--cpu-sample", type=int, default=4000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -201,9 +214,11 @@ def main():
                scn=torch.empty(count * SCN_SCORE_DTYPE.itemsize, dtype=torch.uint8, device=dev),
                totals=torch.zeros(4, dtype=torch.int64, device=dev))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    from paper_1910_07776_b200.speedrec import default_params
+    prm = default_params(learner=LEARNERS[args.learner])
 
     for _ in range(args.warmup):
-        ctx.evaluate(first, count, out=out)
+        ctx.evaluate(first, count, params=prm, out=out)
     torch.cuda.synchronize()
 
     # ---------------- timed region: K steps, device events, L2 flushed between steps
@@ -217,7 +232,7 @@ def main():
         for k in range(args.steps):
             flush.fill_(float(k))
             evs[k][0].record(stream)
-            ctx.evaluate(first, count, out=out)
+            ctx.evaluate(first, count, params=prm, out=out)
             evs[k][1].record(stream)
         torch.cuda.synchronize()
     if dist:
@@ -236,8 +251,12 @@ def main():
     big = ds.n_groups > 64          # CTA-per-fit path (C4): prediction runs in k_rank_big
     n_tr, n_te = opt["n_train"].ravel(), opt["n_test"].ravel()
     name_dom = "k_fit_big" if big else "k_fit_warp"
-    flops_launch = fit_flops(n_tr, np.where(big, 0, n_te), ds.n_counters,
-                             refine=2) if not big else fit_flops_big(n_tr, n_te, ds.n_counters)
+    if args.learner == "ibk":
+        flops_launch = knn_flops(n_tr, n_te, ds.n_counters)
+    elif big:
+        flops_launch = fit_flops_big(n_tr, n_te, ds.n_counters)
+    else:
+        flops_launch = fit_flops(n_tr, n_te, ds.n_counters, refine=2)
     n_dom, ms_dom = stats.get(name_dom, (0, 0.0))
     avg_dom = ms_dom / max(n_dom, 1)                 # average launch duration (CUDA events, live)
     launches_per_step = max(n_dom // max(args.steps, 1), 1)
@@ -260,10 +279,9 @@ def main():
         hopt = torch.empty(count * O * OPT_SCORE_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
         hscn = torch.empty(count * SCN_SCORE_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
         htot = torch.zeros(4, dtype=torch.int64).pin_memory()
-        from paper_1910_07776_b200.speedrec import sr_outputs, lib, default_params
+        from paper_1910_07776_b200.speedrec import sr_outputs, lib
         import ctypes as ct
         hout = sr_outputs(hopt.data_ptr(), hscn.data_ptr(), None, None, htot.data_ptr(), 0)
-        prm = default_params()
         e2e_ms = []
         for k in range(max(2, min(args.steps, 5)) + 1):
             flush.fill_(float(k))
@@ -287,7 +305,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        v = oracle_rate(cfg, 0, args.cpu_sample, threads)
+        v = oracle_rate(cfg, 0, args.cpu_sample, threads, LEARNERS[args.learner])
         cpu = {"value": v, "unit": "scenario_evals/s", "cores": threads, "kind": "oracle",
                "sample": f"first {args.cpu_sample} scenarios of {args.config} (same splits the GPU evaluates)"}
 

@@ -138,7 +138,8 @@ sr_status sr_define_scenarios(sr_ctx* ctx, const sr_scenarios* sc, int64_t* n_sc
 typedef enum { SR_LINREG = 0, SR_IBK = 1 } sr_learner;
 
 typedef struct {
-  int32_t learner;       /* SR_LINREG (ridge LS, reading D1); SR_IBK -> SR_E_UNSUPPORTED (NEXT-1) */
+  int32_t learner;       /* SR_LINREG (ridge LS, reading D1) or SR_IBK (k-nearest neighbours,
+                            P:147-149, reading R22; <= 64 groups only, else SR_E_UNSUPPORTED) */
   int32_t max_count;     /* Tier-3 max recommendations, 3 */
   int32_t refine_steps;  /* iterative-refinement steps of the solve, 2 */
   int32_t debug_mcap;    /* 0 = auto; >0 caps the shared-memory Cholesky size so larger
@@ -148,7 +149,7 @@ typedef struct {
   double clamp_floor;    /* EX <= 0 -> clamp_floor, 0.01 */
   double guard_tol;      /* guard band for n_guard, 1e-9 (reading R21) */
   int32_t top_k;         /* masks kept by the mask ranking, 64, <= 512 */
-  int32_t pad_;
+  int32_t k_nn;          /* IBK neighbours k, 10 (P:149 IBk default reading R22), 1..16 */
 } sr_params;
 
 void sr_default_params(sr_params* out);

@@ -179,8 +179,88 @@ __device__ __noinline__ bool fit_generic(const FitView& f, const double* yc, dou
   return true;
 }
 
+// ------------------------------------------------------------- IBK (NEXT-1)
+// EX of one test case under IBk (reading R22): the mean training
+// label of the min(k, n) training befores nearest in min-max scaled counter
+// space, x' = (x - mn) / rg over the active features (D3), squared Euclidean
+// distance accumulated with fma in active-feature order, neighbours ordered by
+// (distance, training index), labels summed in that order and divided by k'.
+// Every operation is the definition's, in its order, so EX is bit-exact.
+// Warp-collective: each sweep stages kKnnRows scaled training rows in S
+// (shared) and every lane scans them against its own test row xq (null for an
+// idle lane).  The lane's k-best list lives in registers (kKnnMax slots,
+// sorted; a new candidate has the largest index so far, so strict > keeps
+// (distance, index) order).
+__device__ __forceinline__ double knn_ex(const double* __restrict__ X, int ldx, const int32_t* trs,
+                                         const double* y, int n, const int16_t* col, const double* mnv,
+                                         const double* rgv, int deff, int kk, const double* xq,
+                                         double* S, int lane) {
+  double bd[kKnnMax];
+  int bi[kKnnMax];
+#pragma unroll
+  for (int q = 0; q < kKnnMax; ++q) {
+    bd[q] = INFINITY;
+    bi[q] = 0;
+  }
+  double thr = INFINITY;  // distance of the current kk-th neighbour
+  #pragma unroll 1
+  for (int i0 = 0; i0 < n; i0 += kKnnRows) {
+    const int rows = min(kKnnRows, n - i0);
+    __syncwarp();
+    for (int e = lane; e < rows * deff; e += 32) {
+      const int r = e / deff, a = e - r * deff;
+      S[r * deff + a] = (X[(long long)trs[i0 + r] * ldx + col[a]] - mnv[a]) / rgv[a];
+    }
+    __syncwarp();
+    if (xq) {
+      double acc[kKnnRows];
+#pragma unroll
+      for (int r = 0; r < kKnnRows; ++r) acc[r] = 0.0;
+      #pragma unroll 1
+      for (int a = 0; a < deff; ++a) {
+        const double v = (xq[col[a]] - mnv[a]) / rgv[a];
+#pragma unroll
+        for (int r = 0; r < kKnnRows; ++r) {   // rows >= `rows` read stale values, dropped below
+          const double dl = v - S[r * deff + a];
+          acc[r] = fma(dl, dl, acc[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kKnnRows; ++r) {
+        const double D = acc[r];
+        if (r < rows && D < thr) {
+          const int id = i0 + r;
+#pragma unroll
+          for (int q = kKnnMax - 1; q > 0; --q) {
+            const bool sh = bd[q - 1] > D, put = !sh && bd[q] > D;
+            if (sh) {
+              bd[q] = bd[q - 1];
+              bi[q] = bi[q - 1];
+            } else if (put) {
+              bd[q] = D;
+              bi[q] = id;
+            }
+          }
+          if (bd[0] > D) {
+            bd[0] = D;
+            bi[0] = id;
+          }
+#pragma unroll
+          for (int q = 0; q < kKnnMax; ++q)
+            if (q == kk - 1) thr = bd[q];
+        }
+      }
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < kKnnMax; ++q)
+    if (q < kk) s += y[bi[q]];
+  return s / (double)kk;
+}
+
 // ---------------------------------------------------------------- fit kernel
-template <int WMAX>
+template <int WMAX, bool IBK>   // IBK: the NEXT-1 learner instead of ridge LS (separate code)
 __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const WarpLayout& L = A.L;
@@ -299,6 +379,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
     }
 
     // ---- A2: per-fit min-max statistics over the training befores (D3) ----
+    constexpr bool ibk = IBK;
     int deff = 0;
     for (int a0 = 0; a0 < d; a0 += 64) {       // two features per lane per row pass
       const int a1 = a0 + lane, a2 = a0 + 32 + lane;
@@ -327,6 +408,10 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
           col[p] = (int16_t)(h ? c2 : c1);
           xb[p] = sm / (double)n;
           sv[p] = 1.0 / (mx - mn);
+          if (ibk) {
+            uv[p] = mn;
+            wv[p] = mx - mn;
+          }
         }
         deff += __popc(bm);
       }
@@ -339,59 +424,48 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
         sv[p] = 0.0;
       }
     }
-    double ysum = 0.0;
-    #pragma unroll 1
-    for (int i = lane; i < n; i += 32) ysum += yc[i];
-    const double ybar = warp_sum(ysum) / (double)n;
-    for (int i = lane; i < n; i += 32) yc[i] -= ybar;
-    __syncwarp();
-
-    // ---- A3/A4: centred normal equations, dual or primal ----
-    const bool dual = (n - 1) < deff;
-    const int m = dual ? n : deff;
-    // refine where conditioning or the O(n eps) Gram accumulation error needs it
-    const int nref = (dual ? 2 * (n - 1) >= deff : ((n - 1) < 2 * deff || n > 64)) ? A.refine : 0;
+    double c0 = 0.0;
     bool ok = true;
-    if (m > 0 && m <= (L.mcap < 32 ? L.mcap : 32)) {
-      const FastView fv{X, ldx, trs, n, col, xb, sv, deff};
-      ok = dual ? fit_fast<true>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane)
-                : fit_fast<false>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane);
-    } else if (m > 0) {
-      const FitView fv{X, ldx, trs, n, col, xb, sv, deff};
-      ok = fit_generic(fv, yc, A.lambda, nref, dual, scr, L.vmax, uv, v2, wv, lane);
-    }
-    // weights on raw counters: EX = c0 + sum_c x_c * ufull[c]
-    for (int c = lane; c < C; c += 32) ufull[c] = 0.0;
-    __syncwarp();
-    double cpart = 0.0;
-    if (m > 0 && ok)
-      for (int a = lane; a < deff; a += 32) {
-        const double u = wv[a] * sv[a];
-        ufull[col[a]] = u;
-        cpart = fma(xb[a], u, cpart);
+    if (!ibk) {
+      double ysum = 0.0;
+      #pragma unroll 1
+      for (int i = lane; i < n; i += 32) ysum += yc[i];
+      const double ybar = warp_sum(ysum) / (double)n;
+      for (int i = lane; i < n; i += 32) yc[i] -= ybar;
+      __syncwarp();
+
+      // ---- A3/A4: centred normal equations, dual or primal ----
+      const bool dual = (n - 1) < deff;
+      const int m = dual ? n : deff;
+      // refine where conditioning or the O(n eps) Gram accumulation error needs it
+      const int nref = (dual ? 2 * (n - 1) >= deff : ((n - 1) < 2 * deff || n > 64)) ? A.refine : 0;
+      if (m > 0 && m <= (L.mcap < 32 ? L.mcap : 32)) {
+        const FastView fv{X, ldx, trs, n, col, xb, sv, deff};
+        ok = dual ? fit_fast<true>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane)
+                  : fit_fast<false>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane);
+      } else if (m > 0) {
+        const FitView fv{X, ldx, trs, n, col, xb, sv, deff};
+        ok = fit_generic(fv, yc, A.lambda, nref, dual, scr, L.vmax, uv, v2, wv, lane);
       }
-    const double c0 = ybar - warp_sum(cpart);
-    __syncwarp();
+      // weights on raw counters: EX = c0 + sum_c x_c * ufull[c]
+      for (int c = lane; c < C; c += 32) ufull[c] = 0.0;
+      __syncwarp();
+      double cpart = 0.0;
+      if (m > 0 && ok)
+        for (int a = lane; a < deff; a += 32) {
+          const double u = wv[a] * sv[a];
+          ufull[col[a]] = u;
+          cpart = fma(xb[a], u, cpart);
+        }
+      c0 = ybar - warp_sum(cpart);
+      __syncwarp();
+    }
 
     // ---- A5: predict + clamp; A7 per-(s,o) scores ----
     double* ext = A.extab + sl * A.ex_stride + q * A.tg_stride;
     int ncorr = 0, ncl = 0, guard = ok ? 0 : 1000000;
     double rsum = 0.0, rmin = INFINITY, rmax = -INFINITY;
-    for (int j = lane; j < nt; j += 32) {
-      const double* xr = X + (long long)tes[j] * ldx;
-      double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;   // 4 independent chains
-      int c = 0;
-      #pragma unroll 1
-      for (; c + 3 < C; c += 4) {
-        const double2 u01 = *reinterpret_cast<const double2*>(ufull + c);
-        const double2 u23 = *reinterpret_cast<const double2*>(ufull + c + 2);
-        e0 = fma(xr[c], u01.x, e0);
-        e1 = fma(xr[c + 1], u01.y, e1);
-        e2 = fma(xr[c + 2], u23.x, e2);
-        e3 = fma(xr[c + 3], u23.y, e3);
-      }
-      for (; c < C; ++c) e0 = fma(xr[c], ufull[c], e0);
-      double e = c0 + ((e0 + e1) + (e2 + e3));
+    auto score = [&](const int j, double e) {
       if (near_tol(e, 0.0, A.guard_tol) || near_tol(e, 1.0, A.guard_tol)) ++guard;
       bool cl = false;
       if (e <= 0.0) {
@@ -408,6 +482,34 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
       rmax = fmax(rmax, ratio);
       ext[test_group_index(A.sd, split, gk >> 5) * 32 + (gk & 31)] = cl ? -e : e;
       if (A.ex_out) A.ex_out[(so * O + o) * (long long)G * 32 + gk] = e;
+    };
+    if (ibk) {   // NEXT-1: IBk prediction, all lanes sweep together (knn_ex)
+      const int kk = min(A.k_nn, n);
+      #pragma unroll 1
+      for (int j0 = 0; j0 < nt; j0 += 32) {
+        const int j = j0 + lane;
+        const double* xq = j < nt ? X + (long long)tes[j] * ldx : nullptr;
+        const double e = knn_ex(X, ldx, trs, yc, n, col, uv, wv, deff, kk, xq, Msm, lane);
+        if (j < nt) score(j, e);
+      }
+    } else {
+      for (int j = lane; j < nt; j += 32) {
+        const double* xr = X + (long long)tes[j] * ldx;
+        double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;   // 4 independent chains
+        int c = 0;
+        #pragma unroll 1
+        for (; c + 3 < C; c += 4) {
+          const double2 u01 = *reinterpret_cast<const double2*>(ufull + c);
+          const double2 u23 = *reinterpret_cast<const double2*>(ufull + c + 2);
+          e0 = fma(xr[c], u01.x, e0);
+          e1 = fma(xr[c + 1], u01.y, e1);
+          e2 = fma(xr[c + 2], u23.x, e2);
+          e3 = fma(xr[c + 3], u23.y, e3);
+        }
+        for (; c < C; ++c) e0 = fma(xr[c], ufull[c], e0);
+        double e = c0 + ((e0 + e1) + (e2 + e3));
+        score(j, e);
+      }
     }
     row.n_correct = warp_isum(ncorr);
     row.n_clamped = warp_isum(ncl);

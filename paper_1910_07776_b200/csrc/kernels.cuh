@@ -27,6 +27,8 @@ constexpr int kMaxGroups = 64;       // warp-per-scenario path
 constexpr int kMaxGroupsBig = 4096;  // CTA-per-fit path (config C4)
 constexpr int kMaxCounters = 128;
 constexpr int kMaxRec = 8;
+constexpr int kKnnMax = 16;            // largest IBK k (sr_params.k_nn)
+constexpr int kKnnRows = 8;            // training rows staged per IBK distance sweep
 constexpr int kMaxWarpsPerBlock = 16;  // default warps/CTA of k_fit_warp (tools/tune_launch.sh)
 
 struct OptScore {
@@ -91,6 +93,7 @@ struct EvalArgs {
   // params
   double lambda, threshold, clamp_floor, guard_tol;
   int max_count, refine;
+  int learner, k_nn;    // SR_LINREG / SR_IBK and the IBK k
   // scenario range of this launch (a chunk of the sr_evaluate range)
   long long first, count;
   long long out0;        // index of `first` inside the caller's output arrays

@@ -261,7 +261,7 @@ void sr_default_params(sr_params* p) {
   p->clamp_floor = 0.01;
   p->guard_tol = 1e-9;
   p->top_k = 64;
-  p->pad_ = 0;
+  p->k_nn = 10;
 }
 
 sr_status sr_load_dataset(sr_ctx* c, const sr_dataset* d) {
@@ -437,7 +437,7 @@ sr_status sr_define_scenarios(sr_ctx* c, const sr_scenarios* s, int64_t* n_scena
 namespace {
 
 // Shared-memory plan of k_eval_warp for the current batch.
-WarpLayout plan_layout(const sr_ctx* c, int mcap) {
+WarpLayout plan_layout(const sr_ctx* c, int mcap, bool ibk) {
   WarpLayout L{};
   int off = 0;
   auto take = [&](int bytes) {
@@ -464,7 +464,8 @@ WarpLayout plan_layout(const sr_ctx* c, int mcap) {
   L.vmax = vmax;
   L.off_v2 = take(8 * vmax);
   L.mcap = mcap;
-  L.off_M = take(8 * std::max(rb2(mcap), mcap * (mcap + 1) / 2));
+  // Cholesky factor, or for IBK the kKnnRows scaled training rows being scanned
+  L.off_M = take(8 * std::max({rb2(mcap), mcap * (mcap + 1) / 2, ibk ? kKnnRows * d : 0}));
   L.off_ufull = take(8 * c->C);
   L.bytes = align16(off);
   return L;
@@ -591,7 +592,10 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     return fail(c, SR_E_ARG, "evaluate: mask aggregation needs first/count multiples of n_splits=%lld",
                 (long long)c->sc.n_splits);
   if (agg && (prm->top_k < 1 || prm->top_k > 512)) return fail(c, SR_E_ARG, "evaluate: top_k=%d", prm->top_k);
-  if (prm->learner != SR_LINREG) return fail(c, SR_E_UNSUPPORTED, "evaluate: learner %d (IBK is NEXT-1)", prm->learner);
+  if (prm->learner != SR_LINREG && prm->learner != SR_IBK)
+    return fail(c, SR_E_ARG, "evaluate: learner %d", prm->learner);
+  if (prm->learner == SR_IBK && (prm->k_nn < 1 || prm->k_nn > kKnnMax))
+    return fail(c, SR_E_ARG, "evaluate: k_nn=%d outside [1, %d]", prm->k_nn, kKnnMax);
   if (prm->max_count < 1 || prm->max_count > kMaxRec) return fail(c, SR_E_ARG, "evaluate: max_count=%d", prm->max_count);
   if (prm->refine_steps < 0 || prm->refine_steps > 8) return fail(c, SR_E_ARG, "evaluate: refine_steps=%d", prm->refine_steps);
   if (!(prm->ridge > 0.0)) return fail(c, SR_E_ARG, "evaluate: ridge must be > 0");
@@ -617,6 +621,7 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   if (count == 0) return SR_OK;
   if (G > kMaxGroups) {
     if (agg) return fail(c, SR_E_UNSUPPORTED, "evaluate: mask aggregation needs <= %d groups", kMaxGroups);
+    if (prm->learner == SR_IBK) return fail(c, SR_E_UNSUPPORTED, "evaluate: IBK needs <= %d groups", kMaxGroups);
     return evaluate_big(c, prm, first, count, out);
   }
 
@@ -633,11 +638,12 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   if (const char* e = getenv("SPEEDREC_STAGE")) stage = atoi(e) && stage_bytes <= 96 * 1024;
   int wmax = kMaxWarpsPerBlock;
   if (const char* e = getenv("SPEEDREC_WMAX")) wmax = atoi(e) >= 24 ? 24 : atoi(e) >= 16 ? 16 : 12;
+  if (prm->learner == SR_IBK) wmax = 16;   // the one IBK instantiation
   int budget_cap = budget;
   if (const char* e = getenv("SPEEDREC_SMEM_KB")) budget_cap = std::min(budget, std::max(16, atoi(e)) * 1024);
   int mcap = std::min(mmax, 32);
   if (prm->debug_mcap > 0) mcap = std::min(mcap, prm->debug_mcap);
-  WarpLayout L = plan_layout(c, mcap);
+  WarpLayout L = plan_layout(c, mcap, prm->learner == SR_IBK);
   int avail = budget_cap - head - (stage ? align16((int)stage_bytes) : 0);
   int wpb = std::min(wmax, avail / std::max(L.bytes, 1));
   if (wpb < 1 && stage) {
@@ -665,6 +671,8 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.guard_tol = prm->guard_tol;
   A.max_count = prm->max_count;
   A.refine = prm->refine_steps;
+  A.learner = prm->learner;
+  A.k_nn = prm->k_nn;
   A.L = L;
   A.warps_per_block = wpb;
   A.stage_x = stage;
@@ -672,7 +680,8 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.off_stage = head;
   A.off_warps = head + (stage ? align16((int)stage_bytes) : 0);
   const int smem = A.off_warps + wpb * L.bytes;
-  auto kfit = wmax == 24 ? k_fit_warp<24> : wmax == 16 ? k_fit_warp<16> : k_fit_warp<12>;
+  auto kfit = prm->learner == SR_IBK ? k_fit_warp<16, true>
+              : wmax == 24 ? k_fit_warp<24, false> : wmax == 16 ? k_fit_warp<16, false> : k_fit_warp<12, false>;
   CU(cudaFuncSetAttribute(kfit, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfit, wpb * 32, smem));

@@ -55,7 +55,7 @@ class sr_params(ct.Structure):
     _fields_ = [("learner", ct.c_int32), ("max_count", ct.c_int32), ("refine_steps", ct.c_int32),
                 ("debug_mcap", ct.c_int32), ("ridge", ct.c_double), ("threshold", ct.c_double),
                 ("clamp_floor", ct.c_double), ("guard_tol", ct.c_double), ("top_k", ct.c_int32),
-                ("pad_", ct.c_int32)]
+                ("k_nn", ct.c_int32)]
 
 
 class sr_outputs(ct.Structure):

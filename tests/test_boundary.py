@@ -51,6 +51,7 @@ def test_default_params_and_version(libpath):
     from paper_1910_07776_b200 import speedrec
     p = speedrec.default_params()
     assert (p.max_count, p.refine_steps, p.ridge, p.threshold, p.clamp_floor) == (3, 2, 1e-8, 1.05, 0.01)
+    assert (p.learner, p.k_nn, p.top_k) == (0, 10, 64)
     assert speedrec.lib().sr_version().startswith(b"speedrec")
 
 

@@ -1,0 +1,101 @@
+"""GPU parity of the NEXT-1 learner (IBk, reading R22) vs the oracle.
+
+IBk's EX is the mean of k training labels picked by distances computed with
+the same operations in the same order on both sides (oracle or_knn_predict,
+kernel knn_ex), so the bar is BIT-EXACT: every EX, every integer field and
+every recommendation identical, no guard exemption.  Only the FP64 ratio
+sums (a quad sum in the oracle, a warp tree on the GPU) keep the 1e-9
+relative bar.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from tests.parity import compare
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(cfg, first, count, k=10):
+    from paper_1910_07776_b200 import Context, default_params
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    got = ctx.evaluate(first, count, params=default_params(learner=1, k_nn=k), want_ex=True, want_recs=True)
+    ctx.close()
+    ref = oracle.evaluate(cfg.dataset, cfg.scenarios, first, count, want_ex=True, want_recs=True,
+                          learner=1, k_nn=k)
+    return got, ref
+
+
+def _exact(got, ref):
+    assert np.array_equal(got["ex"], ref["ex"], equal_nan=True), "IBK EX not bit-exact"
+    go, ro, gs, rs = got["opt"], ref["opt"], got["scn"], ref["scn"]
+    for f in ("n_train", "n_test", "n_correct", "n_clamped", "fp_train", "fp_test", "min_ratio", "max_ratio"):
+        assert np.array_equal(go[f], ro[f]), f
+    for f in ("n_rec", "n_rec_hit", "n_untrained", "n_guard"):
+        assert np.array_equal(gs[f], rs[f]), f
+    assert np.array_equal(got["recs"], ref["recs"])
+    return compare(got, ref, max_guard_frac=1.0)
+
+
+@pytest.mark.parametrize("k", [1, 3, 10, 16])
+def test_ibk_c1_all_k(k):
+    cfg = gen.make_config("C1")
+    got, ref = _run(cfg, 0, 64, k)
+    print("IBK C1 k", k, _exact(got, ref))
+
+
+def test_ibk_c2_table2():
+    cfg = gen.make_config("C2")
+    got, ref = _run(cfg, 0, 240)
+    print("IBK C2", _exact(got, ref))
+
+
+def test_ibk_c3_ragged():
+    cfg = gen.make_config("C3", n_splits=2001)
+    got, ref = _run(cfg, 0, 2001)
+    print("IBK C3", _exact(got, ref))
+    got, ref = _run(cfg, 999, 77)
+    _exact(got, ref)
+
+
+def test_ibk_c5_masks():
+    cfg = gen.make_config("C5", n_masks_k=5)
+    n = cfg.scenarios.n_scenarios
+    got, ref = _run(cfg, 0, n)
+    print("IBK C5k5", _exact(got, ref))
+
+
+def test_ibk_degenerate():
+    # constant / zero features (d_eff = 0: every distance 0 -> the first k
+    # training pairs by index) and feature masks selecting nothing
+    cfg = gen.make_config("C1")
+    ds = cfg.dataset
+    ds.counters[:, :8] = ds.cycles[:, None] * 0.25
+    ds.counters[:, 8:16] = 0.0
+    cfg.scenarios.feature_masks = np.array([[0, 0], [1 << 20, 0], [0xFFFF0000, 0], [~0 & 0xFFFFFFFF, 0]],
+                                           dtype=np.uint64)
+    cfg.scenarios.n_masks = 4
+    got, ref = _run(cfg, 0, 64 * 4)
+    _exact(got, ref)
+
+
+def test_ibk_rejects_bad_k_and_big_path():
+    from paper_1910_07776_b200 import Context, SpeedrecError, default_params
+    cfg = gen.make_config("C1")
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    for k in (0, 17):
+        with pytest.raises(SpeedrecError, match="k_nn"):
+            ctx.evaluate(0, 1, params=default_params(learner=1, k_nn=k))
+    ctx.close()
+    cfg = gen.make_config("C4", n_splits=2, n_programs=96)
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    with pytest.raises(SpeedrecError, match="IBK"):
+        ctx.evaluate(0, 1, params=default_params(learner=1))
+    ctx.close()
