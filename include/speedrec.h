@@ -205,6 +205,39 @@ typedef struct {
 sr_status sr_evaluate(sr_ctx* ctx, const sr_params* params, int64_t first, int64_t count,
                       sr_outputs* out);
 
+/* ---------------------------------------------------------------------- */
+/* Tool path: one scenario, one user profile (SPEC train_all S:282,        */
+/* predict_all S:291, rank_and_filter S:300; P:60-62 Tiers 2 and 3).        */
+/* ---------------------------------------------------------------------- */
+
+/* Fit the ridge model of every optimization id of one scenario (A1-A4, the
+ * same kernels as sr_evaluate) and return it in raw-counter form:
+ *   coef_out host [O][1 + C]: row o = (c0, u_0 .. u_{C-1}) with
+ *   EX = c0 + sum_c u_c * x_c,  x_c = counters_c / cycles,
+ * i.e. the scaled-feature model b + w.x' of reading D1/D3 with the scaling
+ * folded in (u_c = w_c / rg_c for active c, 0 otherwise).  Rows of ids not
+ * scored in the scenario, or untrained (n = 0, reading R18): c0 = NaN, u = 0.
+ * Caller owns coef_out.  Errors: SR_E_ARG, SR_E_STATE, SR_E_UNSUPPORTED
+ * (learner IBK: the model is its training set), and sr_evaluate's. */
+sr_status sr_fit(sr_ctx* ctx, const sr_params* params, int64_t scenario, double* coef_out);
+
+/* Tier 2 for one user profile (host, no context; O(O*C) work):
+ *   ex_out[o] = c0 + sum_c u_c * (counters[c] / cycles), clamped to
+ *   params->clamp_floor when <= 0; NaN for rows with c0 = NaN.
+ * coef [n_opts][1 + n_counters] as written by sr_fit.  Borrowed pointers.
+ * Errors: SR_E_ARG (null/size), SR_E_DATA (cycles <= 0, counter < 0 or
+ * non-finite). */
+sr_status sr_predict(const sr_params* params, const double* coef, int32_t n_opts, int32_t n_counters,
+                     const double* counters, double cycles, double* ex_out);
+
+/* Tier 3: candidates are ids with candidate[o] != 0 (all
+ * when candidate is NULL) and a non-NaN EX >= params->threshold (R8); sorted
+ * by (EX desc, id asc) (R10); the first params->max_count (1..64) go to
+ * rec_out [max_count], -1 padded; *n_rec_out = their number.  An empty list is valid
+ * (S:304).  Errors: SR_E_ARG. */
+sr_status sr_recommend(const sr_params* params, const double* ex, const uint8_t* candidate, int32_t n_opts,
+                       int8_t* rec_out, int32_t* n_rec_out);
+
 /* A0 alone: rates x[N][C] (bit-exact IEEE FP64 division) into x_out
  * (host if on_device == 0).  For parity tests of Tier 1. */
 sr_status sr_rates(sr_ctx* ctx, double* x_out, int32_t on_device);

@@ -260,7 +260,9 @@ __device__ __forceinline__ double knn_ex(const double* __restrict__ X, int ldx, 
 }
 
 // ---------------------------------------------------------------- fit kernel
-template <int WMAX, bool IBK>   // IBK: the NEXT-1 learner instead of ridge LS (separate code)
+// MODE 0: ridge LS (the paper's model); 1: IBK (NEXT-1); 2: ridge LS + the
+// sr_fit coefficient store.  Separate instantiations keep the hot code lean.
+template <int WMAX, int MODE>
 __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const WarpLayout& L = A.L;
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
     }
 
     // ---- A2: per-fit min-max statistics over the training befores (D3) ----
-    constexpr bool ibk = IBK;
+    constexpr bool ibk = MODE == 1;
     int deff = 0;
     for (int a0 = 0; a0 < d; a0 += 64) {       // two features per lane per row pass
       const int a1 = a0 + lane, a2 = a0 + 32 + lane;
@@ -459,6 +461,11 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
         }
       c0 = ybar - warp_sum(cpart);
       __syncwarp();
+      if (MODE == 2) {   // sr_fit: the model in raw-counter form, EX = c0 + sum_c u_c x_c
+        double* cf = A.coef_out + (sl * O + o) * (long long)(C + 1);
+        for (int c = lane; c < C; c += 32) cf[1 + c] = ufull[c];
+        if (lane == 0) cf[0] = c0;
+      }
     }
 
     // ---- A5: predict + clamp; A7 per-(s,o) scores ----

@@ -108,6 +108,7 @@ struct EvalArgs {
   double* ex_out;        // [.][O][G*32] or null (pre-zeroed)
   int8_t* rec_out;       // [.][N][max_count] or null (pre-filled with -1)
   unsigned long long* totals;  // [4] or null
+  double* coef_out;            // sr_fit: [count][O][1 + C] raw-counter weights (c0, u), or null
   // mask aggregation (C5)
   int agg;
   int* mask_acc;         // [masks of the evaluate range][4], atomically accumulated

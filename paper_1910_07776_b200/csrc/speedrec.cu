@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -65,6 +66,8 @@ struct sr_ctx {
   // scratch + outputs
   DevBuf gscratch, out_opt, out_scn, out_ex, out_rec, out_tot, out_mask, out_top, keys_a, keys_b;
   DevBuf big_lists, big_y, big_U, big_c0, big_flag;  // large-batch path (> 64 groups)
+  DevBuf fit_coef;              // sr_fit: [O][1 + C]
+  double* coef_req = nullptr;   // set by sr_fit for the duration of its evaluate
   DevBuf extab, trained, guard_acc, mask_acc;         // fit -> rank exchange (warp path)
   // accounting
   bool timing = false;
@@ -638,7 +641,7 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   if (const char* e = getenv("SPEEDREC_STAGE")) stage = atoi(e) && stage_bytes <= 96 * 1024;
   int wmax = kMaxWarpsPerBlock;
   if (const char* e = getenv("SPEEDREC_WMAX")) wmax = atoi(e) >= 24 ? 24 : atoi(e) >= 16 ? 16 : 12;
-  if (prm->learner == SR_IBK) wmax = 16;   // the one IBK instantiation
+  if (prm->learner == SR_IBK || c->coef_req) wmax = 16;   // the one IBK / sr_fit instantiation
   int budget_cap = budget;
   if (const char* e = getenv("SPEEDREC_SMEM_KB")) budget_cap = std::min(budget, std::max(16, atoi(e)) * 1024);
   int mcap = std::min(mmax, 32);
@@ -680,8 +683,11 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.off_stage = head;
   A.off_warps = head + (stage ? align16((int)stage_bytes) : 0);
   const int smem = A.off_warps + wpb * L.bytes;
-  auto kfit = prm->learner == SR_IBK ? k_fit_warp<16, true>
-              : wmax == 24 ? k_fit_warp<24, false> : wmax == 16 ? k_fit_warp<16, false> : k_fit_warp<12, false>;
+  auto kfit = prm->learner == SR_IBK ? k_fit_warp<16, 1>
+              : c->coef_req      ? k_fit_warp<16, 2>
+              : wmax == 24       ? k_fit_warp<24, 0>
+              : wmax == 16       ? k_fit_warp<16, 0>
+                                 : k_fit_warp<12, 0>;
   CU(cudaFuncSetAttribute(kfit, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfit, wpb * 32, smem));
@@ -699,6 +705,7 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.tg_stride = tg_stride;
   A.trained = (uint32_t*)c->trained.p;
   A.guard_acc = (int*)c->guard_acc.p;
+  A.coef_out = c->coef_req;
   const long long max_fit_blocks = (long long)c->sm_count * per_sm;
   if (mscr > 0) {
     if ((st = ensure(c, c->gscratch, (size_t)(max_fit_blocks * wpb * mscr * 8)))) return st;
@@ -839,6 +846,83 @@ sr_status sr_rates(sr_ctx* c, double* x_out, int32_t on_device) {
   CU(cudaMemcpyAsync(x_out, c->x.p, N * C * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                      c->stream));
   CU(cudaStreamSynchronize(c->stream));
+  return SR_OK;
+}
+
+// ---------------------------------------------------------------- tool path
+// SPEC train_all / predict_all / rank_and_filter for
+// one scenario and one user profile (include/speedrec.h).
+sr_status sr_fit(sr_ctx* c, const sr_params* prm, int64_t scenario, double* coef_out) {
+  if (!c) return SR_E_ARG;
+  c->err.clear();
+  if (!prm || !coef_out) return fail(c, SR_E_ARG, "fit: null params or output");
+  if (prm->learner != SR_LINREG)
+    return fail(c, SR_E_UNSUPPORTED, "fit: learner %d has no coefficients (IBK keeps its training set)", prm->learner);
+  if (!c->have_ds) return fail(c, SR_E_STATE, "fit: no dataset loaded");
+  if (!c->have_sc) return fail(c, SR_E_STATE, "fit: no scenarios defined");
+  const int O = c->O, C = c->C;
+  const size_t bytes = (size_t)O * (C + 1) * 8;
+  sr_status st;
+  if ((st = ensure(c, c->fit_coef, bytes))) return st;
+  cudaSetDevice(c->device);
+  CU(cudaMemsetAsync(c->fit_coef.p, 0, bytes, c->stream));
+  std::vector<sr_opt_score> opt(O);
+  sr_scn_score scn;
+  sr_outputs o{};
+  o.opt_scores = opt.data();
+  o.scn_scores = &scn;
+  c->coef_req = (double*)c->fit_coef.p;
+  st = sr_evaluate(c, prm, scenario, 1, &o);
+  c->coef_req = nullptr;
+  if (st) return st;
+  if (c->G > kMaxGroups) {  // large-batch path: the batch-0 weight table holds the fit
+    CU(cudaMemcpy2DAsync((double*)c->fit_coef.p + 1, (C + 1) * 8, c->big_U.p, C * 8, C * 8, O,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemcpy2DAsync(c->fit_coef.p, (C + 1) * 8, c->big_c0.p, 8, 8, O, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  CU(cudaMemcpyAsync(coef_out, c->fit_coef.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (int q = 0; q < O; ++q)
+    if (opt[q].n_train == 0) {  // not scored or untrained (R18): no model
+      coef_out[(size_t)q * (C + 1)] = NAN;
+      for (int k = 0; k < C; ++k) coef_out[(size_t)q * (C + 1) + 1 + k] = 0.0;
+    }
+  return SR_OK;
+}
+
+sr_status sr_predict(const sr_params* prm, const double* coef, int32_t n_opts, int32_t n_counters,
+                     const double* counters, double cycles, double* ex_out) {
+  if (!prm || !coef || !counters || !ex_out || n_opts < 1 || n_opts > 16 || n_counters < 1 || n_counters > 128)
+    return SR_E_ARG;
+  if (!(cycles > 0.0) || !std::isfinite(cycles)) return SR_E_DATA;
+  for (int k = 0; k < n_counters; ++k)
+    if (!(counters[k] >= 0.0) || !std::isfinite(counters[k])) return SR_E_DATA;
+  for (int q = 0; q < n_opts; ++q) {
+    const double* cf = coef + (size_t)q * (n_counters + 1);
+    if (std::isnan(cf[0])) {
+      ex_out[q] = NAN;
+      continue;
+    }
+    double e = 0.0;
+    for (int k = 0; k < n_counters; ++k) e = std::fma(counters[k] / cycles, cf[1 + k], e);  // Tier 1
+    e += cf[0];
+    ex_out[q] = e <= 0.0 ? prm->clamp_floor : e;
+  }
+  return SR_OK;
+}
+
+sr_status sr_recommend(const sr_params* prm, const double* ex, const uint8_t* candidate, int32_t n_opts,
+                       int8_t* rec_out, int32_t* n_rec_out) {
+  if (!prm || !ex || !rec_out || !n_rec_out || n_opts < 0 || n_opts > 16 || prm->max_count < 1 ||
+      prm->max_count > 64)
+    return SR_E_ARG;
+  int ids[16], n = 0;
+  for (int q = 0; q < n_opts; ++q)
+    if ((!candidate || candidate[q]) && !std::isnan(ex[q]) && ex[q] >= prm->threshold) ids[n++] = q;  // R8
+  std::stable_sort(ids, ids + n, [&](int a, int b) { return ex[a] > ex[b]; });  // (EX desc, id asc), R10
+  const int k = std::min(n, (int)prm->max_count);
+  for (int q = 0; q < prm->max_count; ++q) rec_out[q] = q < k ? (int8_t)ids[q] : (int8_t)-1;
+  *n_rec_out = k;
   return SR_OK;
 }
 

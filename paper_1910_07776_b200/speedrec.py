@@ -71,7 +71,8 @@ MASK_SCORE_DTYPE = np.dtype([("n_correct", "<i4"), ("n_test", "<i4"), ("n_rec", 
 # Every symbol include/speedrec.h declares (checked by tests/test_boundary.py).
 EXPORTS = ["sr_create", "sr_destroy", "sr_last_error", "sr_version", "sr_load_dataset",
            "sr_define_scenarios", "sr_default_params", "sr_evaluate", "sr_rates", "sr_synchronize",
-           "sr_set_timing", "sr_kernel_stats", "sr_reset_kernel_stats", "sr_last_launch_count"]
+           "sr_set_timing", "sr_kernel_stats", "sr_reset_kernel_stats", "sr_last_launch_count",
+           "sr_fit", "sr_predict", "sr_recommend"]
 
 _lib = None
 
@@ -112,6 +113,14 @@ def lib() -> ct.CDLL:
         L.sr_reset_kernel_stats.restype = ct.c_int32
         L.sr_last_launch_count.argtypes = [ct.c_void_p]
         L.sr_last_launch_count.restype = ct.c_int32
+        L.sr_fit.argtypes = [ct.c_void_p, ct.POINTER(sr_params), ct.c_int64, ct.c_void_p]
+        L.sr_fit.restype = ct.c_int32
+        L.sr_predict.argtypes = [ct.POINTER(sr_params), ct.c_void_p, ct.c_int32, ct.c_int32, ct.c_void_p,
+                                 ct.c_double, ct.c_void_p]
+        L.sr_predict.restype = ct.c_int32
+        L.sr_recommend.argtypes = [ct.POINTER(sr_params), ct.c_void_p, ct.c_void_p, ct.c_int32, ct.c_void_p,
+                                   ct.POINTER(ct.c_int32)]
+        L.sr_recommend.restype = ct.c_int32
         _lib = L
     return _lib
 
@@ -239,6 +248,13 @@ class Context:
         self._check(lib().sr_evaluate(self._h, ct.byref(p), first, count, ct.byref(o)))
         return out
 
+    def fit(self, scenario: int, params: Optional[sr_params] = None) -> np.ndarray:
+        """sr_fit: [O][1 + C] raw-counter models (c0, u) of one scenario; NaN c0 = no model."""
+        coef = np.zeros((self.shape["O"], self.shape["C"] + 1) if self.shape else 1)
+        p = params or default_params()
+        self._check(lib().sr_fit(self._h, ct.byref(p), int(scenario), _ptr(coef)))
+        return coef
+
     def rates(self) -> np.ndarray:
         N = self.shape["G"] * 64
         x = np.zeros((N, self.shape["C"]))
@@ -265,3 +281,30 @@ class Context:
 
     def last_launch_count(self) -> int:
         return int(lib().sr_last_launch_count(self._h))
+
+
+def predict(coef: np.ndarray, counters: np.ndarray, cycles: float, params: Optional[sr_params] = None) -> np.ndarray:
+    """sr_predict: Tier-2 EX of one user profile from sr_fit's models."""
+    coef = np.ascontiguousarray(coef, dtype=np.float64)
+    counters = np.ascontiguousarray(counters, dtype=np.float64)
+    O, C1 = coef.shape
+    ex = np.zeros(O)
+    st = lib().sr_predict(ct.byref(params or default_params()), _ptr(coef), O, C1 - 1, _ptr(counters),
+                          float(cycles), _ptr(ex))
+    if st:
+        raise SpeedrecError(st, f"predict: status {st}")
+    return ex
+
+
+def recommend(ex: np.ndarray, candidate: Optional[np.ndarray] = None,
+              params: Optional[sr_params] = None) -> list:
+    """sr_recommend: Tier-3 list: ids with EX >= threshold, (EX desc, id asc), first max_count."""
+    p = params or default_params()
+    ex = np.ascontiguousarray(ex, dtype=np.float64)
+    cand = None if candidate is None else np.ascontiguousarray(candidate, dtype=np.uint8)
+    rec = np.zeros(p.max_count, dtype=np.int8)
+    n = ct.c_int32(0)
+    st = lib().sr_recommend(ct.byref(p), _ptr(ex), _ptr(cand), len(ex), _ptr(rec), ct.byref(n))
+    if st:
+        raise SpeedrecError(st, f"recommend: status {st}")
+    return [int(r) for r in rec[:n.value]]

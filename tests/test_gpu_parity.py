@@ -232,8 +232,8 @@ def test_errors_name_the_entity(Context):
         ctx.evaluate(60, 10)
     assert e.value.status == S.SR_E_ARG
     with pytest.raises(SpeedrecError) as e:
-        ctx.evaluate(0, 1, params=default_params(learner=1))
-    assert e.value.status == S.SR_E_UNSUPPORTED
+        ctx.evaluate(0, 1, params=default_params(learner=7))
+    assert e.value.status == S.SR_E_ARG and "learner" in str(e.value)
     r = ctx.evaluate(0, 0)                           # empty batch is valid
     assert r["opt"].shape[0] == 0
     ctx.close()
