@@ -165,6 +165,8 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--splits", type=int, default=None, help="scenarios per GPU (default: config size)")
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
+    ap.add_argument("--masks-k", type=int, default=10,
+                    help="C5: all 2^k subsets of counters [0, k) (the full config is k = 20)")
     ap.add_argument("--learner", default="linreg", choices=list(LEARNERS),
                     help="linreg = ridge LS (the paper's model); ibk = the NEXT-1 k-NN learner")
     ap.add_argument("--ref-sample", type=int, default=4000)
@@ -179,7 +181,7 @@ def main():
     import gen
     per_gpu = args.splits or {"C3": 1_000_000, "C1": 64, "C2": 240}.get(args.config, 100_000)
     cfg = gen.make_config(args.config, n_splits=per_gpu * world if args.config in ("C3", "C4") else None,
-                          n_masks_k=10 if args.config == "C5" else None)
+                          n_masks_k=args.masks_k if args.config == "C5" else None)
     if args.config not in ("C3", "C4"):
         per_gpu = cfg.scenarios.n_scenarios // world
 
@@ -207,15 +209,31 @@ def main():
     ds = cfg.dataset
     ctx.load(ds)
     ctx.define_scenarios(cfg.scenarios)
-    first, count = D.weak_range(per_gpu, rank)               # scenario shard of this rank
     O = ds.n_opt_ids
     dev = torch.device("cuda", local)
-    out = dict(opt=torch.empty(count * O * OPT_SCORE_DTYPE.itemsize, dtype=torch.uint8, device=dev),
-               scn=torch.empty(count * SCN_SCORE_DTYPE.itemsize, dtype=torch.uint8, device=dev),
-               totals=torch.zeros(4, dtype=torch.int64, device=dev))
+    c5 = args.config == "C5"
+    if c5:
+        # C5: popcount-stratified round-robin of the 2^k masks,
+        # per-mask sums over the 128 LOO folds + top-64 in the kernels
+        masks = D.stratified_masks(args.masks_k, rank, world)
+        sc = cfg.scenarios
+        sc.all_subsets_k = 0
+        sc.feature_masks = np.stack([masks.astype(np.uint64), np.zeros(len(masks), np.uint64)], 1)
+        sc.n_masks = len(masks)
+        ctx.define_scenarios(sc)
+        folds = sc.n_splits
+        first, count = 0, len(masks) * folds
+        out = dict(masks=torch.empty(len(masks) * 16, dtype=torch.uint8, device=dev),
+                   top=torch.empty(64, dtype=torch.int64, device=dev),
+                   totals=torch.zeros(4, dtype=torch.int64, device=dev))
+    else:
+        first, count = D.weak_range(per_gpu, rank)           # scenario shard of this rank
+        out = dict(opt=torch.empty(count * O * OPT_SCORE_DTYPE.itemsize, dtype=torch.uint8, device=dev),
+                   scn=torch.empty(count * SCN_SCORE_DTYPE.itemsize, dtype=torch.uint8, device=dev),
+                   totals=torch.zeros(4, dtype=torch.int64, device=dev))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     from paper_1910_07776_b200.speedrec import default_params
-    prm = default_params(learner=LEARNERS[args.learner])
+    prm = default_params(learner=LEARNERS[args.learner], top_k=64)
 
     for _ in range(args.warmup):
         ctx.evaluate(first, count, params=prm, out=out)
@@ -247,16 +265,34 @@ def main():
     value = world * count / (ms / 1e3)
 
     # ---------------- roofline of the dominant kernel (FP64 ALU/DMMA bound)
-    opt = out["opt"].cpu().numpy().view(OPT_SCORE_DTYPE).reshape(count, O)
     big = ds.n_groups > 64          # CTA-per-fit path (C4): prediction runs in k_rank_big
-    n_tr, n_te = opt["n_train"].ravel(), opt["n_test"].ravel()
     name_dom = "k_fit_big" if big else "k_fit_warp"
-    if args.learner == "ibk":
-        flops_launch = knn_flops(n_tr, n_te, ds.n_counters)
-    elif big:
-        flops_launch = fit_flops_big(n_tr, n_te, ds.n_counters)
+    if c5:
+        # n, t per (fold, opt) do not depend on the mask: take them from one
+        # untimed per-scenario pass over the folds of this rank's first mask,
+        # then d = popcount(mask) per mask
+        r1 = ctx.evaluate(0, folds, params=prm)
+        n_tr, n_te = r1["opt"]["n_train"].ravel(), r1["opt"]["n_test"].ravel()
+        pcs = np.array([bin(int(m)).count("1") for m in masks])
+        if stats.get("k_mask_fit", (0, 0.0))[0] > 0:
+            # feature-mask path: per fit on the precomputed Gram
+            name_dom = "k_mask_fit"
+            n_fit = float(np.sum((n_tr > 0) & (n_te > 0)))
+            ff = lambda d: n_fit * 2.0 * (d ** 3 / 6 + d ** 2 + d)
+        elif args.learner == "ibk":
+            ff = lambda d: knn_flops(n_tr, n_te, d)
+        else:
+            ff = lambda d: fit_flops(n_tr, n_te, d, refine=2)
+        flops_launch = sum(float(np.sum(pcs == d)) * ff(int(d)) for d in np.unique(pcs))
     else:
-        flops_launch = fit_flops(n_tr, n_te, ds.n_counters, refine=2)
+        opt = out["opt"].cpu().numpy().view(OPT_SCORE_DTYPE).reshape(count, O)
+        n_tr, n_te = opt["n_train"].ravel(), opt["n_test"].ravel()
+        if args.learner == "ibk":
+            flops_launch = knn_flops(n_tr, n_te, ds.n_counters)
+        elif big:
+            flops_launch = fit_flops_big(n_tr, n_te, ds.n_counters)
+        else:
+            flops_launch = fit_flops(n_tr, n_te, ds.n_counters, refine=2)
     n_dom, ms_dom = stats.get(name_dom, (0, 0.0))
     avg_dom = ms_dom / max(n_dom, 1)                 # average launch duration (CUDA events, live)
     launches_per_step = max(n_dom // max(args.steps, 1), 1)
@@ -266,7 +302,8 @@ def main():
     sm_max = clk_sum.get("sm_max_mhz") or 1965.0
     props = torch.cuda.get_device_properties(dev)
     peak = props.multi_processor_count * FP64_FMA_PER_CLK_PER_SM * 2 * sm_max * 1e6 / 1e12
-    achieved = flops_launch / (avg_dom / 1e3) / 1e12 if avg_dom > 0 else 0.0
+    # = flops per launch / average launch time; also right for unequal launches
+    achieved = flops_step / (ms_dom / max(args.steps, 1) / 1e3) / 1e12 if ms_dom > 0 else 0.0
     share = ms_dom / max(sum(v[1] for v in stats.values()), 1e-9)
 
     # ---------------- end to end: host buffers through the C-ABI, copies inside
@@ -276,12 +313,19 @@ def main():
         hy = torch.from_numpy(ds.cycles).pin_memory()
         hr = torch.from_numpy(ds.runtime_ms).pin_memory()
         hb = torch.from_numpy(ds.opt_bit).pin_memory()
-        hopt = torch.empty(count * O * OPT_SCORE_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
-        hscn = torch.empty(count * SCN_SCORE_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
         htot = torch.zeros(4, dtype=torch.int64).pin_memory()
         from paper_1910_07776_b200.speedrec import sr_outputs, lib
         import ctypes as ct
-        hout = sr_outputs(hopt.data_ptr(), hscn.data_ptr(), None, None, htot.data_ptr(), 0)
+        if c5:
+            hmask = torch.empty(len(masks) * 16, dtype=torch.uint8).pin_memory()
+            htop = torch.empty(64, dtype=torch.int64).pin_memory()
+            hout = sr_outputs(None, None, None, None, htot.data_ptr(), hmask.data_ptr(), htop.data_ptr(), 0)
+            d2h = hmask.numel() + htop.numel() * 8 + 32
+        else:
+            hopt = torch.empty(count * O * OPT_SCORE_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+            hscn = torch.empty(count * SCN_SCORE_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+            hout = sr_outputs(hopt.data_ptr(), hscn.data_ptr(), None, None, htot.data_ptr(), None, None, 0)
+            d2h = hopt.numel() + hscn.numel() + 32
         e2e_ms = []
         for k in range(max(2, min(args.steps, 5)) + 1):
             flush.fill_(float(k))
@@ -299,7 +343,7 @@ def main():
         te = D.max_over_ranks(float(np.mean(e2e_ms)), dist, device=xdev)
         e2e = {"value": world * count / (te / 1e3), "unit": "scenario_evals/s",
                "h2d_bytes_per_step": int(hc.numel() * 8 + hy.numel() * 8 + hr.numel() * 8 + hb.numel()),
-               "d2h_bytes_per_step": int(hopt.numel() + hscn.numel() + 32)}
+               "d2h_bytes_per_step": int(d2h)}
 
     # ---------------- CPU oracle baseline (rank 0, N=1 only, bounded sample)
     cpu = None
@@ -309,12 +353,19 @@ def main():
         cpu = {"value": v, "unit": "scenario_evals/s", "cores": threads, "kind": "oracle",
                "sample": f"first {args.cpu_sample} scenarios of {args.config} (same splits the GPU evaluates)"}
 
+    top_global = None
+    if c5:   # C5 A7: local top-64 (library) -> global mask ids -> exact merge over ranks
+        from paper_1910_07776_b200.speedrec import MASK_SCORE_DTYPE
+        rows = out["masks"].cpu().numpy().view(MASK_SCORE_DTYPE)
+        tl = out["top"].cpu().numpy()
+        corr = [int(rows["n_correct"][i]) if i >= 0 else 0 for i in tl]
+        top_global = D.merge_top_masks(D.local_top_to_global(tl, masks).tolist(), corr, 64, dist, device=xdev)
     if rank == 0:
         tt = tot.cpu().numpy()
         line = {
             "metric": METRIC, "value": value, "unit": "scenario_evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if c5 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg, args, count),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": None,
@@ -328,6 +379,10 @@ def main():
                          "recommendations": int(tt[2]), "rec_hits": int(tt[3])},
             "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in stats.items()},
         }
+        if c5:
+            line["config"].update(masks_k=args.masks_k, masks_per_gpu=int(len(masks)), folds=int(folds),
+                                  partition="popcount-stratified round-robin (SURVEY 8(e))")
+            line["top_masks_head"] = [int(m) for m in top_global[:8]]
         print(json.dumps(line), flush=True)
     ctx.close()
     if dist:

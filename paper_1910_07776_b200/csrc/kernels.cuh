@@ -201,6 +201,11 @@ __device__ __forceinline__ int warp_isum(int v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
 }
+__device__ __forceinline__ unsigned long long warp_usum(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
 __device__ __forceinline__ uint64_t warp_xor(uint64_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v ^= __shfl_xor_sync(FULL, v, o);
@@ -220,7 +225,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // ---------------------------------------------------------------- A0 / A1
 // x = counters / cycles, IEEE division => bit-exact with any
 // correctly rounded implementation.
-__global__ void k_rates(const double* __restrict__ counters, const double* __restrict__ cycles,
+static __global__ void k_rates(const double* __restrict__ counters, const double* __restrict__ cycles,
                         double* __restrict__ x, long long n_slots, int C) {
   long long total = n_slots * C;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -230,7 +235,7 @@ __global__ void k_rates(const double* __restrict__ counters, const double* __res
 
 // ylab[g][o][k] = rt[before] / rt[after] (reading D2), 0 when the
 // optimization is absent from the group's program.
-__global__ void k_labels(const double* __restrict__ rt, const int8_t* __restrict__ opt_bit,
+static __global__ void k_labels(const double* __restrict__ rt, const int8_t* __restrict__ opt_bit,
                          double* __restrict__ ylab, int G, int O, int IR) {
   int total = G * O * 32;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -249,7 +254,7 @@ __global__ void k_labels(const double* __restrict__ rt, const int8_t* __restrict
 // each 1024-thread block bitonic-sorts up to 1024 keys in shared memory
 // (descending) and keeps its first K.  Launched repeatedly (n -> n/1024*K)
 // until one block remains.  Integer keys => exact and order-independent.
-__global__ void __launch_bounds__(1024) k_topk_keys(const unsigned long long* __restrict__ in, long long n,
+static __global__ void __launch_bounds__(1024) k_topk_keys(const unsigned long long* __restrict__ in, long long n,
                                                     unsigned long long* __restrict__ out, int K) {
   __shared__ unsigned long long sk[1024];
   const long long base = (long long)blockIdx.x * 1024;
@@ -274,7 +279,7 @@ __global__ void __launch_bounds__(1024) k_topk_keys(const unsigned long long* __
 }
 
 // keys -> mask ids (-1 for padding), first K of a descending-sorted list.
-__global__ void k_decode_top(const unsigned long long* __restrict__ keys, long long n, int64_t* __restrict__ ids,
+static __global__ void k_decode_top(const unsigned long long* __restrict__ keys, long long n, int64_t* __restrict__ ids,
                              int K) {
   for (int t = threadIdx.x; t < K; t += blockDim.x) {
     const unsigned long long k = t < n ? keys[t] : 0ull;
@@ -283,7 +288,7 @@ __global__ void k_decode_top(const unsigned long long* __restrict__ keys, long l
 }
 
 // Validation of the Tier-1 input: first offending flat index.
-__global__ void k_validate(const double* __restrict__ counters, const double* __restrict__ cycles,
+static __global__ void k_validate(const double* __restrict__ counters, const double* __restrict__ cycles,
                            const double* __restrict__ rt, long long n_slots, int C,
                            unsigned long long* __restrict__ bad) {
   long long total = n_slots * C;

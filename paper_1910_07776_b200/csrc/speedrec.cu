@@ -16,6 +16,7 @@
 #include <cstdlib>
 
 #include "../../include/speedrec.h"
+#include "eval_masks.cuh"
 #include "eval_warp.cuh"
 #include "fit_big.cuh"
 #include "kernels.cuh"
@@ -67,6 +68,10 @@ struct sr_ctx {
   DevBuf gscratch, out_opt, out_scn, out_ex, out_rec, out_tot, out_mask, out_top, keys_a, keys_b;
   DevBuf big_lists, big_y, big_U, big_c0, big_flag;  // large-batch path (> 64 groups)
   DevBuf fit_coef;              // sr_fit: [O][1 + C]
+  // feature-mask path (eval_masks.cuh)
+  DevBuf mp_G, mp_r, mp_z, mp_meta, mp_perm;
+  long long sc_gen = 0, perm_key[3] = {-1, -1, -1};
+  std::vector<int> perm_off;     // [kMaskMaxD + 2] start of each popcount group in mp_perm
   double* coef_req = nullptr;   // set by sr_fit for the duration of its evaluate
   DevBuf extab, trained, guard_acc, mask_acc;         // fit -> rank exchange (warp path)
   // accounting
@@ -433,6 +438,7 @@ sr_status sr_define_scenarios(sr_ctx* c, const sr_scenarios* s, int64_t* n_scena
   c->n_tg = std::max(n_tg, 1);
   c->n_os = std::max(n_os, 1);
   c->have_sc = true;
+  ++c->sc_gen;
   *n_scenarios = s->n_splits * s->n_masks;
   return SR_OK;
 }
@@ -472,6 +478,120 @@ WarpLayout plan_layout(const sr_ctx* c, int mcap, bool ibk) {
   L.off_ufull = take(8 * c->C);
   L.bytes = align16(off);
   return L;
+}
+
+// Feature-mask path: LOO batches of whole feature masks
+// (config C5).  Sets *used = false, with no side effects on the outputs,
+// when the batch is outside its regime; the warp path then runs.
+sr_status run_mask_path(sr_ctx* c, const sr_params* prm, long long first, long long count, const EvalArgs& A,
+                        bool* used) {
+  *used = false;
+  const long long S = c->sc.n_splits;
+  const int O = c->O, C = c->C;
+  if (const char* e = getenv("SPEEDREC_MASK_PATH"))
+    if (atoi(e) == 0) return SR_OK;
+  if (c->sc.kind != SR_SPLIT_LOO || C > kMaskMaxC || O > kMaskMaxO || prm->learner != SR_LINREG ||
+      prm->debug_mcap > 0 || count <= 0 || first % S || count % S || c->sc.n_masks < 2)
+    return SR_OK;
+  const long long mask0 = first / S, nm = count / S;
+  if (nm > INT32_MAX) return SR_OK;
+  sr_status st;
+  // popcount groups of the call's masks (cached per scenario definition and range)
+  if (c->perm_key[0] != c->sc_gen || c->perm_key[1] != mask0 || c->perm_key[2] != nm) {
+    std::vector<int> pc(nm);
+    for (long long i = 0; i < nm; ++i) {
+      const long long f = mask0 + i;
+      int d;
+      if (c->sc.all_subsets_k > 0) {
+        d = __builtin_popcountll((unsigned long long)f);
+      } else if (c->sc.feature_masks) {
+        if (c->h_fmasks[2 * f + 1] != 0ull) return SR_OK;
+        d = __builtin_popcountll(c->h_fmasks[2 * f] & (C >= 64 ? ~0ull : ((1ull << C) - 1ull)));
+      } else {
+        d = C;
+      }
+      if (d > kMaskMaxD) return SR_OK;
+      pc[i] = d;
+    }
+    std::vector<int> off(kMaskMaxD + 2, 0), perm(nm);
+    for (long long i = 0; i < nm; ++i) ++off[pc[i] + 1];
+    for (int d = 0; d <= kMaskMaxD; ++d) off[d + 1] += off[d];
+    std::vector<int> pos(off.begin(), off.end() - 1);
+    for (long long i = 0; i < nm; ++i) perm[pos[pc[i]]++] = (int)i;
+    if ((st = ensure(c, c->mp_perm, (size_t)nm * 4))) return st;
+    CU(cudaMemcpyAsync(c->mp_perm.p, perm.data(), (size_t)nm * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));   // perm is a stack vector
+    c->perm_off = off;
+    c->perm_key[0] = c->sc_gen;
+    c->perm_key[1] = mask0;
+    c->perm_key[2] = nm;
+  }
+  int dmax = 0;
+  for (int d = 0; d <= kMaskMaxD; ++d)
+    if (c->perm_off[d + 1] > c->perm_off[d]) dmax = d;
+  const long long items = S * O;
+  if ((st = ensure(c, c->mp_G, (size_t)items * C * C * 8)) || (st = ensure(c, c->mp_r, (size_t)items * C * 8)) ||
+      (st = ensure(c, c->mp_z, (size_t)items * C * 8)) || (st = ensure(c, c->mp_meta, (size_t)items * sizeof(PrepMeta))))
+    return st;
+  MaskArgs M{};
+  M.sd = A.sd;
+  M.x = A.x;
+  M.ylab = A.ylab;
+  M.opt_bit = A.opt_bit;
+  M.P = c->P;
+  M.IR = c->I * c->R;
+  M.C = C;
+  M.O = O;
+  M.G = c->G;
+  M.lambda = prm->ridge;
+  M.threshold = prm->threshold;
+  M.clamp_floor = prm->clamp_floor;
+  M.guard_tol = prm->guard_tol;
+  M.max_count = prm->max_count;
+  M.first = first;
+  M.mask0 = mask0;
+  M.pG = (double*)c->mp_G.p;
+  M.pr = (double*)c->mp_r.p;
+  M.pz = (double*)c->mp_z.p;
+  M.pm = (PrepMeta*)c->mp_meta.p;
+  M.np_tr = c->np_tr;
+  const int prep_smem = 4 * c->np_tr * 12;
+  if (prep_smem > 48 * 1024) CU(cudaFuncSetAttribute(k_mask_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep_smem));
+  if ((st = launch(c, "k_mask_prep", [&] {
+         k_mask_prep<<<(unsigned)((items + 3) / 4), 128, prep_smem, c->stream>>>(M);
+       })))
+    return st;
+  // regime check (one small read-back): every fit primal without refinement
+  // under the warp path's rule: n <= 64 and n - 1 >= 2 d
+  std::vector<PrepMeta> pm(items);
+  CU(cudaMemcpyAsync(pm.data(), M.pm, items * sizeof(PrepMeta), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (const PrepMeta& q : pm)
+    if (q.n > 0 && (q.n > 64 || q.n - 1 < 2 * dmax || q.nt > 1)) return SR_OK;
+  M.opt_out = A.opt_out;
+  M.scn_out = A.scn_out;
+  M.ex_out = A.ex_out;
+  M.rec_out = A.rec_out;
+  M.totals = A.totals;
+  M.mask_acc = A.agg ? A.mask_acc : nullptr;
+  for (int d = 0; d <= kMaskMaxD; ++d) {
+    const int n_it = c->perm_off[d + 1] - c->perm_off[d];
+    if (n_it == 0) continue;
+    M.perm = (const int32_t*)c->mp_perm.p + c->perm_off[d];
+    M.n_items = n_it;
+    // enough threads to fill the GPU: split the folds when a group has few masks
+    const long long want = (long long)c->sm_count * 1024;
+    M.fold_chunks = (int)std::max(1LL, std::min<long long>(S, want / n_it));
+    const unsigned grid = (unsigned)(((long long)n_it * M.fold_chunks + 127) / 128);
+    auto fn = d < 10 ? mask_fit_launch_a : d < 14 ? mask_fit_launch_b : d < 17 ? mask_fit_launch_c
+                                                                         : mask_fit_launch_d;
+    cudaError_t ce = cudaSuccess;
+    const sr_status s2 = launch(c, "k_mask_fit", [&] { ce = fn(d, grid, c->stream, M); });
+    if (ce != cudaSuccess) return fail(c, SR_E_CUDA, "k_mask_fit<%d>: %s", d, cudaGetErrorString(ce));
+    if (s2) return s2;
+  }
+  *used = true;
+  return SR_OK;
 }
 
 // Large-batch path (> 64 groups, config C4): k_fit_big per (scenario, opt)
@@ -768,7 +888,9 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   if (A.ex_out) CU(cudaMemsetAsync(A.ex_out, 0, b_ex, c->stream));
   if (A.rec_out) CU(cudaMemsetAsync(A.rec_out, 0xFF, b_rec, c->stream));
   const int cmax = c->n_os <= 8 ? 8 : 16;
-  for (long long c0 = 0; c0 < count; c0 += chunk) {
+  bool mask_path = false;
+  if ((st = run_mask_path(c, prm, first, count, A, &mask_path))) return st;
+  for (long long c0 = 0; c0 < (mask_path ? 0 : count); c0 += chunk) {
     const long long cc = std::min(chunk, count - c0);
     A.first = first + c0;
     A.count = cc;

@@ -28,6 +28,31 @@ def strong_range(total: int, rank: int, world: int, align: int = 1) -> Tuple[int
     return lo * align, (hi - lo) * align
 
 
+def stratified_masks(k: int, rank: int, world: int) -> np.ndarray:
+    """C5 partition: sort the 2^k feature masks by (popcount,
+    mask) and give the j-th to rank j mod W, so every rank gets the same
+    number of masks of each size to within one (a fit's cost grows with the
+    mask's popcount; contiguous or mod-W blocks leave the busiest rank ~36 %
+    above the mean at W = 8).  Returns this rank's masks, ascending, so local
+    index order is global mask order (ties in the top-K rule stay exact)."""
+    m = np.arange(1 << k, dtype=np.int64)
+    pc = np.zeros_like(m)
+    for b in range(k):
+        pc += (m >> b) & 1
+    order = np.lexsort((m, pc))
+    return np.sort(m[order[rank::world]])
+
+
+def local_top_to_global(top_local: np.ndarray, masks: np.ndarray) -> np.ndarray:
+    """Map the library's local top-K indices (into this rank's mask list) to
+    global mask ids; -1 padding stays -1."""
+    top_local = np.asarray(top_local, dtype=np.int64)
+    out = np.full(len(top_local), -1, dtype=np.int64)
+    ok = top_local >= 0
+    out[ok] = masks[top_local[ok]]
+    return out
+
+
 def reduce_totals(totals, dist) -> "torch.Tensor":
     """Sum the 4 pooled int64 totals over ranks (exact)."""
     t = totals.clone()
@@ -49,18 +74,18 @@ def topk_key(n_correct: int, mask_id: int) -> int:
     return (int(n_correct) << 32) | (0xFFFFFFFF - int(mask_id))
 
 
-def merge_top_masks(local_ids, local_correct, k: int, dist) -> np.ndarray:
+def merge_top_masks(local_ids, local_correct, k: int, dist, device="cpu") -> np.ndarray:
     """Global top-k mask ids from each rank's local top-k (ids -1 padded):
     all-gather the (key) lists and select the k largest integer keys."""
     import torch
     keys = np.array([topk_key(c, m) if m >= 0 else 0 for m, c in zip(local_ids, local_correct)],
                     dtype=np.uint64).view(np.int64)
-    t = torch.from_numpy(keys.copy())
+    t = torch.from_numpy(keys.copy()).to(device)
     if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
         out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
         dist.all_gather(out, t)
         t = torch.cat(out)
-    allk = t.numpy().view(np.uint64)
+    allk = t.cpu().numpy().view(np.uint64)
     allk = np.sort(allk[allk != 0])[::-1][:k]
     ids = (0xFFFFFFFF - (allk & np.uint64(0xFFFFFFFF))).astype(np.int64)
     return np.concatenate([ids, -np.ones(k - len(ids), dtype=np.int64)])

@@ -57,6 +57,71 @@ def test_gloo_world2_exchange():
         assert top == [1, 2, 4, 7]          # ties on 9 correct broken by mask id (O8)
 
 
+def test_stratified_mask_partition_covers_and_balances():
+    for k, world in ((10, 8), (12, 4), (20, 8), (5, 2)):
+        parts = [D.stratified_masks(k, r, world) for r in range(world)]
+        allm = np.sort(np.concatenate(parts))
+        assert np.array_equal(allm, np.arange(1 << k))
+        # work proxy per mask: p^3/6 + p^2 + p with p = popcount + 1
+        cost = []
+        for q in parts:
+            p = np.array([bin(int(x)).count("1") + 1 for x in q], dtype=np.float64)
+            cost.append((p ** 3 / 6 + p ** 2 + p).sum())
+            assert (np.diff(q) > 0).all()               # ascending: local order = global order
+        cost = np.array(cost)
+        assert cost.max() / cost.mean() - 1 < (1e-4 if k >= 16 else 3e-2 if k >= 10 else 0.15), (k, world, cost)
+    # contiguous blocks are measurably worse (the reason for stratifying)
+    blocks = np.array_split(np.arange(1 << 20), 8)
+    pcs = [np.array([bin(int(x)).count("1") for x in b[:: 64]]).mean() for b in blocks]
+    assert max(pcs) - min(pcs) > 2
+
+
+def _c5_worker(rank, world, port, q):
+    """Per-rank C5 evaluation of its stratified masks (the oracle stands in
+    for the GPU here), local top-K -> global ids -> all-gather merge."""
+    import gen
+    import oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = gen.make_config("C5", n_masks_k=5)
+        sc = cfg.scenarios
+        masks = D.stratified_masks(5, rank, world)
+        sc.all_subsets_k = 0
+        sc.feature_masks = np.stack([masks.astype(np.uint64), np.zeros(len(masks), np.uint64)], 1)
+        sc.n_masks = len(masks)
+        folds = sc.n_splits
+        ref = oracle.evaluate(cfg.dataset, sc, 0, len(masks) * folds, n_threads=2)
+        rows, top_local = oracle.aggregate_masks(ref["opt"], ref["scn"], folds, top_k=6)
+        top = D.local_top_to_global(np.r_[top_local, -np.ones(6 - len(top_local), np.int64)], masks)
+        corr = [int(rows["n_correct"][i]) if i >= 0 else 0 for i in np.r_[top_local, -np.ones(6 - len(top_local), np.int64)]]
+        merged = D.merge_top_masks(top.tolist(), corr, 6, dist)
+        q.put((rank, merged.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_c5_stratified_top_k_equals_single_process():
+    import gen
+    import oracle
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_c5_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = gen.make_config("C5", n_masks_k=5)
+    folds = cfg.scenarios.n_splits
+    ref = oracle.evaluate(cfg.dataset, cfg.scenarios, 0, cfg.scenarios.n_scenarios)
+    _, want = oracle.aggregate_masks(ref["opt"], ref["scn"], folds, top_k=6)
+    for _, got in res:
+        assert got == want.tolist()
+
+
 def test_shard_ranges_partition():
     for total, world, align in ((1000, 2, 1), (1003, 4, 1), (128 * 1024, 8, 128), (64, 8, 1)):
         seen = []

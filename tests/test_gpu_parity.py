@@ -107,6 +107,45 @@ def test_c5_mask_aggregation_and_top_k(Context):
     ctx.close()
 
 
+def test_c5_full_2pow20_masks_sampled(Context):
+    """Full C5 (all 2^20 masks x 128 LOO folds = 1.34e8 scenarios) through the
+    feature-mask path in the bench's launch: the mask rows of sampled masks
+    (each popcount, the extremes, the reported top 8) equal the oracle's sums
+    over their 128 folds exactly; the top-64 keys are ordered by the rule and
+    dominate every sampled mask."""
+    from paper_1910_07776_b200 import default_params
+    cfg = gen.make_config("C5", n_masks_k=20)
+    folds = cfg.scenarios.n_splits
+    n = cfg.scenarios.n_scenarios
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    got = ctx.evaluate(0, n, params=default_params(top_k=64), want_masks=True, per_scenario=False, n_folds=folds)
+    ctx.close()
+    rows, top = got["masks"], got["top"]
+    rng = np.random.default_rng(3)
+    sample = {0, 1, (1 << 20) - 1, 0b1010101010, *top[:8].tolist()}
+    for d in range(21):            # one mask of each popcount
+        bits = rng.choice(20, size=d, replace=False)
+        sample.add(int(sum(1 << int(b) for b in bits)))
+    sample |= set(rng.integers(0, 1 << 20, size=12).tolist())
+    from concurrent.futures import ThreadPoolExecutor
+    def one(m):
+        r = oracle.evaluate(cfg.dataset, cfg.scenarios, m * folds, folds, n_threads=1)
+        assert r["scn"]["n_guard"].sum() == 0
+        return oracle.aggregate_masks(r["opt"], r["scn"], folds, first_mask=m, top_k=1)[0][0]
+    with ThreadPoolExecutor(8) as pool:
+        refs = dict(zip(sorted(sample), pool.map(one, sorted(sample))))
+    for m, ref in refs.items():
+        for f in ref.dtype.names:
+            assert rows[f][m] == ref[f], (m, f, rows[f][m], ref[f])
+    keys = [(int(rows["n_correct"][m]), -int(m)) for m in top]
+    assert keys == sorted(keys, reverse=True)
+    kth = keys[-1]
+    for m in refs:
+        assert m in set(top.tolist()) or (int(refs[m]["n_correct"]), -m) < kth
+
+
 def test_c4_large_batch_path_small(Context):
     """> 64 groups -> the CTA-per-fit DMMA path (k_fit_big + k_rank_big):
     96 programs x 64 variants x 128 counters (n ~ 770 training pairs, d = 128)."""
