@@ -146,6 +146,32 @@ def knn_flops(n: np.ndarray, t: np.ndarray, d: int) -> float:
     return float(3.0 * np.where((n > 0) & (t > 0), n * t * d, 0.0).sum())
 
 
+OTHER_CONFIGS = [("C1", ["--cpu-sample", "64"]), ("C2", ["--cpu-sample", "240"]),
+                 ("C4", ["--splits", "592", "--no-cpu-baseline"]), ("C5", ["--masks-k", "20", "--cpu-sample", "2048"])]
+
+
+def run_other_configs(args):
+    """Secondary lines: the other four configs, each in its own process
+    (same GPU, after the headline measurement), summarised into the headline
+    JSON line under "other_configs"."""
+    res = {}
+    for name, extra in OTHER_CONFIGS:
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", name, "--steps", "5", "--warmup", "3",
+               "--no-e2e", "--no-extra", "--learner", args.learner] + extra
+        try:
+            out = subprocess.run(cmd, capture_output=True, text=True, timeout=600).stdout.strip().splitlines()
+            d = json.loads(out[-1])
+            r = d["roofline"]
+            res[name] = {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
+                         "workload": d["config"]["workload"], "scenarios_per_step": d["config"]["splits_per_gpu"],
+                         "scaling": d["scaling"], "roofline": {k: r[k] for k in ("kernel", "achieved", "frac")},
+                         "cpu_baseline": d.get("cpu_baseline"), "accuracy": d.get("accuracy"),
+                         "top_masks_head": d.get("top_masks_head")}
+        except Exception as e:   # reported, never fatal for the headline line
+            res[name] = {"error": f"{type(e).__name__}: {e}"[:200]}
+    return res
+
+
 METRIC = "train/test scenario evals/sec at 1/2/4/8 B200 (roofline frac) vs CPU oracle"
 
 
@@ -173,6 +199,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=4000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg (tuning runs)")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the secondary per-config lines (C1, C2, C4, C5) of the default run")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -383,6 +411,9 @@ def main():
             line["config"].update(masks_k=args.masks_k, masks_per_gpu=int(len(masks)), folds=int(folds),
                                   partition="popcount-stratified round-robin (SURVEY 8(e))")
             line["top_masks_head"] = [int(m) for m in top_global[:8]]
+        if world == 1 and args.config == "C3" and not args.no_extra:
+            ctx.synchronize()
+            line["other_configs"] = run_other_configs(args)
         print(json.dumps(line), flush=True)
     ctx.close()
     if dist:
