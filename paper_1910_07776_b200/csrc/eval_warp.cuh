@@ -262,7 +262,9 @@ __device__ __forceinline__ double knn_ex(const double* __restrict__ X, int ldx, 
 // ---------------------------------------------------------------- fit kernel
 // MODE 0: ridge LS (the paper's model); 1: IBK (NEXT-1); 2: ridge LS + the
 // sr_fit coefficient store.  Separate instantiations keep the hot code lean.
-template <int WMAX, int MODE>
+// STAGED: x staged in shared memory (compile-time, so every x access is an
+// LDS rather than a generic load).
+template <int WMAX, int MODE, bool STAGED>
 __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const WarpLayout& L = A.L;
@@ -271,10 +273,10 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
   for (int i = tid; i < A.P * A.O; i += nthr) obit[i] = A.opt_bit[i];
   const double* X = A.x;
   int ldx = A.C;
-  if (A.stage_x) {
+  if (STAGED) {
     double* xs = reinterpret_cast<double*>(smem + A.off_stage);
-    const long long tot = (long long)A.G * 64 * A.C;
-    for (long long i = tid; i < tot; i += nthr) xs[(i / A.C) * A.ldxs + (i % A.C)] = A.x[i];
+    const int tot = A.G * 64 * A.C;
+    for (int i = tid; i < tot; i += nthr) xs[(i / A.C) * A.ldxs + (i % A.C)] = A.x[i];
     X = xs;
     ldx = A.ldxs;
   }
@@ -386,11 +388,31 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
     for (int a0 = 0; a0 < d; a0 += 64) {       // two features per lane per row pass
       const int a1 = a0 + lane, a2 = a0 + 32 + lane;
       const int c1 = a1 < d ? F[a1] : 0, c2 = a2 < d ? F[a2] : 0;
-      const double* x0 = X + (long long)trs[0] * ldx;
+      const double* x0 = X + trs[0] * ldx;
       double mn1 = x0[c1], mx1 = mn1, sm1 = mn1, mn2 = x0[c2], mx2 = mn2, sm2 = mn2;
-      #pragma unroll 2
-      for (int i = 1; i < n; ++i) {
-        const double* xr = X + (long long)trs[i] * ldx;
+      // two rows per pass into separate accumulators (independent min/max chains)
+      double nb1 = mn1, xb1 = mx1, tb1 = 0.0, nb2 = mn2, xb2 = mx2, tb2 = 0.0;
+      int i = 1;
+      #pragma unroll 1
+      for (; i + 1 < n; i += 2) {
+        const double* xr = X + trs[i] * ldx;
+        const double* xq = X + trs[i + 1] * ldx;
+        const double v1 = xr[c1], v2 = xr[c2], w1 = xq[c1], w2 = xq[c2];
+        mn1 = fmin(mn1, v1);
+        nb1 = fmin(nb1, w1);
+        mx1 = fmax(mx1, v1);
+        xb1 = fmax(xb1, w1);
+        sm1 += v1;
+        tb1 += w1;
+        mn2 = fmin(mn2, v2);
+        nb2 = fmin(nb2, w2);
+        mx2 = fmax(mx2, v2);
+        xb2 = fmax(xb2, w2);
+        sm2 += v2;
+        tb2 += w2;
+      }
+      if (i < n) {
+        const double* xr = X + trs[i] * ldx;
         const double v1 = xr[c1], v2 = xr[c2];
         mn1 = fmin(mn1, v1);
         mx1 = fmax(mx1, v1);
@@ -399,6 +421,12 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
         mx2 = fmax(mx2, v2);
         sm2 += v2;
       }
+      mn1 = fmin(mn1, nb1);
+      mx1 = fmax(mx1, xb1);
+      sm1 += tb1;
+      mn2 = fmin(mn2, nb2);
+      mx2 = fmax(mx2, xb2);
+      sm2 += tb2;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int a = h ? a2 : a1;
@@ -443,8 +471,8 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
       const int nref = (dual ? 2 * (n - 1) >= deff : ((n - 1) < 2 * deff || n > 64)) ? A.refine : 0;
       if (m > 0 && m <= (L.mcap < 32 ? L.mcap : 32)) {
         const FastView fv{X, ldx, trs, n, col, xb, sv, deff};
-        ok = dual ? fit_fast<true>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane)
-                  : fit_fast<false>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane);
+        ok = dual ? fit_fast<true>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane, L.mcap)
+                  : fit_fast<false>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane, L.mcap);
       } else if (m > 0) {
         const FitView fv{X, ldx, trs, n, col, xb, sv, deff};
         ok = fit_generic(fv, yc, A.lambda, nref, dual, scr, L.vmax, uv, v2, wv, lane);

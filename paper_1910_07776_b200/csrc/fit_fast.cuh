@@ -42,7 +42,7 @@ struct FastView {
 // tiles beyond nb = ceil(m/8) skipped by warp-uniform branches (code size
 // matters more than the template specialisation: instruction cache).
 template <bool DUAL>
-__device__ SR_FAST_FN void gram_fast(const FastView f, int m, double lambda, double* Mpk, int lane) {
+__device__ SR_FAST_FN void gram_fast(const FastView& f, int m, double lambda, double* Mpk, int lane) {
   constexpr int NB = 4, NT = 10;
   const int nb = (m + 7) >> 3;
   double acc[NT][2];
@@ -53,10 +53,12 @@ __device__ SR_FAST_FN void gram_fast(const FastView f, int m, double lambda, dou
   int ca[NB];
   double xba[NB], sa[NB];
   if (DUAL) {
+    // rows >= n only reach Gram rows/columns >= m, which are never stored or
+    // read: point them at row 0 instead of masking every fragment element
 #pragma unroll
     for (int I = 0; I < NB; ++I) {
       const int r = I * 8 + rl;
-      so[I] = r < f.n ? f.trs[r] * f.ldx : -1;
+      so[I] = f.trs[r < f.n ? r : 0] * f.ldx;
     }
   } else {
 #pragma unroll
@@ -84,7 +86,7 @@ __device__ SR_FAST_FN void gram_fast(const FastView f, int m, double lambda, dou
       sr = ri < f.n ? f.trs[ri] * f.ldx : -1;
     }
     auto frag = [&](int I) -> double {
-      if (DUAL) return so[I] >= 0 ? (f.X[so[I] + c] - xbv) * sv : 0.0;
+      if (DUAL) return (f.X[so[I] + c] - xbv) * sv;
       return sr >= 0 ? (f.X[sr + ca[I]] - xba[I]) * sa[I] : 0.0;
     };
     fr[0] = frag(0);
@@ -174,10 +176,13 @@ __device__ SR_FAST_FN double solve_rl(const double* M, int m, int lane, double m
 // (vectorised 16-byte loads, row j broadcast), lane j takes the rsqrt pivot,
 // lanes i > j scale.  One __syncwarp per pivot, no stores of partial updates.
 // On exit M holds L (scaled); myinv = 1/L_{lane,lane}.
-__device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv) {
+// aug: row m holds a right-hand side b (m < 32); the same column steps turn it
+// into y = L^-1 b (forward substitution fused into the factorisation).
+__device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv, bool aug = false) {
   bool ok = true;
   myinv = 0.0;
-  double* ri = M + rb2(lane < m ? lane : 0);
+  const int mr = m + (aug ? 1 : 0);               // rows carried through the column steps
+  double* ri = M + rb2(lane < mr ? lane : 0);
   const double* rj = M;                           // row j, advanced by its padded length
   #pragma unroll 1
   for (int j = 0; j < m; ++j) {
@@ -193,7 +198,7 @@ __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv) {
     if (k < j) s0 = fma(ri[k], rj[k], s0);
     const double v = ri[j] - (s0 + s1);          // lane j: pivot; lanes i > j: unscaled L_ij
     const double r = __shfl_sync(FULL, rsqrt(v), j);  // 1/L_jj (NaN/inf iff the pivot is not > 0)
-    if (lane >= j && lane < m) ri[j] = v * r;
+    if (lane >= j && lane < mr) ri[j] = v * r;
     if (lane == j) myinv = r;
     rj += (j + 2) & ~1;
     __syncwarp();
@@ -202,6 +207,19 @@ __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv) {
   // later pivots): one vote at the end instead of a test per step
   ok = __all_sync(FULL, lane >= m || (myinv > 0.0 && myinv < INFINITY));
   return ok;
+}
+
+// z <- L^{-T} z for the chol_ll factor; z lane-owned, m <= 32.
+__device__ SR_FAST_FN double solve_bwd(const double* M, int m, int lane, double myinv, double z) {
+  const double* rj = M + rb2(m - 1) + lane;         // row j, column `lane`
+  #pragma unroll 1
+  for (int j = m - 1; j >= 0; --j) {                // backward: L^T x = y
+    if (lane == j) z *= myinv;
+    const double xj = __shfl_sync(FULL, z, j);
+    if (lane < j) z = fma(-*rj, xj, z);
+    rj -= (j + 1) & ~1;                             // padded length of row j-1
+  }
+  return z;
 }
 
 // z <- (L L^T)^{-1} z for the chol_ll factor; z lane-owned, m <= 32.
@@ -213,15 +231,7 @@ __device__ SR_FAST_FN double solve_ll(const double* M, int m, int lane, double m
     const double yj = __shfl_sync(FULL, z, j);
     if (lane > j && lane < m) z = fma(-ri[j], yj, z);
   }
-  const double* rj = M + rb2(m - 1) + lane;         // row j, column `lane`
-  #pragma unroll 1
-  for (int j = m - 1; j >= 0; --j) {                // backward: L^T x = y
-    if (lane == j) z *= myinv;
-    const double xj = __shfl_sync(FULL, z, j);
-    if (lane < j) z = fma(-*rj, xj, z);
-    rj -= (j + 1) & ~1;                             // padded length of row j-1
-  }
-  return z;
+  return solve_bwd(M, m, lane, myinv, z);
 }
 #endif
 
@@ -259,16 +269,26 @@ __device__ __forceinline__ double xrow_dot(const FastView& f, const double* xr, 
 // One fit on the fast path (m <= 32).  yc: y - ybar per training row (smem [n]).
 // Output: w' (weights on the scaled features) in wout[0..deff).
 // scratch: [n] doubles for the primal residual; uwork: [deff].
+// mcap: rows the factor buffer holds (the dual fuses the forward solve as row m when m < mcap).
 template <bool DUAL>
-__device__ bool fit_fast(const FastView& f, const double* yc, double lambda, int refine, double* Mpk,
-                         double* scratch, double* uwork, double* wout, int lane) {
+__device__ SR_FAST_FN bool fit_fast(const FastView& f, const double* yc, double lambda, int refine, double* Mpk,
+                         double* scratch, double* uwork, double* wout, int lane, int mcap) {
   const int m = DUAL ? f.n : f.deff;
   gram_fast<DUAL>(f, m, lambda, Mpk, lane);
   double myinv;
-  const bool ok = chol_ll(Mpk, m, lane, myinv);
+#if SPEEDREC_CHOL_RL
+  const bool aug = false;
+#else
+  const bool aug = DUAL && m < mcap;
+#endif
+  if (aug) {
+    if (lane < m) Mpk[rb2(m) + lane] = yc[lane];
+    __syncwarp();
+  }
+  const bool ok = chol_ll(Mpk, m, lane, myinv, aug);
   if (DUAL) {
-    double alpha = lane < f.n ? yc[lane] : 0.0;
-    alpha = solve_ll(Mpk, m, lane, myinv, alpha);
+    double alpha = lane < f.n ? (aug ? Mpk[rb2(m) + lane] : yc[lane]) : 0.0;
+    alpha = aug ? solve_bwd(Mpk, m, lane, myinv, alpha) : solve_ll(Mpk, m, lane, myinv, alpha);
     for (int it = 0; it < refine; ++it) {
       xt_alpha_lanes(f, alpha, wout, lane, scratch);
       for (int a = lane; a < f.deff; a += 32) uwork[a] = wout[a] * f.s[a];

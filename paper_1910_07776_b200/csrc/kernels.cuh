@@ -196,20 +196,17 @@ __device__ __forceinline__ double warp_max(double v) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
   return v;
 }
-__device__ __forceinline__ int warp_isum(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-  return v;
+__device__ __forceinline__ int warp_isum(int v) {   // one REDUX (sm_80+)
+  return (int)__reduce_add_sync(FULL, (unsigned)v);
 }
 __device__ __forceinline__ unsigned long long warp_usum(unsigned long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
 }
-__device__ __forceinline__ uint64_t warp_xor(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v ^= __shfl_xor_sync(FULL, v, o);
-  return v;
+__device__ __forceinline__ uint64_t warp_xor(uint64_t v) {   // two REDUX on the halves
+  const unsigned lo = __reduce_xor_sync(FULL, (unsigned)v), hi = __reduce_xor_sync(FULL, (unsigned)(v >> 32));
+  return ((uint64_t)hi << 32) | lo;
 }
 __device__ __forceinline__ bool near_tol(double a, double b, double tol) {
   double s = fabs(a) > 1.0 ? fabs(a) : 1.0;

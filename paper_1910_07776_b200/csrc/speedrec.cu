@@ -750,7 +750,7 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
 
   // ---- plan k_fit_warp ----
   // Launch-shape knobs (defaults = the tuned configuration): SPEEDREC_STAGE=0/1
-  // forces staging of x in shared memory, SPEEDREC_WMAX in {12,16,24} picks the
+  // forces staging of x in shared memory, SPEEDREC_WMAX in {12,16} picks the
   // warps-per-CTA variant, SPEEDREC_SMEM_KB caps shared memory per CTA.
   const int budget = c->max_smem_optin;                  // 232448 on B200
   const int head = align16(c->P * O);
@@ -760,7 +760,7 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   int stage = stage_bytes <= 96 * 1024 ? 1 : 0;
   if (const char* e = getenv("SPEEDREC_STAGE")) stage = atoi(e) && stage_bytes <= 96 * 1024;
   int wmax = kMaxWarpsPerBlock;
-  if (const char* e = getenv("SPEEDREC_WMAX")) wmax = atoi(e) >= 24 ? 24 : atoi(e) >= 16 ? 16 : 12;
+  if (const char* e = getenv("SPEEDREC_WMAX")) wmax = atoi(e) >= 16 ? 16 : 12;
   if (prm->learner == SR_IBK || c->coef_req) wmax = 16;   // the one IBK / sr_fit instantiation
   int budget_cap = budget;
   if (const char* e = getenv("SPEEDREC_SMEM_KB")) budget_cap = std::min(budget, std::max(16, atoi(e)) * 1024);
@@ -803,11 +803,10 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.off_stage = head;
   A.off_warps = head + (stage ? align16((int)stage_bytes) : 0);
   const int smem = A.off_warps + wpb * L.bytes;
-  auto kfit = prm->learner == SR_IBK ? k_fit_warp<16, 1>
-              : c->coef_req      ? k_fit_warp<16, 2>
-              : wmax == 24       ? k_fit_warp<24, 0>
-              : wmax == 16       ? k_fit_warp<16, 0>
-                                 : k_fit_warp<12, 0>;
+  auto kfit = prm->learner == SR_IBK ? (stage ? k_fit_warp<16, 1, true> : k_fit_warp<16, 1, false>)
+              : c->coef_req      ? (stage ? k_fit_warp<16, 2, true> : k_fit_warp<16, 2, false>)
+              : wmax == 16       ? (stage ? k_fit_warp<16, 0, true> : k_fit_warp<16, 0, false>)
+                                 : (stage ? k_fit_warp<12, 0, true> : k_fit_warp<12, 0, false>);
   CU(cudaFuncSetAttribute(kfit, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfit, wpb * 32, smem));
