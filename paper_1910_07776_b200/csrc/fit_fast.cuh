@@ -179,34 +179,46 @@ __device__ SR_FAST_FN double solve_rl(const double* M, int m, int lane, double m
 // aug: row m holds a right-hand side b (m < 32); the same column steps turn it
 // into y = L^-1 b (forward substitution fused into the factorisation).
 __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv, bool aug = false) {
-  bool ok = true;
   myinv = 0.0;
   const int mr = m + (aug ? 1 : 0);               // rows carried through the column steps
   double* ri = M + rb2(lane < mr ? lane : 0);
-  const double* rj = M;                           // row j, advanced by its padded length
+  const double* rj = M;                           // row j (j even), advanced two rows per step
+  // two columns per step: the row-prefix sums over k < j for columns j and
+  // j+1 share the loads of row i; column j+1 then takes the k = j term with
+  // L_{j+1,j} from lane j+1.  One __syncwarp per two pivots.
   #pragma unroll 1
-  for (int j = 0; j < m; ++j) {
-    double s0 = 0.0, s1 = 0.0;
-    int k = 0;
+  for (int j = 0; j < m; j += 2) {
+    const double* rj1 = j + 1 < m ? rj + j + 2 : rj;   // row j+1 (row j has padded length j+2)
+    double s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
     #pragma unroll 2
-    for (; k + 1 < j; k += 2) {
+    for (int k = 0; k < j; k += 2) {              // j even: pairs cover k < j exactly
       const double2 a = *reinterpret_cast<const double2*>(ri + k);
       const double2 b = *reinterpret_cast<const double2*>(rj + k);
+      const double2 c = *reinterpret_cast<const double2*>(rj1 + k);
       s0 = fma(a.x, b.x, s0);
       s1 = fma(a.y, b.y, s1);
+      t0 = fma(a.x, c.x, t0);
+      t1 = fma(a.y, c.y, t1);
     }
-    if (k < j) s0 = fma(ri[k], rj[k], s0);
-    const double v = ri[j] - (s0 + s1);          // lane j: pivot; lanes i > j: unscaled L_ij
+    const double2 kij = *reinterpret_cast<const double2*>(ri + j);   // K_ij, K_i,j+1 (row i >= j+1)
+    const double v = kij.x - (s0 + s1);           // lane j: pivot; lanes i > j: unscaled L_ij
     const double r = __shfl_sync(FULL, rsqrt(v), j);  // 1/L_jj (NaN/inf iff the pivot is not > 0)
-    if (lane >= j && lane < mr) ri[j] = v * r;
+    const double lij = v * r;
+    if (lane >= j && lane < mr) ri[j] = lij;
     if (lane == j) myinv = r;
-    rj += (j + 2) & ~1;
+    if (j + 1 < m) {
+      const double l1 = __shfl_sync(FULL, lij, j + 1);              // L_{j+1,j}
+      const double v1 = kij.y - (t0 + t1) - lij * l1;              // lane j+1: pivot
+      const double r1 = __shfl_sync(FULL, rsqrt(v1), j + 1);
+      if (lane > j && lane < mr) ri[j + 1] = v1 * r1;
+      if (lane == j + 1) myinv = r1;
+    }
+    rj += 2 * j + 4;                              // row j+2 (rows j, j+1 have padded length j+2)
     __syncwarp();
   }
   // a non-positive pivot makes its 1/L_jj NaN or inf (and NaN propagates to
   // later pivots): one vote at the end instead of a test per step
-  ok = __all_sync(FULL, lane >= m || (myinv > 0.0 && myinv < INFINITY));
-  return ok;
+  return __all_sync(FULL, lane >= m || (myinv > 0.0 && myinv < INFINITY));
 }
 
 // z <- L^{-T} z for the chol_ll factor; z lane-owned, m <= 32.

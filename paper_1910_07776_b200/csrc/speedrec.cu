@@ -815,7 +815,9 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   // ---- per-chunk exchange buffers (EX table, trained masks, guard counts) ----
   const int tg_stride = 32 * c->n_tg;
   const int ex_stride = c->n_os * tg_stride;
-  const long long chunk = std::max(1LL, std::min<long long>(count, (256LL << 20) / (8LL * ex_stride)));
+  long long chunk_bytes = 1024LL << 20;                 // EX table per launch (SPEEDREC_CHUNK_MB overrides; tools/sweep_c3.sh)
+  if (const char* e = getenv("SPEEDREC_CHUNK_MB")) chunk_bytes = std::max(1LL, atoll(e)) << 20;
+  const long long chunk = std::max(1LL, std::min<long long>(count, chunk_bytes / (8LL * ex_stride)));
   if ((st = ensure(c, c->extab, (size_t)chunk * ex_stride * 8)) || (st = ensure(c, c->trained, (size_t)chunk * 4)) ||
       (st = ensure(c, c->guard_acc, (size_t)chunk * 4)))
     return st;
