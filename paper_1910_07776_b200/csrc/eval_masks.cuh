@@ -197,8 +197,8 @@ __global__ void __launch_bounds__(128) k_mask_fit(const MaskArgs M) {
     const long long fidx = M.mask0 + ml;
     const uint32_t fm = mask_bits(M.sd, fidx) & (C >= 32 ? 0xFFFFFFFFu : ((1u << C) - 1u));
     int s_corr = 0, s_test = 0, s_rec = 0, s_hit = 0;
-    #pragma unroll 1
     const long long s0 = S * chunk / M.fold_chunks, s1 = S * (chunk + 1) / M.fold_chunks;
+    #pragma unroll 1
     for (long long split = s0; split < s1; ++split) {
       const long long sl = fidx * S + split - M.first;
       const uint32_t om = scored_mask(M.sd, split, O);

@@ -141,23 +141,46 @@ __device__ __forceinline__ uint64_t cta_xor(uint64_t v, uint64_t* red) {
   return s;
 }
 
-// Stage rows [r0, r0+32) of the training list into registers (thread: row
-// t>>3, features (t&7)+8q), centred and scaled; rows past n are zero.
-__device__ __forceinline__ void big_load_chunk(const double* X, int C, const int32_t* trs, int n, int r0,
-                                               const int* col, const double* xb, const double* s, int deff,
-                                               double (&v)[16]) {
-  const int r = r0 + (threadIdx.x >> 3);
+// Gather one row of a 32-row chunk into registers (thread: row t>>3,
+// features (t&7)+8q), raw values; slot < 0 (row past n) and features past
+// deff give 0.  The caller prefetches the slot index one chunk ahead, so the
+// gather issues at once and stays in flight until big_scale_chunk consumes
+// it (the L2 gather overlaps the contraction of the previous chunk).
+__device__ __forceinline__ void big_load_rows(const double* X, int C, int slot, const int* col, int deff,
+                                              double (&v)[16]) {
   const int a0 = threadIdx.x & 7;
-  const double* xr = r < n ? X + (long long)trs[r] * C : nullptr;
+  const double* xr = slot >= 0 ? X + (long long)slot * C : nullptr;
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     const int a = a0 + 8 * q;
     v[q] = (xr && a < deff) ? xr[col[a]] : 0.0;
   }
+}
+
+// 8-byte asynchronous global -> shared copy (LDGSTS); zero-fills when !valid.
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gsrc), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Training slot of this thread's row in chunk ch (-1 past n).
+__device__ __forceinline__ int big_slot(const int32_t* trs, int n, int ch) {
+  const int r = ch * kBigChunk + (threadIdx.x >> 3);
+  return r < n ? trs[r] : -1;
+}
+
+// Centre and scale a gathered chunk in registers (padding stays exactly 0).
+__device__ __forceinline__ void big_scale_chunk(int n, int r0, const double* xb, const double* s, int deff,
+                                                double (&v)[16]) {
+  const int r = r0 + (threadIdx.x >> 3);
+  const int a0 = threadIdx.x & 7;
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     const int a = a0 + 8 * q;
-    if (xr && a < deff) v[q] = (v[q] - xb[a]) * s[a];  // padding rows stay exactly 0
+    if (r < n && a < deff) v[q] = (v[q] - xb[a]) * s[a];
   }
 }
 
@@ -196,6 +219,18 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
   int32_t* trs = A.lists + blockIdx.x * A.np;
   double* yl = A.ylist + blockIdx.x * A.np;
   const int G = A.G, O = A.O, C = A.C;
+#if SPEEDREC_PHASE_TIMING
+  // instrumented build (-DSPEEDREC_PHASE_TIMING=1): cycles per phase, CTA 0 prints at exit
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ph_last = clock64();
+#define SR_PT(k)                            \
+  if (t == 0) {                             \
+    const long long now_ = clock64();       \
+    ph[k] += now_ - ph_last;                \
+    ph_last = now_;                         \
+  }
+#else
+#define SR_PT(k)
+#endif
 
   for (long long fit = blockIdx.x; fit < A.count * O; fit += gridDim.x) {
     const long long sl = fit / O;
@@ -289,157 +324,173 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       __syncthreads();
     }
     const int d = misc[0];
-    // ---- A2: min / max / sum per feature (two row halves), ybar ----
-    {
-      const int a = t & (kBigMaxD - 1), h = t >> 7;
-      double mn = INFINITY, mx = -INFINITY, sm = 0.0;
-      if (a < d) {
-        const int c = Fl[a];
-        for (int i = h; i < n; i += 2) {
-          const double vv = A.x[(long long)trs[i] * C + c];
-          mn = fmin(mn, vv);
-          mx = fmax(mx, vv);
-          sm += vv;
-        }
-      }
-      if (h == 1) {
-        zv[a] = mn;
-        wv[a] = mx;
-        rhs[a] = sm;
-      }
-      __syncthreads();
-      bool act = false;
-      if (h == 0) {
-        mn = fmin(mn, zv[a]);
-        mx = fmax(mx, wv[a]);
-        sm += rhs[a];
-        act = a < d && mx > mn;
-      }
-      const unsigned bm = __ballot_sync(FULL, act);
-      if (h == 0 && lane == 0) wsum[warp] = __popc(bm);
-      __syncthreads();
-      if (h == 0) {
-        int base = 0;
-        for (int q = 0; q < warp; ++q) base += wsum[q];
-        if (act) {
-          const int p = base + __popc(bm & ltm);
-          col[p] = Fl[a];
-          xb[p] = sm / (double)n;
-          sv[p] = 1.0 / (mx - mn);
-        }
-        if (t == 0) {
-          int de = 0;
-          for (int q = 0; q < kBigMaxD / 32; ++q) de += wsum[q];
-          misc[1] = de;
-        }
-      }
-      __syncthreads();
-    }
-    const int deff = misc[1];
+    SR_PT(0);
+    // ---- ybar, centred labels ----
     double ys = 0.0;
     for (int i = t; i < n; i += kBigThreads) ys += yl[i];
     const double ybar = cta_sum(ys, red) / (double)n;
     for (int i = t; i < n; i += kBigThreads) yl[i] -= ybar;
-    for (int a = t; a < kBigMaxD; a += kBigThreads) rhs[a] = 0.0;
     __syncthreads();
+    SR_PT(1);
 
-    // primal always (n >> d here); refinement always: the Gram's accumulation
-    // error grows with n (thousands of rows), the streamed residual removes it
+    // ---- A2 + A3 in one pass over the training rows ----
+    // Rows stream through a 3-stage cp.async ring (32 rows x all d selected
+    // features per stage) in the Gbuf region.  Per chunk, thread (feature fa,
+    // row parity fh) folds the raw values into the D3 min / max / sum of its
+    // feature and shifts them in place by c = the fit's first training row,
+    // accumulating the rhs sum_i (x_i - c) y~_i; the warps then accumulate the
+    // shifted Gram G^ = sum_i (x_i - c)(x_i - c)^T on DMMA.  After the pass:
+    // xbar, rg and the activity of D3, and the centred, scaled system
+    // G~_ab = s_a s_b (G^_ab - n (xbar_a - c_a)(xbar_b - c_b)) + lambda, exact
+    // algebra of the definition (sum_i y~_i = 0); the streamed refinement below
+    // removes the rounding.  Inactive features (rg = 0) become identity rows
+    // with s = 0, so the solution on the active ones is unchanged.
     const int nref = A.refine;
     bool ok = true;
+    const int deff = d;                   // system over the selected features
     if (deff > 0) {
-      // ---- A3: centred Gram on DMMA, chunks of 32 rows double-buffered ----
-      const int nb = (deff + 7) >> 3;
       const int I1 = warp, I2 = 15 - warp;
-      const bool has1 = I1 < nb, has2 = I2 < nb;
-      double acc1[8][2], acc2[16][2];
+      double accU[8][2], accS[8][2], accX[2] = {0.0, 0.0};
 #pragma unroll
-      for (int J = 0; J < 8; ++J) acc1[J][0] = acc1[J][1] = 0.0;
-#pragma unroll
-      for (int J = 0; J < 16; ++J) acc2[J][0] = acc2[J][1] = 0.0;
-      double rpart[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) rpart[q] = 0.0;
-      double v[16];
+      for (int J = 0; J < 8; ++J) accU[J][0] = accU[J][1] = accS[J][0] = accS[J][1] = 0.0;
+      const int fa = t & (kBigMaxD - 1), fh = t >> 7;
+      const bool fin = fa < d;
+      const double cshift = fin ? A.x[(long long)trs[0] * C + Fl[fa]] : 0.0;
+      double pmn = INFINITY, pmx = -INFINITY, psm = 0.0, prh = 0.0;
+      double* ring = Gbuf;                                  // [3][32][kBigLd]
+      double* yring = rpt;                                  // [3][32] centred labels of the stage rows
       const int nchunks = (n + kBigChunk - 1) / kBigChunk;
-      big_load_chunk(A.x, C, trs, n, 0, col, xb, sv, deff, v);
-      big_store_chunk(chunk0, v);
-      if (t < kBigChunk) ych[t] = t < n ? yl[t] : 0.0;
-      __syncthreads();
-      const int rl = lane >> 2, kl = lane & 3;
-      for (int ch = 0; ch < nchunks; ++ch) {
-        double* cur = (ch & 1) ? chunk1 : chunk0;
-        double* nxt = (ch & 1) ? chunk0 : chunk1;
-        const double* ycur = ych + (ch & 1) * kBigChunk;
-        if (ch + 1 < nchunks) big_load_chunk(A.x, C, trs, n, (ch + 1) * kBigChunk, col, xb, sv, deff, v);
-        // rhs partials from the current chunk: thread's row/features
-        {
-          const int r = t >> 3, a0 = t & 7;
-          const double yv = ycur[r];
+      const int crow = t >> 3, ca0 = t & 7;
+      // copy mapping: thread (row crow, features ca0 + 8q); rows >= n and
+      // features >= d are zero-filled
+      auto issue = [&](int ch, int slot) {
+        double* dst = ring + (ch % 3) * kBigChunk * kBigLd + crow * kBigLd + ca0;
+        const double* xr = A.x + (slot >= 0 ? (long long)slot * C : 0);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) rpart[q] = fma(cur[r * kBigLd + a0 + 8 * q], yv, rpart[q]);
+        for (int q = 0; q < 16; ++q) {
+          const int a = ca0 + 8 * q;
+          const bool ok_ = slot >= 0 && a < d;
+          cp_async8(dst + 8 * q, xr + (ok_ ? Fl[a] : 0), ok_);
         }
-#pragma unroll 2
+        if (ca0 == 0) {
+          const int r = ch * kBigChunk + crow;
+          cp_async8(yring + (ch % 3) * kBigChunk + crow, yl + (r < n ? r : 0), r < n);
+        }
+      };
+      // fold chunk cc's raw values into the statistics and shift them in
+      // place (thread: feature fa, rows fh + 2j)
+      auto shift_rows = [&](int cc, int j0, int j1) {
+        double* st = ring + (cc % 3) * kBigChunk * kBigLd;
+        const double* ys = yring + (cc % 3) * kBigChunk;
+#pragma unroll
+        for (int j = j0; j < j1; ++j) {
+          const int r = fh + 2 * j;
+          const bool live = fin && cc * kBigChunk + r < n;
+          double xv = st[r * kBigLd + fa];
+          if (live) {
+            pmn = fmin(pmn, xv);
+            pmx = fmax(pmx, xv);
+            psm += xv;
+          }
+          xv = live ? xv - cshift : 0.0;
+          if (fin) st[r * kBigLd + fa] = xv;
+          prh = fma(xv, ys[r], prh);
+        }
+      };
+      issue(0, big_slot(trs, n, 0));
+      cp_commit();
+      if (nchunks > 1) issue(1, big_slot(trs, n, 1));
+      cp_commit();
+      int slot_pf = big_slot(trs, n, 2);
+      cp_wait<1>();
+      __syncthreads();
+      shift_rows(0, 0, 16);
+      const int rl = lane >> 2, kl = lane & 3;
+      // iteration ch: contract chunk ch on DMMA while the same warps fold and
+      // shift chunk ch+1 (two rows per k-step); one barrier per chunk
+      for (int ch = 0; ch < nchunks; ++ch) {
+        cp_wait<0>();                                       // this thread's copies of chunk ch+1 landed
+        __syncthreads();                                    // chunk ch shifted, ch+1 visible, ch-1 free
+        if (ch + 2 < nchunks) {
+          issue(ch + 2, slot_pf);
+          slot_pf = big_slot(trs, n, ch + 3);
+        }
+        cp_commit();
+        const double* cur = ring + (ch % 3) * kBigChunk * kBigLd;
+        const bool nxt = ch + 1 < nchunks;
+#pragma unroll
         for (int k0 = 0; k0 < kBigChunk; k0 += 4) {
+          if (nxt) shift_rows(ch + 1, k0 / 2, k0 / 2 + 2);
           const double* base = cur + (k0 + kl) * kBigLd + rl;
           double f[16];
 #pragma unroll
-          for (int J = 0; J < 16; ++J) f[J] = (J < nb) ? base[8 * J] : 0.0;
+          for (int J = 0; J < 16; ++J) f[J] = base[8 * J];
           const double fa1 = base[8 * I1], fa2 = base[8 * I2];  // A fragments of the warp's block-rows
-          if (has1) {
 #pragma unroll
-            for (int J = 0; J < 8; ++J)
-              if (J <= I1) dmma(acc1[J][0], acc1[J][1], fa1, f[J]);
-          }
-          if (has2) {
+          for (int J = 0; J < 8; ++J) dmma(accU[J][0], accU[J][1], fa2, f[J]);
 #pragma unroll
-            for (int J = 0; J < 16; ++J)
-              if (J <= I2) dmma(acc2[J][0], acc2[J][1], fa2, f[J]);
+          for (int J = 0; J < 8; ++J) {
+            const bool lo = J <= I1;
+            dmma(accS[J][0], accS[J][1], lo ? fa1 : fa2, lo ? f[J] : f[15 - J]);
           }
+          dmma(accX[0], accX[1], fa2, fa2);
         }
-        if (ch + 1 < nchunks) {
-          big_store_chunk(nxt, v);
-          const int r = (ch + 1) * kBigChunk + t;
-          if (t < kBigChunk) ych[((ch + 1) & 1) * kBigChunk + t] = r < n ? yl[r] : 0.0;
-        }
-        __syncthreads();
       }
-      // rhs: reduce the 32 row-threads per feature in fixed order via smem (chunk buffers are free)
+      cp_wait<0>();
+      // statistics of D3 from the two row halves (fixed order), rhs, shift difference
+      if (fh == 1) {
+        zv[fa] = pmn;
+        wv[fa] = pmx;
+        rhs[fa] = psm;
+        invd[fa] = prh;
+      }
+      __syncthreads();                                      // ring consumed; Gbuf free
+      if (fh == 0) {
+        const double mn = fmin(pmn, zv[fa]), mx = fmax(pmx, wv[fa]), sm = psm + rhs[fa], rh = prh + invd[fa];
+        const bool act = fin && mx > mn;
+        const double xbar = fin ? sm / (double)n : 0.0;
+        const double sc = act ? 1.0 / (mx - mn) : 0.0;
+        col[fa] = fin ? Fl[fa] : 0;
+        xb[fa] = xbar;
+        sv[fa] = sc;
+        rhs[fa] = sc * rh;                                  // s_a sum_i (x_ia - c_a) y~_i
+        zv[fa] = xbar - cshift;                             // xbar_a - c_a
+        if (t == 0) misc[1] = 0;
+      }
+      // shifted Gram tiles -> Gbuf (lower triangle, unscaled)
       {
-        double* part = chunk0;  // [32 rows][128]
-        const int r = t >> 3, a0 = t & 7;
+        auto put = [&](int I, int J, const double (&acc)[2]) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) part[r * kBigMaxD + a0 + 8 * q] = rpart[q];
-        __syncthreads();
-        if (t < kBigMaxD) {
-          double acc = 0.0;
-          for (int rr = 0; rr < kBigChunk; ++rr) acc += part[rr * kBigMaxD + t];
-          rhs[t] = acc;
+          for (int e = 0; e < 2; ++e) {
+            const int r = I * 8 + rl, c = J * 8 + 2 * kl + e;
+            if (r < deff && c <= r) Gbuf[r * kBigGLd + c] = acc[e];
+          }
+        };
+#pragma unroll
+        for (int J = 0; J < 8; ++J) {
+          put(I2, J, accU[J]);
+          if (J <= I1) put(I1, J, accS[J]);
+          else put(I2, 15 - J, accS[J]);
         }
-        __syncthreads();
-      }
-      // tiles -> Gbuf (lower triangle, + lambda on the diagonal)
-      if (has1) {
-#pragma unroll
-        for (int J = 0; J < 8; ++J)
-          if (J <= I1)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int r = I1 * 8 + rl, c = J * 8 + 2 * kl + e;
-              if (r < deff && c <= r) Gbuf[r * kBigGLd + c] = acc1[J][e] + (r == c ? A.lambda : 0.0);
-            }
-      }
-      if (has2) {
-#pragma unroll
-        for (int J = 0; J < 16; ++J)
-          if (J <= I2)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int r = I2 * 8 + rl, c = J * 8 + 2 * kl + e;
-              if (r < deff && c <= r) Gbuf[r * kBigGLd + c] = acc2[J][e] + (r == c ? A.lambda : 0.0);
-            }
+        put(I2, I2, accX);
       }
       __syncthreads();
+      // centred, scaled system; inactive features -> identity rows
+      for (int e = t; e < deff * (deff + 1) / 2; e += kBigThreads) {
+        int r = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+        while (r * (r + 1) / 2 > e) --r;
+        while ((r + 1) * (r + 2) / 2 <= e) ++r;
+        const int c = e - r * (r + 1) / 2;
+        const double sr = sv[r], sc = sv[c];
+        double g;
+        if (sr != 0.0 && sc != 0.0)
+          g = sr * sc * (Gbuf[r * kBigGLd + c] - (double)n * zv[r] * zv[c]) + (r == c ? A.lambda : 0.0);
+        else
+          g = (r == c) ? 1.0 : 0.0;
+        Gbuf[r * kBigGLd + c] = g;
+      }
+      __syncthreads();
+      SR_PT(2);
       // ---- A4: LDL-form Cholesky (unscaled columns), CTA-wide ----
       for (int j = 0; j < deff; ++j) {
         const double djj = Gbuf[j * kBigGLd + j];
@@ -453,6 +504,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
         }
         __syncthreads();
       }
+      SR_PT(3);
       // solves by warp 0: w' = G^{-1} rhs, then refinement steps
       for (int it = 0; it <= nref; ++it) {
         if (warp == 0) {
@@ -477,6 +529,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
           for (int a = lane; a < deff; a += 32) wv[a] = (it == 0) ? zv[a] : wv[a] + zv[a];
         }
         __syncthreads();
+        SR_PT(4);
         if (it == nref) break;
         // residual r = X~^T (yc - X~ w') - lambda w' streamed over the training rows
         for (int a = t; a < kBigMaxD; a += kBigThreads) rhs[a] = 0.0;
@@ -484,7 +537,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
         // Register-only pass: thread (row t>>3, features (t&7)+8q) holds its 16
         // centred values; the row's residual is a 3-step shuffle reduction over
         // the 8 threads of the row (fixed order), next chunk prefetched.
-        double rp[16], wq[16], vn[16];
+        double rp[16], wq[16], v[16], vn[16], vnn[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           rp[q] = 0.0;
@@ -492,21 +545,40 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
           wq[q] = a < deff ? wv[a] : 0.0;
         }
         const int nch = (n + kBigChunk - 1) / kBigChunk;
-        big_load_chunk(A.x, C, trs, n, 0, col, xb, sv, deff, v);
+        const int rrow = t >> 3;
+        // gathers two chunks ahead (register ring v <- vn <- vnn), slot indices three ahead
+        int snext = big_slot(trs, n, 2);
+        double ycur = rrow < n ? yl[rrow] : 0.0, ynext = kBigChunk + rrow < n ? yl[kBigChunk + rrow] : 0.0;
+        big_load_rows(A.x, C, big_slot(trs, n, 0), col, deff, v);
+        big_load_rows(A.x, C, big_slot(trs, n, 1), col, deff, vn);
         for (int ch = 0; ch < nch; ++ch) {
-          if (ch + 1 < nch) big_load_chunk(A.x, C, trs, n, (ch + 1) * kBigChunk, col, xb, sv, deff, vn);
+          double yfut = 0.0;
+          if (ch + 2 < nch) {
+            big_load_rows(A.x, C, snext, col, deff, vnn);
+            snext = big_slot(trs, n, ch + 3);
+          }
+          {
+            const int r2 = (ch + 2) * kBigChunk + rrow;
+            yfut = r2 < n ? yl[r2] : 0.0;
+          }
+          big_scale_chunk(n, ch * kBigChunk, xb, sv, deff, v);
           double dot = 0.0;
 #pragma unroll
           for (int q = 0; q < 16; ++q) dot = fma(v[q], wq[q], dot);
           dot += __shfl_xor_sync(FULL, dot, 1);
           dot += __shfl_xor_sync(FULL, dot, 2);
           dot += __shfl_xor_sync(FULL, dot, 4);
-          const int gr = ch * kBigChunk + (t >> 3);
-          const double e = gr < n ? yl[gr] - dot : 0.0;
+          const int gr = ch * kBigChunk + rrow;
+          const double e = gr < n ? ycur - dot : 0.0;
 #pragma unroll
           for (int q = 0; q < 16; ++q) rp[q] = fma(v[q], e, rp[q]);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) v[q] = vn[q];
+          for (int q = 0; q < 16; ++q) {
+            v[q] = vn[q];
+            vn[q] = vnn[q];
+          }
+          ycur = ynext;
+          ynext = yfut;
         }
         {
           double* part = rpt;  // never aliases the factor in Gbuf
@@ -521,6 +593,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
           }
           __syncthreads();
         }
+        SR_PT(5);
       }
     }
     // ---- outputs: weights on raw counters, intercept ----
@@ -540,7 +613,13 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       A.opt_out[sl * O + o] = row;
     }
     __syncthreads();
+    SR_PT(6);
   }
+#if SPEEDREC_PHASE_TIMING
+  if (blockIdx.x == 0 && t == 0)
+    printf("k_fit_big CTA0 cycles: A1 %lld stats %lld gram %lld chol %lld solves %lld refine %lld out %lld\n", ph[0],
+           ph[1], ph[2], ph[3], ph[4], ph[5], ph[6]);
+#endif
 }
 
 // ---- A5-A7 for one scenario per CTA ----
