@@ -17,6 +17,7 @@
 
 #include "../../include/speedrec.h"
 #include "eval_masks.cuh"
+#include "eval_schur.cuh"
 #include "eval_warp.cuh"
 #include "fit_big.cuh"
 #include "kernels.cuh"
@@ -72,6 +73,12 @@ struct sr_ctx {
   DevBuf mp_G, mp_r, mp_z, mp_meta, mp_perm;
   long long sc_gen = 0, perm_key[3] = {-1, -1, -1};
   std::vector<int> perm_off;     // [kMaskMaxD + 2] start of each popcount group in mp_perm
+  unsigned mask_or = 0;          // union of the call's masks (with the perm cache)
+  // prefix-shared mask path (eval_schur.cuh): plan cached per (definition, range)
+  DevBuf mp_rec, mp_order, mp_units, mp_pfx;
+  long long splan_key[4] = {-1, -1, -1, -1};
+  int splan_groups = 0;
+  std::vector<int> splan_doff;   // [kSchurU + 2] start of each suffix-size group in mp_order
   double* coef_req = nullptr;   // set by sr_fit for the duration of its evaluate
   DevBuf extab, trained, guard_acc, mask_acc;         // fit -> rank exchange (warp path)
   // accounting
@@ -249,7 +256,9 @@ void sr_destroy(sr_ctx* c) {
                     &c->train_g, &c->test_g, &c->split_om, &c->pool_list, &c->fmasks, &c->gscratch,
                     &c->out_opt, &c->out_scn, &c->out_ex, &c->out_rec, &c->out_tot, &c->out_mask,
                     &c->out_top, &c->keys_a, &c->keys_b, &c->big_lists, &c->big_y, &c->big_U, &c->big_c0,
-                    &c->big_flag, &c->extab, &c->trained, &c->guard_acc, &c->mask_acc})
+                    &c->big_flag, &c->extab, &c->trained, &c->guard_acc, &c->mask_acc, &c->fit_coef,
+                    &c->mp_G, &c->mp_r, &c->mp_z, &c->mp_meta, &c->mp_perm, &c->mp_rec, &c->mp_order,
+                    &c->mp_units, &c->mp_pfx})
     release(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -480,6 +489,79 @@ WarpLayout plan_layout(const sr_ctx* c, int mcap, bool ibk) {
   return L;
 }
 
+// Prefix-shared mask path (eval_schur.cuh): masks sorted by
+// (suffix popcount, prefix, suffix); one Schur record per (prefix, fold, opt)
+// from k_mask_sprep; one k_mask_sfit<D> launch per suffix size D, folds split
+// over threads (integer atomics) when a launch has too few masks to fill the GPU.
+sr_status run_schur_path(sr_ctx* c, const MaskArgs& M, long long S, int T, int U, long long mask0, long long nm) {
+  sr_status st;
+  const int O = c->O;
+  const uint32_t pmask = (1u << T) - 1u, smask = (1u << U) - 1u;
+  if (c->splan_key[0] != c->sc_gen || c->splan_key[1] != mask0 || c->splan_key[2] != nm ||
+      c->splan_key[3] != (T << 8 | U)) {
+    std::vector<uint32_t> bits(nm);
+    for (long long i = 0; i < nm; ++i) {
+      const long long f = mask0 + i;
+      bits[i] = c->sc.all_subsets_k > 0 ? (uint32_t)f : (uint32_t)c->h_fmasks[2 * f];
+    }
+    auto key = [&](int32_t i) {
+      const uint32_t b = bits[i], sfx = (b >> T) & smask;
+      return ((uint64_t)__builtin_popcount(sfx) << 56) | ((uint64_t)(b & pmask) << 24) | sfx;
+    };
+    std::vector<int32_t> order(nm), group(nm);
+    for (long long i = 0; i < nm; ++i) order[i] = (int32_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return key(a) < key(b); });
+    // prefix groups: dense ids in prefix order
+    std::vector<uint32_t> pfx;
+    for (long long i = 0; i < nm; ++i) pfx.push_back(bits[i] & pmask);
+    std::sort(pfx.begin(), pfx.end());
+    pfx.erase(std::unique(pfx.begin(), pfx.end()), pfx.end());
+    for (long long i = 0; i < nm; ++i)
+      group[i] = (int32_t)(std::lower_bound(pfx.begin(), pfx.end(), bits[order[i]] & pmask) - pfx.begin());
+    c->splan_doff.assign(kSchurU + 2, 0);
+    for (long long i = 0; i < nm; ++i) ++c->splan_doff[__builtin_popcount((bits[i] >> T) & smask) + 1];
+    for (int d = 0; d <= kSchurU; ++d) c->splan_doff[d + 1] += c->splan_doff[d];
+    if ((st = ensure(c, c->mp_order, (size_t)nm * 4)) || (st = ensure(c, c->mp_units, (size_t)nm * 4)) ||
+        (st = ensure(c, c->mp_pfx, pfx.size() * 4)))
+      return st;
+    CU(cudaMemcpyAsync(c->mp_order.p, order.data(), (size_t)nm * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->mp_units.p, group.data(), (size_t)nm * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->mp_pfx.p, pfx.data(), pfx.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));   // host vectors go out of scope
+    c->splan_groups = (int)pfx.size();
+    c->splan_key[0] = c->sc_gen;
+    c->splan_key[1] = mask0;
+    c->splan_key[2] = nm;
+    c->splan_key[3] = T << 8 | U;
+  }
+  const long long nrec = (long long)c->splan_groups * S * O;
+  if ((st = ensure(c, c->mp_rec, (size_t)nrec * kRec * 8))) return st;
+  SchurArgs SA{};
+  SA.M = M;
+  SA.T = T;
+  SA.U = U;
+  SA.pfx = (const uint32_t*)c->mp_pfx.p;
+  SA.n_groups = c->splan_groups;
+  SA.rec = (double*)c->mp_rec.p;
+  SA.order = (const int32_t*)c->mp_order.p;
+  SA.group = (const int32_t*)c->mp_units.p;
+  if ((st = launch(c, "k_mask_sprep",
+                   [&] { k_mask_sprep<<<(unsigned)((nrec + 127) / 128), 128, 0, c->stream>>>(SA); })))
+    return st;
+  for (int d = 0; d <= kSchurU; ++d) {
+    const int off = c->splan_doff[d], n_it = c->splan_doff[d + 1] - off;
+    if (n_it == 0) continue;
+    const long long want = (long long)c->sm_count * 1024;
+    const int fc = (int)std::max(1LL, std::min<long long>(S, want / n_it));
+    const unsigned grid = (unsigned)(((long long)n_it * fc + kSfitThreads - 1) / kSfitThreads);
+    cudaError_t ce = cudaSuccess;
+    const sr_status s2 = launch(c, "k_mask_sfit", [&] { ce = mask_sfit_launch(d, grid, c->stream, SA, off, n_it, fc); });
+    if (ce != cudaSuccess) return fail(c, SR_E_CUDA, "k_mask_sfit<%d>: %s", d, cudaGetErrorString(ce));
+    if (s2) return s2;
+  }
+  return SR_OK;
+}
+
 // Feature-mask path: LOO batches of whole feature masks
 // (config C5).  Sets *used = false, with no side effects on the outputs,
 // when the batch is outside its regime; the warp path then runs.
@@ -499,16 +581,21 @@ sr_status run_mask_path(sr_ctx* c, const sr_params* prm, long long first, long l
   // popcount groups of the call's masks (cached per scenario definition and range)
   if (c->perm_key[0] != c->sc_gen || c->perm_key[1] != mask0 || c->perm_key[2] != nm) {
     std::vector<int> pc(nm);
+    unsigned mor = 0;
     for (long long i = 0; i < nm; ++i) {
       const long long f = mask0 + i;
       int d;
       if (c->sc.all_subsets_k > 0) {
         d = __builtin_popcountll((unsigned long long)f);
+        mor |= (unsigned)f;
       } else if (c->sc.feature_masks) {
         if (c->h_fmasks[2 * f + 1] != 0ull) return SR_OK;
-        d = __builtin_popcountll(c->h_fmasks[2 * f] & (C >= 64 ? ~0ull : ((1ull << C) - 1ull)));
+        const unsigned long long mm = c->h_fmasks[2 * f] & (C >= 64 ? ~0ull : ((1ull << C) - 1ull));
+        d = __builtin_popcountll(mm);
+        mor |= (unsigned)mm;
       } else {
         d = C;
+        mor |= C >= 32 ? 0xFFFFFFFFu : ((1u << C) - 1u);
       }
       if (d > kMaskMaxD) return SR_OK;
       pc[i] = d;
@@ -522,6 +609,7 @@ sr_status run_mask_path(sr_ctx* c, const sr_params* prm, long long first, long l
     CU(cudaMemcpyAsync(c->mp_perm.p, perm.data(), (size_t)nm * 4, cudaMemcpyHostToDevice, c->stream));
     CU(cudaStreamSynchronize(c->stream));   // perm is a stack vector
     c->perm_off = off;
+    c->mask_or = mor;
     c->perm_key[0] = c->sc_gen;
     c->perm_key[1] = mask0;
     c->perm_key[2] = nm;
@@ -574,6 +662,16 @@ sr_status run_mask_path(sr_ctx* c, const sr_params* prm, long long first, long l
   M.rec_out = A.rec_out;
   M.totals = A.totals;
   M.mask_acc = A.agg ? A.mask_acc : nullptr;
+  // prefix-shared path unless SPEEDREC_MASK_PATH=1 asks for k_mask_fit
+  int mode = 2;
+  if (const char* e = getenv("SPEEDREC_MASK_PATH")) mode = atoi(e);
+  const int K = c->mask_or ? 32 - __builtin_clz(c->mask_or) : 0;
+  const int U = std::min(kSchurU, K), T = K - U;
+  if (mode == 2 && T <= kSchurT && K <= C) {
+    if ((st = run_schur_path(c, M, S, T, U, mask0, nm))) return st;
+    *used = true;
+    return SR_OK;
+  }
   for (int d = 0; d <= kMaskMaxD; ++d) {
     const int n_it = c->perm_off[d + 1] - c->perm_off[d];
     if (n_it == 0) continue;

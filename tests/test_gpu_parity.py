@@ -75,6 +75,31 @@ def test_c5_small_masks(Context):
     print("C5k5", compare(got, ref))
 
 
+@pytest.mark.parametrize("mask_path", ["2", "1"])
+def test_c5_prefix_shared_path_explicit_masks(Context, mask_path, monkeypatch):
+    """The mask paths with masks spanning all 20 counters (prefix [0, 10) and
+    suffix [10, 20) of the prefix-shared path; "1" = the
+    per-mask k_mask_fit), an inactive counter in each half (constant rates,
+    reading D3), shared and unshared prefixes, the empty and the full mask:
+    every per-scenario field vs the oracle."""
+    monkeypatch.setenv("SPEEDREC_MASK_PATH", mask_path)
+    cfg = gen.make_config("C5", n_masks_k=1)
+    ds = cfg.dataset
+    ds.counters[:, 3] = ds.cycles * 0.125        # inactive in the prefix half
+    ds.counters[:, 14] = ds.cycles * 0.5         # inactive in the suffix half
+    rng = np.random.default_rng(11)
+    masks = [0, (1 << 20) - 1, 0x3FF, 0xFFC00, 1 << 3, 1 << 14, (1 << 14) | 1, 0x5555, 0xAAAAA]
+    masks += [int(m) for m in rng.integers(0, 1 << 20, size=24)]
+    masks += [0x155 | (int(m) << 10) for m in rng.integers(0, 1 << 10, size=8)]   # one shared prefix
+    sc = cfg.scenarios
+    sc.all_subsets_k = 0
+    sc.feature_masks = np.stack([np.array(masks, np.uint64), np.zeros(len(masks), np.uint64)], 1)
+    sc.n_masks = len(masks)
+    n = sc.n_splits * sc.n_masks
+    got, ref = _run(Context, cfg, 0, n)
+    print("C5 explicit masks path", mask_path, compare(got, ref))
+
+
 def test_c5_mask_aggregation_and_top_k(Context):
     """A7 for C5: per-mask sums over the 128 LOO folds and the mask ranking
     (sum correct desc, id asc), fused in the kernel, per-scenario rows not
