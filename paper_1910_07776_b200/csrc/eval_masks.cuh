@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(128) k_mask_fit(const MaskArgs M) {
 #pragma unroll
               for (int k = 0; k < j; ++k) djj = fma(-L[j * (j + 1) / 2 + k], L[j * (j + 1) / 2 + k], djj);
               ok &= djj > 0.0;
-              const double r = rsqrt(djj);
+              const double r = rsqrt_nr(djj);
               L[j * (j + 1) / 2 + j] = r;
 #pragma unroll
               for (int i = j + 1; i < D + 2; ++i) {

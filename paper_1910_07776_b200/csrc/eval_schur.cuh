@@ -96,7 +96,7 @@ static __global__ void __launch_bounds__(128) k_mask_sprep(const SchurArgs SA) {
     double d = L[jc + c];
     for (int k = 0; k < c; ++k) d = fma(-L[jc + k], L[jc + k], d);
     ok &= d > 0.0;
-    const double r = rsqrt(d);
+    const double r = rsqrt_nr(d);
     L[jc + c] = r;                                   // diagonal holds 1/L_cc
     for (int i = c + 1; i < p; ++i) {
       const int ji = i * (i + 1) / 2;
@@ -161,7 +161,7 @@ __device__ __forceinline__ double schur_fit(const double* R, const int* f, bool&
 #pragma unroll
     for (int k = 0; k < j; ++k) djj = fma(-L[j * (j + 1) / 2 + k], L[j * (j + 1) / 2 + k], djj);
     ok &= djj > 0.0;
-    const double r = rsqrt(djj);
+    const double r = rsqrt_nr(djj);
 #pragma unroll
     for (int i = j + 1; i < D + 2; ++i) {
       const int ri = i < D ? i * (i + 1) / 2 : TT + (i - D) * D;

@@ -82,7 +82,7 @@ __device__ bool chol_packed(double* M, double* invd, int m, int lane) {
     const double djj = M[pk(j, j)];
     __syncwarp();
     if (!(djj > 0.0)) return false;
-    const double r = rsqrt(djj);
+    const double r = rsqrt_nr(djj);
     for (int i = j + 1 + lane; i < m; i += 32) M[pk(i, j)] *= r;
     if (lane == 0) {
       M[pk(j, j)] = djj * r;

@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       for (int j = 0; j < deff; ++j) {
         const double djj = Gbuf[j * kBigGLd + j];
         if (!(djj > 0.0)) ok = false;
-        const double r = rsqrt(djj);
+        const double r = rsqrt_nr(djj);
         if (t == 0) invd[j] = r;
         const double q = r * r;
         for (int i = j + 1 + warp; i < deff; i += kBigThreads / 32) {

@@ -141,7 +141,7 @@ __device__ SR_FAST_FN bool chol_rl(double* M, int m, int lane, double& myinv) {
   for (int j = 0; j < m; ++j) {
     const double djj = M[rb2(j) + j];
     ok = ok && djj > 0.0;
-    const double r = rsqrt(djj);
+    const double r = rsqrt_nr(djj);
     if (lane == j) myinv = r;
     if (lane > j && lane < m) {
       const double sij = ri[j] * (r * r);
@@ -202,14 +202,14 @@ __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv, bo
     }
     const double2 kij = *reinterpret_cast<const double2*>(ri + j);   // K_ij, K_i,j+1 (row i >= j+1)
     const double v = kij.x - (s0 + s1);           // lane j: pivot; lanes i > j: unscaled L_ij
-    const double r = __shfl_sync(FULL, rsqrt(v), j);  // 1/L_jj (NaN/inf iff the pivot is not > 0)
+    const double r = __shfl_sync(FULL, rsqrt_nr(v), j);  // 1/L_jj (NaN/inf iff the pivot is not > 0)
     const double lij = v * r;
     if (lane >= j && lane < mr) ri[j] = lij;
     if (lane == j) myinv = r;
     if (j + 1 < m) {
       const double l1 = __shfl_sync(FULL, lij, j + 1);              // L_{j+1,j}
       const double v1 = kij.y - (t0 + t1) - lij * l1;              // lane j+1: pivot
-      const double r1 = __shfl_sync(FULL, rsqrt(v1), j + 1);
+      const double r1 = __shfl_sync(FULL, rsqrt_nr(v1), j + 1);
       if (lane > j && lane < mr) ri[j + 1] = v1 * r1;
       if (lane == j + 1) myinv = r1;
     }

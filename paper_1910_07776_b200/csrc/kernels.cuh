@@ -208,6 +208,19 @@ __device__ __forceinline__ uint64_t warp_xor(uint64_t v) {   // two REDUX on the
   const unsigned lo = __reduce_xor_sync(FULL, (unsigned)v), hi = __reduce_xor_sync(FULL, (unsigned)(v >> 32));
   return ((uint64_t)hi << 32) | lo;
 }
+// 1/sqrt(x) for a Cholesky pivot: MUFU.RSQ64H estimate + two branch-free
+// Newton steps (relative error a few ulp).  x <= 0, inf or NaN give NaN or
+// inf, which the callers' pivot checks reject; subnormal x is flushed (a
+// pivot that small never passes them either).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = fma(y, fma(-h * y, y, 0.5), y);
+  y = fma(y, fma(-h * y, y, 0.5), y);
+  return y;
+}
+
 __device__ __forceinline__ bool near_tol(double a, double b, double tol) {
   double s = fabs(a) > 1.0 ? fabs(a) : 1.0;
   return fabs(a - b) <= tol * s;
