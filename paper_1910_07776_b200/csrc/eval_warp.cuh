@@ -259,6 +259,10 @@ __device__ __forceinline__ double knn_ex(const double* __restrict__ X, int ldx, 
   return s / (double)kk;
 }
 
+template <int CMAX>
+__device__ __forceinline__ void rank_scenario(const EvalArgs& A, long long sl, int lane, bool ext_cg,
+                                              unsigned long long& tot_rec, unsigned long long& tot_hit);
+
 // ---------------------------------------------------------------- fit kernel
 // MODE 0: ridge LS (the paper's model); 1: IBK (NEXT-1); 2: ridge LS + the
 // sr_fit coefficient store.  Separate instantiations keep the hot code lean.
@@ -305,7 +309,20 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
   const long long nwarps = (long long)gridDim.x * A.warps_per_block;
   double* scr = A.gscratch ? A.gscratch + gwarp * A.mscratch : nullptr;
   const int G = A.G, O = A.O, C = A.C;
-  unsigned long long tot_corr = 0, tot_test = 0;
+  unsigned long long tot_corr = 0, tot_test = 0, tot_rec = 0, tot_hit = 0;
+  // fused A6 (A.fuse_rank): the warp finishing the last scored fit of a
+  // scenario ranks it at once, from the L2-hot EX table
+  auto finish = [&](long long sl, uint32_t om) {
+    if (MODE != 0 || !A.fuse_rank) return;
+    __threadfence();                      // this warp's EX / trained / guard writes before the count
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(&A.done[sl], 1) == __popc(om) - 1;
+    if (__shfl_sync(FULL, last, 0)) {
+      __threadfence();
+      rank_scenario<8>(A, sl, lane, true, tot_rec, tot_hit);
+    }
+  };
 
   for (long long f = gwarp; f < A.count * O; f += nwarps) {
     const long long sl = f / O;
@@ -319,6 +336,8 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
     row.fp_train = row.fp_test = 0ull;
     if (!((om >> o) & 1u)) {
       if (lane == 0 && A.opt_out) A.opt_out[so * O + o] = row;
+      // no scored optimization at all: nothing will finish, rank (empty row) here
+      if (MODE == 0 && A.fuse_rank && om == 0u && o == 0) rank_scenario<8>(A, sl, lane, true, tot_rec, tot_hit);
       continue;
     }
     const int q = __popc(om & ((1u << o) - 1u));  // scored-optimization slot in the EX table
@@ -378,7 +397,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
     if (n == 0 || nt == 0) {          // untrained (reading R18) or nothing to predict
       if (lane == 0 && A.opt_out) A.opt_out[so * O + o] = row;
       if (A.agg && lane == 0 && nt > 0) atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 1], nt);
-      tot_test += (n == 0) ? 0 : 0;
+      finish(sl, om);
       continue;
     }
 
@@ -563,10 +582,15 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
       }
     }
     __syncwarp();
+    finish(sl, om);
   }
   if (A.totals && lane == 0 && tot_test) {
     atomicAdd(&A.totals[0], tot_corr);
     atomicAdd(&A.totals[1], tot_test);
+  }
+  if (A.totals && lane == 0 && (tot_rec | tot_hit)) {
+    atomicAdd(&A.totals[2], tot_rec);
+    atomicAdd(&A.totals[3], tot_hit);
   }
 }
 
@@ -574,105 +598,114 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
 // A6: per test slot, candidates = scored, trained optimizations whose bit is
 // clear (reading R13); sort by (EX desc, id asc), keep EX >= threshold, first
 // max_count.  One warp per scenario, lanes over the slot's versions.
+// A6 + A7 (per scenario) for scenario sl of the chunk, one warp.  ext_cg:
+// the EX table, trained masks and guard counts were written by other SMs in
+// this launch (the fused path): read them from L2 (ld.global.cg).
+template <int CMAX>
+__device__ __forceinline__ void rank_scenario(const EvalArgs& A, long long sl, int lane, bool ext_cg,
+                                              unsigned long long& tot_rec, unsigned long long& tot_hit) {
+  const int G = A.G, O = A.O;
+  const long long s = A.first + sl, so = A.out0 + sl;
+  const long long split = s % A.sd.n_splits, fidx = s / A.sd.n_splits;
+  const uint32_t om = scored_mask(A.sd, split, O);
+  const uint32_t trained = ext_cg ? __ldcg(A.trained + sl) : A.trained[sl];
+  int olist[CMAX];
+  int n_os = 0;
+#pragma unroll
+  for (int q = 0; q < CMAX; ++q) olist[q] = -1;
+  {
+    uint32_t mm = om;
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q) {
+      if (mm) {
+        olist[q] = __ffs(mm) - 1;
+        mm &= mm - 1;
+        ++n_os;
+      }
+    }
+  }
+  const double* ext = A.extab + sl * A.ex_stride;
+  int nrec = 0, nhit = 0, guard = 0, untrained = 0;
+  #pragma unroll 1
+  for (int g = 0; g < G; ++g) {
+    uint64_t tr, te;
+    member_words(A.sd, split, g, tr, te);
+    if (te == 0ull) continue;
+    const int gi = test_group_index(A.sd, split, g);
+    const int p = g / A.IR;
+    for (int h = 0; h < 2; ++h) {
+      const int v = h * 32 + lane;
+      if (!((te >> v) & 1ull)) continue;
+      double ce[CMAX];
+      bool cv[CMAX], cc[CMAX];
+      int ck[CMAX];
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) {
+        const int o = olist[q];
+        int b = -1;
+        if (o >= 0) b = A.opt_bit[p * O + o];
+        bool cand = o >= 0 && b >= 0 && !((v >> b) & 1);
+        if (cand && !((trained >> o) & 1u)) {
+          ++untrained;
+          cand = false;
+        }
+        cv[q] = cand;
+        ck[q] = cand ? rmv(v, b) : 0;
+        const double* ep = ext + q * A.tg_stride + gi * 32 + ck[q];
+        const double raw = cand ? (ext_cg ? __ldcg(ep) : *ep) : 0.0;
+        cc[q] = raw < 0.0;
+        ce[q] = fabs(raw);
+      }
+      // guard band (reading R21)
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) {
+        if (!cv[q]) continue;
+        if (near_tol(ce[q], A.threshold, A.guard_tol)) ++guard;
+#pragma unroll
+        for (int r = q + 1; r < CMAX; ++r)
+          if (cv[r] && !(cc[q] && cc[r]) && near_tol(ce[q], ce[r], A.guard_tol)) ++guard;
+      }
+      // rank among candidates with EX >= threshold: (EX desc, id asc)
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) {
+        if (!cv[q] || !(ce[q] >= A.threshold)) continue;
+        int rk = 0;
+#pragma unroll
+        for (int r = 0; r < CMAX; ++r)
+          if (r != q && cv[r] && ce[r] >= A.threshold && (ce[r] > ce[q] || (ce[r] == ce[q] && r < q))) ++rk;
+        if (rk < A.max_count) {
+          ++nrec;
+          const int o = olist[q];
+          if (A.ylab[(g * O + o) * 32 + ck[q]] > 1.0) ++nhit;
+          if (A.rec_out) A.rec_out[(so * G * 64 + g * 64 + v) * A.max_count + rk] = (int8_t)o;
+        }
+      }
+    }
+  }
+  ScnScore sr;
+  sr.n_rec = warp_isum(nrec);
+  sr.n_rec_hit = warp_isum(nhit);
+  sr.n_untrained = warp_isum(untrained);
+  sr.n_guard = warp_isum(guard) + (ext_cg ? __ldcg(A.guard_acc + sl) : A.guard_acc[sl]);
+  tot_rec += sr.n_rec;
+  tot_hit += sr.n_rec_hit;
+  if (lane == 0) {
+    if (A.scn_out) A.scn_out[so] = sr;
+    if (A.agg) {
+      atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 2], sr.n_rec);
+      atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 3], sr.n_rec_hit);
+    }
+  }
+
+}
+
 template <int CMAX>
 __global__ void __launch_bounds__(256) k_rank_warp(const EvalArgs A) {
   const int lane = threadIdx.x & 31;
   const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  const int G = A.G, O = A.O;
   unsigned long long tot_rec = 0, tot_hit = 0;
-  for (long long sl = gwarp; sl < A.count; sl += nwarps) {
-    const long long s = A.first + sl, so = A.out0 + sl;
-    const long long split = s % A.sd.n_splits, fidx = s / A.sd.n_splits;
-    const uint32_t om = scored_mask(A.sd, split, O);
-    const uint32_t trained = A.trained[sl];
-    int olist[CMAX];
-    int n_os = 0;
-#pragma unroll
-    for (int q = 0; q < CMAX; ++q) olist[q] = -1;
-    {
-      uint32_t mm = om;
-#pragma unroll
-      for (int q = 0; q < CMAX; ++q) {
-        if (mm) {
-          olist[q] = __ffs(mm) - 1;
-          mm &= mm - 1;
-          ++n_os;
-        }
-      }
-    }
-    const double* ext = A.extab + sl * A.ex_stride;
-    int nrec = 0, nhit = 0, guard = 0, untrained = 0;
-    #pragma unroll 1
-    for (int g = 0; g < G; ++g) {
-      uint64_t tr, te;
-      member_words(A.sd, split, g, tr, te);
-      if (te == 0ull) continue;
-      const int gi = test_group_index(A.sd, split, g);
-      const int p = g / A.IR;
-      for (int h = 0; h < 2; ++h) {
-        const int v = h * 32 + lane;
-        if (!((te >> v) & 1ull)) continue;
-        double ce[CMAX];
-        bool cv[CMAX], cc[CMAX];
-        int ck[CMAX];
-#pragma unroll
-        for (int q = 0; q < CMAX; ++q) {
-          const int o = olist[q];
-          int b = -1;
-          if (o >= 0) b = A.opt_bit[p * O + o];
-          bool cand = o >= 0 && b >= 0 && !((v >> b) & 1);
-          if (cand && !((trained >> o) & 1u)) {
-            ++untrained;
-            cand = false;
-          }
-          cv[q] = cand;
-          ck[q] = cand ? rmv(v, b) : 0;
-          const double raw = cand ? ext[q * A.tg_stride + gi * 32 + ck[q]] : 0.0;
-          cc[q] = raw < 0.0;
-          ce[q] = fabs(raw);
-        }
-        // guard band (reading R21)
-#pragma unroll
-        for (int q = 0; q < CMAX; ++q) {
-          if (!cv[q]) continue;
-          if (near_tol(ce[q], A.threshold, A.guard_tol)) ++guard;
-#pragma unroll
-          for (int r = q + 1; r < CMAX; ++r)
-            if (cv[r] && !(cc[q] && cc[r]) && near_tol(ce[q], ce[r], A.guard_tol)) ++guard;
-        }
-        // rank among candidates with EX >= threshold: (EX desc, id asc)
-#pragma unroll
-        for (int q = 0; q < CMAX; ++q) {
-          if (!cv[q] || !(ce[q] >= A.threshold)) continue;
-          int rk = 0;
-#pragma unroll
-          for (int r = 0; r < CMAX; ++r)
-            if (r != q && cv[r] && ce[r] >= A.threshold && (ce[r] > ce[q] || (ce[r] == ce[q] && r < q))) ++rk;
-          if (rk < A.max_count) {
-            ++nrec;
-            const int o = olist[q];
-            if (A.ylab[(g * O + o) * 32 + ck[q]] > 1.0) ++nhit;
-            if (A.rec_out) A.rec_out[(so * G * 64 + g * 64 + v) * A.max_count + rk] = (int8_t)o;
-          }
-        }
-      }
-    }
-    ScnScore sr;
-    sr.n_rec = warp_isum(nrec);
-    sr.n_rec_hit = warp_isum(nhit);
-    sr.n_untrained = warp_isum(untrained);
-    sr.n_guard = warp_isum(guard) + A.guard_acc[sl];
-    tot_rec += sr.n_rec;
-    tot_hit += sr.n_rec_hit;
-    if (lane == 0) {
-      if (A.scn_out) A.scn_out[so] = sr;
-      if (A.agg) {
-        atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 2], sr.n_rec);
-        atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 3], sr.n_rec_hit);
-      }
-    }
-  }
+  for (long long sl = gwarp; sl < A.count; sl += nwarps) rank_scenario<CMAX>(A, sl, lane, false, tot_rec, tot_hit);
   if (A.totals && lane == 0 && (tot_rec | tot_hit)) {
     atomicAdd(&A.totals[2], tot_rec);
     atomicAdd(&A.totals[3], tot_hit);

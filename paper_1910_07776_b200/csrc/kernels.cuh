@@ -102,6 +102,8 @@ struct EvalArgs {
   int ex_stride, tg_stride;  // tg_stride = 32 * max test groups; ex_stride = n_os_max * tg_stride
   uint32_t* trained;     // [count] bit o set iff optimization o has >= 1 training pair
   int* guard_acc;        // [count] guard cases counted by the fit kernel
+  int* done;             // [count] scored fits finished (fused ranking)
+  int fuse_rank;         // 1: k_fit_warp ranks each scenario after its last fit (no k_rank_warp)
   // outputs (device, indexed by out0 + local scenario)
   OptScore* opt_out;     // [.][O] or null
   ScnScore* scn_out;     // or null

@@ -80,7 +80,7 @@ struct sr_ctx {
   int splan_groups = 0;
   std::vector<int> splan_doff;   // [kSchurU + 2] start of each suffix-size group in mp_order
   double* coef_req = nullptr;   // set by sr_fit for the duration of its evaluate
-  DevBuf extab, trained, guard_acc, mask_acc;         // fit -> rank exchange (warp path)
+  DevBuf extab, trained, guard_acc, mask_acc, done;   // fit -> rank exchange (warp path)
   // accounting
   bool timing = false;
   std::vector<KStat> kstats;
@@ -256,7 +256,7 @@ void sr_destroy(sr_ctx* c) {
                     &c->train_g, &c->test_g, &c->split_om, &c->pool_list, &c->fmasks, &c->gscratch,
                     &c->out_opt, &c->out_scn, &c->out_ex, &c->out_rec, &c->out_tot, &c->out_mask,
                     &c->out_top, &c->keys_a, &c->keys_b, &c->big_lists, &c->big_y, &c->big_U, &c->big_c0,
-                    &c->big_flag, &c->extab, &c->trained, &c->guard_acc, &c->mask_acc, &c->fit_coef,
+                    &c->big_flag, &c->extab, &c->trained, &c->guard_acc, &c->mask_acc, &c->done, &c->fit_coef,
                     &c->mp_G, &c->mp_r, &c->mp_z, &c->mp_meta, &c->mp_perm, &c->mp_rec, &c->mp_order,
                     &c->mp_units, &c->mp_pfx})
     release(*b);
@@ -917,13 +917,14 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   if (const char* e = getenv("SPEEDREC_CHUNK_MB")) chunk_bytes = std::max(1LL, atoll(e)) << 20;
   const long long chunk = std::max(1LL, std::min<long long>(count, chunk_bytes / (8LL * ex_stride)));
   if ((st = ensure(c, c->extab, (size_t)chunk * ex_stride * 8)) || (st = ensure(c, c->trained, (size_t)chunk * 4)) ||
-      (st = ensure(c, c->guard_acc, (size_t)chunk * 4)))
+      (st = ensure(c, c->guard_acc, (size_t)chunk * 4)) || (st = ensure(c, c->done, (size_t)chunk * 4)))
     return st;
   A.extab = (double*)c->extab.p;
   A.ex_stride = ex_stride;
   A.tg_stride = tg_stride;
   A.trained = (uint32_t*)c->trained.p;
   A.guard_acc = (int*)c->guard_acc.p;
+  A.done = (int*)c->done.p;
   A.coef_out = c->coef_req;
   const long long max_fit_blocks = (long long)c->sm_count * per_sm;
   if (mscr > 0) {
@@ -996,9 +997,17 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     A.out0 = c0;
     CU(cudaMemsetAsync(A.trained, 0, (size_t)cc * 4, c->stream));
     CU(cudaMemsetAsync(A.guard_acc, 0, (size_t)cc * 4, c->stream));
+    // fused ranking in the LS fit kernel: opt-in (SPEEDREC_FUSE_RANK=1).  Its
+    // per-fit __threadfence + cross-SM counter made the C3 step 2x slower
+    // (108 vs 56 ms), so k_rank_warp stays the default.
+    A.fuse_rank = 0;
+    if (const char* e = getenv("SPEEDREC_FUSE_RANK"))
+      A.fuse_rank = (atoi(e) != 0 && cmax == 8 && prm->learner == SR_LINREG && !c->coef_req) ? 1 : 0;
+    if (A.fuse_rank) CU(cudaMemsetAsync(A.done, 0, (size_t)cc * 4, c->stream));
     const long long fblocks = std::max(1LL, std::min(max_fit_blocks, (cc * O + wpb - 1) / wpb));
     if ((st = launch(c, "k_fit_warp", [&] { kfit<<<(unsigned)fblocks, wpb * 32, smem, c->stream>>>(A); }))) return st;
     const long long rblocks = std::max(1LL, std::min<long long>((long long)c->sm_count * 8, (cc + 7) / 8));
+    if (A.fuse_rank) continue;
     if (cmax == 8) {
       if ((st = launch(c, "k_rank_warp", [&] { k_rank_warp<8><<<(unsigned)rblocks, 256, 0, c->stream>>>(A); })))
         return st;
