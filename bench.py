@@ -328,6 +328,19 @@ def main():
     launches_per_step = max(n_dom // max(args.steps, 1), 1)
     flops_step = flops_launch                        # algorithmic flops of one step (all chunks)
     flops_launch = flops_step / launches_per_step    # chunks are equal-sized slices of the batch
+    # DRAM traffic of one launch of the dominant kernel from the committed ncu
+    # capture (profiles/traffic.json), when this run has the captured launch shape
+    traffic, traffic_note = None, None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        ent = tj.get(name_dom)
+        if ent and ent["workload"] == args.config:
+            per_launch_units = (count / launches_per_step) if name_dom != "k_mask_sfit" else None
+            if name_dom == "k_mask_sfit" or abs(per_launch_units - ent["units"]) <= 1:
+                traffic = ent["read"] + ent["write"]
+                traffic_note = f"{ent['per']}; {ent['source']}"
+    except (OSError, ValueError, KeyError):
+        pass
     clk_sum = clk.summary()
     sm_max = clk_sum.get("sm_max_mhz") or 1965.0
     props = torch.cuda.get_device_properties(dev)
@@ -398,7 +411,7 @@ def main():
             "scaling": "strong" if c5 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg, args, count),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "frac": achieved / peak if peak else None, "traffic": traffic, "traffic_note": traffic_note,
                          "kernel": name_dom, "kernel_ms": avg_dom, "kernel_share_of_step": share,
                          "flops_per_launch": flops_launch, "launches_per_step": launches_per_step,
                          "peak_note": f"FP64 (DFMA/DMMA shared pipe): {props.multi_processor_count} SMs x "

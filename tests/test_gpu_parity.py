@@ -68,6 +68,18 @@ def test_c3_small_ragged(Context):
     compare(got, ref)
 
 
+def test_fused_ranking_opt_in(Context, monkeypatch):
+    """SPEEDREC_FUSE_RANK=1: A6 run by the warp that finishes a scenario's
+    last fit (cross-SM counter + fences) instead of k_rank_warp: same rows."""
+    monkeypatch.setenv("SPEEDREC_FUSE_RANK", "1")
+    cfg = gen.make_config("C3", n_splits=1500)
+    got, ref = _run(Context, cfg, 0, 1500)
+    compare(got, ref)
+    cfg = gen.make_config("C2")
+    got, ref = _run(Context, cfg, 0, 240)
+    compare(got, ref, max_guard_frac=0.05)
+
+
 def test_c5_small_masks(Context):
     cfg = gen.make_config("C5", n_masks_k=5)        # 32 masks x 128 folds
     n = cfg.scenarios.n_scenarios
