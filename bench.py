@@ -49,9 +49,11 @@ def fit_flops(n: np.ndarray, t: np.ndarray, d: int, refine: int = 2) -> float:
     return float(2.0 * np.where(live, np.where(dual, fd, fp), 0.0).sum())
 
 
-def fit_flops_big(n: np.ndarray, t: np.ndarray, d: int, refine: int = 2) -> float:
-    """k_fit_big (C4 path, primal, always refined; prediction is in k_rank_big):
-    per fit n*d(d+1)/2 + d^3/6 + nd + d^2 + R*(2nd + d^2) FMA, flop = 2 FMA."""
+def fit_flops_big(n: np.ndarray, t: np.ndarray, d: int, refine: int = 0) -> float:
+    """k_fit_big (C4 path, primal; prediction is in k_rank_big): SURVEY 8(d)'s
+    C4 yardstick n*d(d+1)/2 + d^3/6 + nd + d^2 FMA per fit, flop = 2 FMA.  The
+    refinement passes (adaptive) are not counted: the yardstick
+    says none is needed, they are the kernel's accuracy insurance."""
     n = n.astype(np.float64)
     live = (n > 0) & (t > 0)
     f = n * d * (d + 1) / 2 + d ** 3 / 6 + n * d + d ** 2 + refine * (2 * n * d + d ** 2)

@@ -505,32 +505,71 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
         __syncthreads();
       }
       SR_PT(3);
-      // solves by warp 0: w' = G^{-1} rhs, then refinement steps
+      // solves by warp 0 (lane l owns rows l + 32s in registers, pivots by
+      // shuffle, no shared-memory round trips): w' = G^-1 rhs, then the
+      // refinement corrections.  Adaptive stop: once a correction is below
+      // 1e-8 of w' (relative, max norm), the next one would be below
+      // ~1e-16 (its size is the contraction factor kappa*eps_G times this
+      // one, and kappa*eps_G is itself at most ~ this ratio), so further
+      // passes over the data are skipped.
       for (int it = 0; it <= nref; ++it) {
         if (warp == 0) {
-          for (int a = lane; a < deff; a += 32) zv[a] = (it == 0) ? rhs[a] : zv[a];
-          __syncwarp();
-          for (int j = 0; j < deff; ++j) {
-            const double yj = zv[j] * invd[j];
-            const double tj = yj * invd[j];
-            __syncwarp();
-            if (lane == 0) zv[j] = yj;
-            for (int i = j + 1 + lane; i < deff; i += 32) zv[i] = fma(-Gbuf[i * kBigGLd + j], tj, zv[i]);
-            __syncwarp();
+          double z[4], ir[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = q * 32 + lane;
+            z[q] = r < deff ? (it == 0 ? rhs[r] : zv[r]) : 0.0;
+            ir[q] = r < deff ? invd[r] : 0.0;
           }
-          for (int j = deff - 1; j >= 0; --j) {
-            const double xj = zv[j] * invd[j];
-            __syncwarp();
-            if (lane == 0) zv[j] = xj;
-            const double tj = xj;
-            for (int i = lane; i < j; i += 32) zv[i] = fma(-Gbuf[j * kBigGLd + i] * invd[i], tj, zv[i]);
-            __syncwarp();
+#pragma unroll
+          for (int jb = 0; jb < 4; ++jb) {            // forward: L y = z
+            const int jend = min(32, deff - jb * 32);
+            for (int jj = 0; jj < jend; ++jj) {
+              const int j = jb * 32 + jj;
+              const double ij = __shfl_sync(FULL, ir[jb], jj);
+              const double yj = __shfl_sync(FULL, z[jb], jj) * ij;
+              if (lane == jj) z[jb] = yj;
+              const double tj = yj * ij;
+#pragma unroll
+              for (int q = jb; q < 4; ++q) {
+                const int r = q * 32 + lane;
+                if (r > j && r < deff) z[q] = fma(-Gbuf[r * kBigGLd + j], tj, z[q]);
+              }
+            }
           }
-          for (int a = lane; a < deff; a += 32) wv[a] = (it == 0) ? zv[a] : wv[a] + zv[a];
+#pragma unroll
+          for (int jb = 3; jb >= 0; --jb) {           // backward: L^T x = y
+            const int jend = min(32, deff - jb * 32);
+            for (int jj = jend - 1; jj >= 0; --jj) {
+              const int j = jb * 32 + jj;
+              const double xj = __shfl_sync(FULL, z[jb], jj) * __shfl_sync(FULL, ir[jb], jj);
+              if (lane == jj) z[jb] = xj;
+#pragma unroll
+              for (int q = 0; q <= jb; ++q) {
+                const int r = q * 32 + lane;
+                if (r < j) z[q] = fma(-Gbuf[j * kBigGLd + r] * ir[q], xj, z[q]);
+              }
+            }
+          }
+          double dmax = 0.0, wmax = 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = q * 32 + lane;
+            if (r < deff) {
+              zv[r] = z[q];
+              const double w = (it == 0) ? z[q] : wv[r] + z[q];
+              wv[r] = w;
+              dmax = fmax(dmax, fabs(z[q]));
+              wmax = fmax(wmax, fabs(w));
+            }
+          }
+          dmax = warp_max(dmax);
+          wmax = warp_max(wmax);
+          if (lane == 0) misc[2] = (it > 0 && dmax <= 1e-8 * wmax) ? 1 : 0;
         }
         __syncthreads();
         SR_PT(4);
-        if (it == nref) break;
+        if (it == nref || misc[2]) break;
         // residual r = X~^T (yc - X~ w') - lambda w' streamed over the training rows
         for (int a = t; a < kBigMaxD; a += kBigThreads) rhs[a] = 0.0;
         __syncthreads();
