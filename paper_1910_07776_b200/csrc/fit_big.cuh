@@ -880,4 +880,278 @@ __global__ void __launch_bounds__(kBigThreads) k_rank_big(const BigArgs A) {
   }
 }
 
+// ---- A5-A7 for kRankSB scenarios per CTA ----
+// The scenarios of a CTA share every group's 64 x C rate tile: it is staged
+// once per group in shared memory (cp.async, double-buffered, 64 KB) and
+// multiplied on DMMA by the weights of all kRankSB x 8 (scenario, scored
+// optimization) columns: warp w owns versions 8w..8w+7, 4 column tiles.  Then
+// thread (scenario t>>6, version t&63) clamps, scores and ranks its version's
+// candidates; per-scenario sums are reduced over its 64 threads in a fixed
+// order at the end.
+constexpr int kRankSB = 4;
+constexpr int kBigYO = 16;       // optimization ids a staged label block holds (O <= 16)
+
+static __global__ void __launch_bounds__(kBigThreads, 1) k_rank_big4(const BigArgs A) {
+  constexpr int CM = 8, NC = kRankSB * CM, ULD = kBigMaxD + 4, XLD = kBigMaxD + 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* Us = reinterpret_cast<double*>(smem);                 // [NC][ULD]
+  double* xs = Us + NC * ULD;                                   // [2][64][XLD]
+  double* exs = xs + 2 * 64 * XLD;                              // [64][NC + 1]
+  double* c0s = exs + 64 * (NC + 1);                            // [NC]
+  double* redd = c0s + NC;                                      // [8 warps][CM][3]
+  double* ys = redd + 8 * CM * 3;                               // [2][O][32] labels of the staged group
+  int* ols = reinterpret_cast<int*>(ys + 2 * kBigYO * 32);   // [NC]
+  int* trs_ = ols + NC;                                         // [NC] fit flags
+  int* nos = trs_ + NC;                                         // [kRankSB]
+  int* redi = nos + kRankSB;                                    // [8][CM][2]
+  int* reds = redi + 8 * CM * 2;                                // [8][4]
+  int8_t* obs = reinterpret_cast<int8_t*>(reds + 8 * 4);        // [P][O] opt bits
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int G = A.G, O = A.O, C = A.C;
+  const long long sl0 = (long long)blockIdx.x * kRankSB;
+  const int nsb = (int)(A.count - sl0 < kRankSB ? A.count - sl0 : kRankSB);
+  // weights, intercepts, scored lists
+  if (t < kRankSB) {
+    int n = 0;
+    if (t < nsb) {
+      const long long sl = sl0 + t, split = (A.first + sl) % A.n_splits;
+      const uint32_t om = (A.split_om ? A.split_om[split] : A.opt_mask) & ((1u << O) - 1u);
+      for (int o = 0; o < O && n < CM; ++o)
+        if ((om >> o) & 1u) {
+          ols[t * CM + n] = o;
+          trs_[t * CM + n] = A.fitflag[sl * O + o];
+          c0s[t * CM + n] = A.c0[sl * O + o];
+          ++n;
+        }
+    }
+    nos[t] = n;
+  }
+  for (int i = t; i < A.P * O; i += kBigThreads) obs[i] = A.opt_bit[i];
+  __syncthreads();
+  for (int i = t; i < NC * ULD; i += kBigThreads) {
+    const int col = i / ULD, c = i % ULD, sb = col / CM, q = col % CM;
+    double u = 0.0;
+    if (sb < nsb && q < nos[sb] && c < C) u = A.U[((sl0 + sb) * O + ols[sb * CM + q]) * C + c];
+    Us[i] = u;
+  }
+  for (int sb = 0; sb < nsb; ++sb) {
+    const long long sl = sl0 + sb;
+    if (A.ex_out)
+      for (int i = t; i < O * G * 32; i += kBigThreads) A.ex_out[sl * (long long)O * G * 32 + i] = 0.0;
+    if (A.rec_out)
+      for (int i = t; i < G * 64 * A.max_count; i += kBigThreads) A.rec_out[sl * (long long)G * 64 * A.max_count + i] = -1;
+  }
+  for (int i = t; i < 2 * 64 * (XLD - C); i += kBigThreads) {   // pad columns (never copied) read as 0
+    const int r = i / (XLD - C), c = C + i % (XLD - C);
+    xs[r * XLD + c] = 0.0;
+  }
+  // stage the 64 x C rate tile of group g (16-byte cp.async; C is a multiple of 2)
+  auto stage = [&](int g, int buf) {
+    const double* src = A.x + (long long)g * 64 * C;
+    double* dst = xs + buf * 64 * XLD;
+    const int per_row = C / 2;
+    for (int i = t; i < 64 * per_row; i += kBigThreads) {
+      const int r = i / per_row, c2 = (i % per_row) * 2;
+      const unsigned d = (unsigned)__cvta_generic_to_shared(dst + r * XLD + c2);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + r * C + c2) : "memory");
+    }
+    // the group's labels ylab[g][o][k] (the same for every scenario)
+    const double* ysrc = A.ylab + (long long)g * O * 32;
+    double* ydst = ys + buf * kBigYO * 32;
+    for (int i = t; i < O * 16; i += kBigThreads) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(ydst + 2 * i);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(ysrc + 2 * i) : "memory");
+    }
+    cp_commit();
+  };
+  // this thread's scenario / version and its partial scores
+  const int msb = t >> 6, v = t & 63;
+  const bool mine = msb < nsb;
+  const long long msl = sl0 + msb, msplit = (A.first + msl) % A.n_splits;
+  const int my_n = mine ? nos[msb] : 0;
+  int pc[CM], pcl[CM];
+  double ps[CM], pmn[CM], pmx[CM];
+#pragma unroll
+  for (int q = 0; q < CM; ++q) {
+    pc[q] = pcl[q] = 0;
+    ps[q] = 0.0;
+    pmn[q] = INFINITY;
+    pmx[q] = -INFINITY;
+  }
+  int nrec = 0, nhit = 0, guard = 0, untrained = 0;
+  const int rl = lane >> 2, kl = lane & 3;
+  stage(0, 0);
+  for (int g = 0; g < G; ++g) {
+    if (g + 1 < G) {
+      stage(g + 1, (g + 1) & 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();                              // tile g landed; EX tile of g-1 consumed
+    // ---- EX tile: (64 versions) x (C counters) times (C) x (NC columns) ----
+    {
+      const double* xt = xs + (g & 1) * 64 * XLD;
+      double acc[NC / 8][2];
+#pragma unroll
+      for (int nt = 0; nt < NC / 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+      const double* arow = xt + (warp * 8 + rl) * XLD + kl;
+#pragma unroll 4
+      for (int k0 = 0; k0 < C; k0 += 4) {
+        const double a = arow[k0];
+#pragma unroll
+        for (int nt = 0; nt < NC / 8; ++nt) dmma(acc[nt][0], acc[nt][1], a, Us[(nt * 8 + rl) * ULD + k0 + kl]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NC / 8; ++nt) {
+        exs[(warp * 8 + rl) * (NC + 1) + nt * 8 + 2 * kl] = acc[nt][0];
+        exs[(warp * 8 + rl) * (NC + 1) + nt * 8 + 2 * kl + 1] = acc[nt][1];
+      }
+    }
+    __syncthreads();
+    // ---- per (scenario, version): clamp, score, rank ----
+    if (mine) {
+      uint64_t tr, te;
+      member_words(A, msplit, g, tr, te);
+      if ((te >> v) & 1ull) {
+        const int p = g / A.IR;
+        double ce[CM];
+        bool cv[CM], cc[CM];
+        int ck[CM];
+#pragma unroll
+        for (int q = 0; q < CM; ++q) {
+          cv[q] = false;
+          cc[q] = false;
+          ck[q] = 0;
+          ce[q] = 0.0;
+          if (q < my_n) {
+            const int o = ols[msb * CM + q];
+            const int b = obs[p * O + o];
+            if (b >= 0 && !((v >> b) & 1)) {
+              const int fl = trs_[msb * CM + q];
+              if (fl != 1) {
+                if (fl == 0) ++untrained;
+                if (fl == 2) guard += 1000000;
+                continue;
+              }
+              const int k = rmv(v, b);
+              double e = c0s[msb * CM + q] + exs[v * (NC + 1) + msb * CM + q];
+              if (near_tol(e, 0.0, A.guard_tol) || near_tol(e, 1.0, A.guard_tol)) ++guard;
+              bool cl = false;
+              if (e <= 0.0) {
+                e = A.clamp_floor;
+                cl = true;
+              }
+              const double ac = ys[(g & 1) * kBigYO * 32 + o * 32 + k];
+              cv[q] = true;
+              cc[q] = cl;
+              ck[q] = k;
+              ce[q] = e;
+              const double ratio = ac / e;
+              pc[q] += ((e > 1.0 && ac > 1.0) || (e <= 1.0 && ac <= 1.0)) ? 1 : 0;
+              pcl[q] += cl ? 1 : 0;
+              ps[q] += ratio;
+              pmn[q] = fmin(pmn[q], ratio);
+              pmx[q] = fmax(pmx[q], ratio);
+              if (A.ex_out) A.ex_out[(msl * O + o) * (long long)G * 32 + g * 32 + k] = e;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < CM; ++q) {
+          if (!cv[q]) continue;
+          if (near_tol(ce[q], A.threshold, A.guard_tol)) ++guard;
+#pragma unroll
+          for (int r = q + 1; r < CM; ++r)
+            if (cv[r] && !(cc[q] && cc[r]) && near_tol(ce[q], ce[r], A.guard_tol)) ++guard;
+        }
+#pragma unroll
+        for (int q = 0; q < CM; ++q) {
+          if (!cv[q] || !(ce[q] >= A.threshold)) continue;
+          int rk = 0;
+#pragma unroll
+          for (int r = 0; r < CM; ++r)
+            if (r != q && cv[r] && ce[r] >= A.threshold && (ce[r] > ce[q] || (ce[r] == ce[q] && r < q))) ++rk;
+          if (rk < A.max_count) {
+            ++nrec;
+            const int o = ols[msb * CM + q];
+            if (ys[(g & 1) * kBigYO * 32 + o * 32 + ck[q]] > 1.0) ++nhit;
+            if (A.rec_out) A.rec_out[(msl * G * 64 + g * 64 + v) * A.max_count + rk] = (int8_t)o;
+          }
+        }
+      }
+    }
+  }
+  // ---- deterministic reduction per scenario: lanes (butterfly), its 2 warps in order ----
+#pragma unroll
+  for (int q = 0; q < CM; ++q) {
+    const int a = warp_isum(pc[q]), b = warp_isum(pcl[q]);
+    const double sm = warp_sum(ps[q]), mn = warp_min(pmn[q]), mx = warp_max(pmx[q]);
+    if (lane == 0) {
+      redi[(warp * CM + q) * 2 + 0] = a;
+      redi[(warp * CM + q) * 2 + 1] = b;
+      redd[(warp * CM + q) * 3 + 0] = sm;
+      redd[(warp * CM + q) * 3 + 1] = mn;
+      redd[(warp * CM + q) * 3 + 2] = mx;
+    }
+  }
+  {
+    const int a = warp_isum(nrec), b = warp_isum(nhit), c = warp_isum(untrained), d = warp_isum(guard);
+    if (lane == 0) {
+      reds[warp * 4 + 0] = a;
+      reds[warp * 4 + 1] = b;
+      reds[warp * 4 + 2] = c;
+      reds[warp * 4 + 3] = d;
+    }
+  }
+  __syncthreads();
+  if (t < nsb * CM) {
+    const int sb = t / CM, q = t % CM;
+    if (q < nos[sb]) {
+      const long long sl = sl0 + sb;
+      const int o = ols[sb * CM + q];
+      OptScore row = A.opt_out[sl * O + o];
+      int nc = 0, ncl = 0;
+      double sm = 0.0, mn = INFINITY, mx = -INFINITY;
+      for (int w = 2 * sb; w < 2 * sb + 2; ++w) {
+        nc += redi[(w * CM + q) * 2 + 0];
+        ncl += redi[(w * CM + q) * 2 + 1];
+        sm += redd[(w * CM + q) * 3 + 0];
+        mn = fmin(mn, redd[(w * CM + q) * 3 + 1]);
+        mx = fmax(mx, redd[(w * CM + q) * 3 + 2]);
+      }
+      const bool has = row.n_test > 0 && trs_[sb * CM + q] == 1;
+      row.n_correct = nc;
+      row.n_clamped = ncl;
+      row.sum_ratio = has ? sm : 0.0;
+      row.min_ratio = has ? mn : 0.0;
+      row.max_ratio = has ? mx : 0.0;
+      A.opt_out[sl * O + o] = row;
+      if (A.totals && has) {
+        atomicAdd(&A.totals[0], (unsigned long long)nc);
+        atomicAdd(&A.totals[1], (unsigned long long)row.n_test);
+      }
+    }
+  }
+  if (t < nsb) {
+    ScnScore sr{0, 0, 0, 0};
+    for (int w = 2 * t; w < 2 * t + 2; ++w) {
+      sr.n_rec += reds[w * 4 + 0];
+      sr.n_rec_hit += reds[w * 4 + 1];
+      sr.n_untrained += reds[w * 4 + 2];
+      sr.n_guard += reds[w * 4 + 3];
+    }
+    A.scn_out[sl0 + t] = sr;
+    if (A.totals) {
+      atomicAdd(&A.totals[2], (unsigned long long)sr.n_rec);
+      atomicAdd(&A.totals[3], (unsigned long long)sr.n_rec_hit);
+    }
+  }
+}
+
+// shared-memory bytes of k_rank_big4
+// (+ the [P][O] opt bits, sized at launch)
+constexpr int kRankBig4Smem = (8 * 4 * (kBigMaxD + 4) + 2 * 64 * (kBigMaxD + 4) + 64 * (8 * 4 + 1) + 8 * 4 + 8 * 8 * 3 +
+                               2 * kBigYO * 32) * 8 + (2 * 8 * 4 + 4 + 8 * 8 * 2 + 8 * 4) * 4;
+
 }  // namespace speedrec

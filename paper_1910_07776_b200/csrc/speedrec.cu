@@ -781,8 +781,19 @@ sr_status evaluate_big(sr_ctx* c, const sr_params* prm, long long first, long lo
     B.rec_out = rec ? rec + b0 * N * prm->max_count : nullptr;
     const int grid = (int)std::min<long long>(c->sm_count, bc * O);
     if ((st = launch(c, "k_fit_big", [&] { k_fit_big<<<grid, kBigThreads, smem, c->stream>>>(B); }))) return st;
-    if ((st = launch(c, "k_rank_big", [&] { k_rank_big<8><<<(unsigned)bc, kBigThreads, 0, c->stream>>>(B); })))
+    // batched ranking (kRankSB scenarios share each staged rate tile) unless
+    // C is odd (16-byte staging) or SPEEDREC_RANK_BIG=1 asks for k_rank_big
+    bool r4 = (C % 2) == 0;
+    if (const char* e = getenv("SPEEDREC_RANK_BIG")) r4 = r4 && atoi(e) != 1;
+    if (r4) {
+      const int sm4 = kRankBig4Smem + ((c->P * O + 15) & ~15);
+      CU(cudaFuncSetAttribute(k_rank_big4, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4));
+      const unsigned g4 = (unsigned)((bc + kRankSB - 1) / kRankSB);
+      if ((st = launch(c, "k_rank_big", [&] { k_rank_big4<<<g4, kBigThreads, sm4, c->stream>>>(B); })))
+        return st;
+    } else if ((st = launch(c, "k_rank_big", [&] { k_rank_big<8><<<(unsigned)bc, kBigThreads, 0, c->stream>>>(B); }))) {
       return st;
+    }
   }
   if (!out->on_device) {
     CU(cudaMemcpyAsync(out->opt_scores, opt, b_opt, cudaMemcpyDeviceToHost, c->stream));
