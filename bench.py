@@ -296,7 +296,7 @@ def main():
 
     # ---------------- roofline of the dominant kernel (FP64 ALU/DMMA bound)
     big = ds.n_groups > 64          # CTA-per-fit path (C4): prediction runs in k_rank_big
-    name_dom = "k_fit_big" if big else "k_fit_warp"
+    name_dom = ("k_ibk_dist" if args.learner == "ibk" else "k_fit_big") if big else "k_fit_warp"
     if c5:
         # n, t per (fold, opt) do not depend on the mask: take them from one
         # untimed per-scenario pass over the folds of this rank's first mask,

@@ -20,6 +20,7 @@
 #include "eval_schur.cuh"
 #include "eval_warp.cuh"
 #include "fit_big.cuh"
+#include "ibk_big.cuh"
 #include "kernels.cuh"
 
 using namespace speedrec;
@@ -68,6 +69,7 @@ struct sr_ctx {
   // scratch + outputs
   DevBuf gscratch, out_opt, out_scn, out_ex, out_rec, out_tot, out_mask, out_top, keys_a, keys_b;
   DevBuf big_lists, big_y, big_U, big_c0, big_flag;  // large-batch path (> 64 groups)
+  DevBuf ibk_lists, ibk_xs, ibk_meta;                // IBK on the large-batch path
   DevBuf fit_coef;              // sr_fit: [O][1 + C]
   // feature-mask path (eval_masks.cuh)
   DevBuf mp_G, mp_r, mp_z, mp_meta, mp_perm;
@@ -258,7 +260,7 @@ void sr_destroy(sr_ctx* c) {
                     &c->out_top, &c->keys_a, &c->keys_b, &c->big_lists, &c->big_y, &c->big_U, &c->big_c0,
                     &c->big_flag, &c->extab, &c->trained, &c->guard_acc, &c->mask_acc, &c->done, &c->fit_coef,
                     &c->mp_G, &c->mp_r, &c->mp_z, &c->mp_meta, &c->mp_perm, &c->mp_rec, &c->mp_order,
-                    &c->mp_units, &c->mp_pfx})
+                    &c->mp_units, &c->mp_pfx, &c->ibk_lists, &c->ibk_xs, &c->ibk_meta})
     release(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -692,6 +694,103 @@ sr_status run_mask_path(sr_ctx* c, const sr_params* prm, long long first, long l
   return SR_OK;
 }
 
+// IBK (NEXT-1) on the large-batch path (ibk_big.cuh): per
+// batch of scenarios k_ibk_prep (CTA per fit), k_ibk_dist (CTA per fit and
+// test-tile chunk), k_ibk_score (warp per fit), then A6 in k_rank_warp on the
+// warp path's EX-table layout.
+sr_status evaluate_big_ibk(sr_ctx* c, const sr_params* prm, long long first, long long count, BigArgs B, OptScore* opt,
+                           ScnScore* scn, double* ex, int8_t* rec, unsigned long long* tot, sr_outputs* out) {
+  const int G = c->G, O = c->O;
+  const long long N = c->N;
+  sr_status st;
+  const long long np = 32LL * G;
+  const long long batch = std::min<long long>(count, 16);
+  const long long fits = batch * O;
+  const int tg_stride = 32 * c->n_tg, ex_stride = c->n_os * tg_stride;
+  if ((st = ensure(c, c->ibk_lists, (size_t)fits * np * (4 + 8 + 4 + 4))) ||
+      (st = ensure(c, c->ibk_xs, (size_t)fits * np * kIbkLd * 8)) ||
+      (st = ensure(c, c->ibk_meta, (size_t)fits * sizeof(IbkMeta))) ||
+      (st = ensure(c, c->extab, (size_t)batch * ex_stride * 8)) || (st = ensure(c, c->trained, (size_t)batch * 4)) ||
+      (st = ensure(c, c->guard_acc, (size_t)batch * 4)))
+    return st;
+  IbkArgs I{};
+  I.B = B;
+  I.k_nn = prm->k_nn;
+  I.np = np;
+  unsigned char* lp = (unsigned char*)c->ibk_lists.p;
+  I.trs = (int32_t*)lp;
+  I.yl = (double*)(lp + (size_t)fits * np * 4);
+  I.tes = (int32_t*)(lp + (size_t)fits * np * 12);
+  I.tek = (int32_t*)(lp + (size_t)fits * np * 16);
+  I.xs = (double*)c->ibk_xs.p;
+  I.meta = (IbkMeta*)c->ibk_meta.p;
+  // test-tile chunks per fit: ~8 waves of one CTA per SM (small tail), at most one tile each
+  const long long tiles_max = (np / 2 + kIbkTT - 1) / kIbkTT;
+  I.chunks = (int)std::max(1LL, std::min<long long>(tiles_max, (8LL * c->sm_count + fits - 1) / fits));
+  EvalArgs& E = I.E;
+  E.x = B.x;
+  E.ylab = B.ylab;
+  E.opt_bit = B.opt_bit;
+  E.P = c->P;
+  E.IR = c->I * c->R;
+  E.C = c->C;
+  E.O = O;
+  E.G = G;
+  E.sd = scen_desc(c);
+  E.threshold = prm->threshold;
+  E.clamp_floor = prm->clamp_floor;
+  E.guard_tol = prm->guard_tol;
+  E.max_count = prm->max_count;
+  E.learner = prm->learner;
+  E.k_nn = prm->k_nn;
+  E.extab = (double*)c->extab.p;
+  E.ex_stride = ex_stride;
+  E.tg_stride = tg_stride;
+  E.trained = (uint32_t*)c->trained.p;
+  E.guard_acc = (int*)c->guard_acc.p;
+  E.totals = tot;
+  E.out0 = 0;
+  CU(cudaFuncSetAttribute(k_ibk_dist, cudaFuncAttributeMaxDynamicSharedMemorySize, kIbkDistSmem));
+  for (long long b0 = 0; b0 < count; b0 += batch) {
+    const long long bc = std::min(batch, count - b0);
+    I.B.first = first + b0;
+    I.B.count = bc;
+    E.first = first + b0;
+    E.count = bc;
+    E.opt_out = opt + b0 * O;
+    E.scn_out = scn + b0;
+    E.ex_out = ex ? ex + b0 * O * G * 32 : nullptr;
+    E.rec_out = rec ? rec + b0 * N * prm->max_count : nullptr;
+    if (E.ex_out) CU(cudaMemsetAsync(E.ex_out, 0, (size_t)bc * O * G * 32 * 8, c->stream));
+    if (E.rec_out) CU(cudaMemsetAsync(E.rec_out, 0xFF, (size_t)bc * N * prm->max_count, c->stream));
+    CU(cudaMemsetAsync(E.trained, 0, (size_t)bc * 4, c->stream));
+    CU(cudaMemsetAsync(E.guard_acc, 0, (size_t)bc * 4, c->stream));
+    const long long nf = bc * O;
+    if ((st = launch(c, "k_ibk_prep", [&] { k_ibk_prep<<<(unsigned)nf, kBigThreads, 0, c->stream>>>(I); })))
+      return st;
+    if ((st = launch(c, "k_ibk_dist",
+                     [&] { k_ibk_dist<<<(unsigned)(nf * I.chunks), kBigThreads, kIbkDistSmem, c->stream>>>(I); })))
+      return st;
+    if ((st = launch(c, "k_ibk_score",
+                     [&] { k_ibk_score<<<(unsigned)((nf * 32 + 255) / 256), 256, 0, c->stream>>>(I, nf); })))
+      return st;
+    const long long rblocks = std::max(1LL, std::min<long long>((long long)c->sm_count * 8, (bc + 7) / 8));
+    if ((st = launch(c, "k_rank_warp", [&] { k_rank_warp<8><<<(unsigned)rblocks, 256, 0, c->stream>>>(E); })))
+      return st;
+  }
+  if (!out->on_device) {
+    const size_t b_opt = (size_t)count * O * sizeof(sr_opt_score), b_scn = (size_t)count * sizeof(sr_scn_score);
+    const size_t b_ex = (size_t)count * O * G * 32 * 8, b_rec = (size_t)count * N * prm->max_count;
+    CU(cudaMemcpyAsync(out->opt_scores, opt, b_opt, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(out->scn_scores, scn, b_scn, cudaMemcpyDeviceToHost, c->stream));
+    if (out->ex) CU(cudaMemcpyAsync(out->ex, ex, b_ex, cudaMemcpyDeviceToHost, c->stream));
+    if (out->recs) CU(cudaMemcpyAsync(out->recs, rec, b_rec, cudaMemcpyDeviceToHost, c->stream));
+    if (out->totals) CU(cudaMemcpyAsync(out->totals, tot, 32, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+  }
+  return SR_OK;
+}
+
 // Large-batch path (> 64 groups, config C4): k_fit_big per (scenario, opt)
 // fit + k_rank_big per scenario, over scenario batches that bound the
 // per-batch weight table.
@@ -771,6 +870,7 @@ sr_status evaluate_big(sr_ctx* c, const sr_params* prm, long long first, long lo
                     16 + 8) * 8 + (2 * kBigMaxD + 2 * G + 20) * 4;
   CU(cudaFuncSetAttribute(k_fit_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (c->n_os > 8) return fail(c, SR_E_UNSUPPORTED, "evaluate: > 64 groups supports <= 8 scored optimizations");
+  if (prm->learner == SR_IBK) return evaluate_big_ibk(c, prm, first, count, B, opt, scn, ex, rec, tot, out);
   for (long long b0 = 0; b0 < count; b0 += batch) {
     const long long bc = std::min(batch, count - b0);
     B.first = first + b0;
@@ -853,7 +953,6 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   if (count == 0) return SR_OK;
   if (G > kMaxGroups) {
     if (agg) return fail(c, SR_E_UNSUPPORTED, "evaluate: mask aggregation needs <= %d groups", kMaxGroups);
-    if (prm->learner == SR_IBK) return fail(c, SR_E_UNSUPPORTED, "evaluate: IBK needs <= %d groups", kMaxGroups);
     return evaluate_big(c, prm, first, count, out);
   }
 

@@ -82,20 +82,44 @@ def test_ibk_degenerate():
     _exact(got, ref)
 
 
-def test_ibk_rejects_bad_k_and_big_path():
+def test_ibk_rejects_bad_k():
     from paper_1910_07776_b200 import Context, SpeedrecError, default_params
-    cfg = gen.make_config("C1")
-    ctx = Context(0)
-    ctx.load(cfg.dataset)
-    ctx.define_scenarios(cfg.scenarios)
-    for k in (0, 17):
-        with pytest.raises(SpeedrecError, match="k_nn"):
-            ctx.evaluate(0, 1, params=default_params(learner=1, k_nn=k))
-    ctx.close()
-    cfg = gen.make_config("C4", n_splits=2, n_programs=96)
-    ctx = Context(0)
-    ctx.load(cfg.dataset)
-    ctx.define_scenarios(cfg.scenarios)
-    with pytest.raises(SpeedrecError, match="IBK"):
-        ctx.evaluate(0, 1, params=default_params(learner=1))
-    ctx.close()
+    for name, kw in (("C1", {}), ("C4", dict(n_splits=2, n_programs=96))):
+        cfg = gen.make_config(name, **kw)
+        ctx = Context(0)
+        ctx.load(cfg.dataset)
+        ctx.define_scenarios(cfg.scenarios)
+        for k in (0, 17):
+            with pytest.raises(SpeedrecError, match="k_nn"):
+                ctx.evaluate(0, 1, params=default_params(learner=1, k_nn=k))
+        ctx.close()
+
+
+@pytest.mark.parametrize("k", [10, 3])
+def test_ibk_large_batch_path(k):
+    """IBK on the > 64-group path (k_ibk_prep / k_ibk_dist / k_ibk_score +
+    k_rank_warp): 96 programs x 64 variants x 128 counters (n ~ 770 training
+    rows, t ~ 1,540 test rows per fit, several 64-test x 32-row tiles and
+    ragged tails), 20 splits and a ragged sub-range: bit-exact."""
+    cfg = gen.make_config("C4", n_splits=20, n_programs=96)
+    got, ref = _run(cfg, 0, 20, k=k)
+    print("IBK C4 P=96 k", k, _exact(got, ref))
+    got, ref = _run(cfg, 3, 5, k=k)
+    _exact(got, ref)
+
+
+def test_ibk_large_batch_feature_mask():
+    """IBK on the large-batch path with a feature mask (d = 37 of 128, odd:
+    the last 16-byte staging pair is zero-filled) and an inactive counter."""
+    cfg = gen.make_config("C4", n_splits=6, n_programs=80)
+    ds = cfg.dataset
+    ds.counters[:, 5] = ds.cycles * 0.25                # inactive (constant rate)
+    rng = np.random.default_rng(5)
+    bits = sorted(rng.choice(128, size=36, replace=False).tolist()) + [5]
+    m0 = sum(1 << b for b in bits if b < 64)
+    m1 = sum(1 << (b - 64) for b in bits if b >= 64)
+    sc = cfg.scenarios
+    sc.feature_masks = np.array([[m0, m1]], dtype=np.uint64)
+    sc.n_masks = 1
+    got, ref = _run(cfg, 0, 6)
+    print("IBK C4 masked", _exact(got, ref))
