@@ -17,8 +17,10 @@
 //              shared memory (counter-major), 32-row training tiles
 //              double-buffered by cp.async; thread = 4 tests x 2 rows
 //              register block; per tile the 64 x 32 distances go through
-//              shared memory to the 64 owner threads' sorted top-k lists
-//              (strict <, rows in index order => ties keep the lower index).
+//              shared memory to 4 partial sorted top-k lists per test (each
+//              thread takes 8 rows of every tile; strict <, rows in index
+//              order => ties keep the lower index), merged in (D, index)
+//              order at the end of the test tile.
 //              EX -> the warp path's EX table.
 //  k_ibk_score warp per fit: per-(scenario, opt) scores (A7) in test order.
 // A6 then runs in k_rank_warp on the same EX table.
@@ -259,13 +261,16 @@ static __global__ void __launch_bounds__(kBigThreads, 1) k_ibk_dist(const IbkArg
       if (j0 + j < nt) v = (A.x[(long long)tes[j0 + j] * C + M.col[a]] - M.mn[a]) / M.rg[a];
       Ts[a * kIbkTT + j] = v;
     }
+    // partial top-k of test (t >> 2) over the rows r = 8 (t & 3) .. +7 of every
+    // tile (four lists per test, merged in (D, index) order at the end)
     double bd[kKnnMax];
     int bi[kKnnMax];
     int cnt = 0;
+    double thr = INFINITY;                     // current k-th best distance of this list
 #pragma unroll
     for (int z = 0; z < kKnnMax; ++z) {
       bd[z] = INFINITY;
-      bi[z] = 0;
+      bi[z] = 0x7FFFFFFF;
     }
     stage_rows(0, 0);
     for (int rt = 0; rt < ntile_r; ++rt) {
@@ -299,11 +304,13 @@ static __global__ void __launch_bounds__(kBigThreads, 1) k_ibk_dist(const IbkArg
         Dt[(4 * ty + i) * (kIbkTR + 1) + 2 * tx + 1] = acc[i][1];
       }
       __syncthreads();
-      if (t < kIbkTT) {                        // owner thread of test t: rows in index order
+      {                                        // 4 threads per test, 8 rows each, in index order
+        const int tt = t >> 2, r0 = 8 * (t & 3);
         const int rows = min(kIbkTR, n - rt * kIbkTR);
-        for (int r = 0; r < rows; ++r) {
-          const double D = Dt[t * (kIbkTR + 1) + r];
-          if (cnt < kk || D < bd[kk - 1]) {
+#pragma unroll
+        for (int r = r0; r < r0 + 8; ++r) {
+          const double D = Dt[tt * (kIbkTR + 1) + r];
+          if (r < rows && (cnt < kk || D < thr)) {
             int p = cnt < kk ? cnt++ : kk - 1;
             // sorted insert (registers: compile-time indices, predicated shifts)
 #pragma unroll
@@ -320,22 +327,52 @@ static __global__ void __launch_bounds__(kBigThreads, 1) k_ibk_dist(const IbkArg
                 bd[z] = D;
                 bi[z] = rt * kIbkTR + r;
               }
+#pragma unroll
+            for (int z = 0; z < kKnnMax; ++z)
+              if (z == kk - 1) thr = cnt < kk ? INFINITY : bd[z];
           }
         }
       }
       // (the next iteration's barrier protects Dt and the refilled buffer)
     }
-    if (t < kIbkTT && j0 + t < nt) {
-      double ssum = 0.0;
+    // merge the 4 partial lists of each test in (D, index) order (Ts / Rs are free)
+    __syncthreads();
+    double* MD = Ts;                                            // [256][kKnnMax] distances
+    int* MI = reinterpret_cast<int*>(Rs);                       // [256][kKnnMax] indices
 #pragma unroll
-      for (int z = 0; z < kKnnMax; ++z)
-        if (z < kk) ssum += yl[bi[z]];
+    for (int z = 0; z < kKnnMax; ++z) {
+      MD[t * kKnnMax + z] = bd[z];
+      MI[t * kKnnMax + z] = bi[z];
+    }
+    __syncthreads();
+    if (t < kIbkTT && j0 + t < nt) {
+      int h[4] = {0, 0, 0, 0};
+      double ssum = 0.0;
+      for (int z = 0; z < kk; ++z) {           // k smallest of the 4 sorted lists
+        int best = 0;
+        double bdv = INFINITY;
+        int biv = 0x7FFFFFFF;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int row = 4 * t + w;
+          const double dv = h[w] < kKnnMax ? MD[row * kKnnMax + h[w]] : INFINITY;
+          const int iv = h[w] < kKnnMax ? MI[row * kKnnMax + h[w]] : 0x7FFFFFFF;
+          if (dv < bdv || (dv == bdv && iv < biv)) {
+            bdv = dv;
+            biv = iv;
+            best = w;
+          }
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) h[w] += (w == best) ? 1 : 0;
+        ssum += yl[biv];
+      }
       const double e = ssum / (double)kk;
       const int gk = tek[j0 + t];
       const int g = gk >> 5;
       E.extab[sl * E.ex_stride + q * E.tg_stride + test_group_index(E.sd, split, g) * 32 + (gk & 31)] = e;
     }
-    __syncthreads();                           // Ts / Dt reused by the next test tile
+    __syncthreads();                           // Ts / Dt / Rs reused by the next test tile
   }
 }
 
