@@ -148,8 +148,10 @@ def knn_flops(n: np.ndarray, t: np.ndarray, d: int) -> float:
     return float(3.0 * np.where((n > 0) & (t > 0), n * t * d, 0.0).sum())
 
 
-OTHER_CONFIGS = [("C1", ["--cpu-sample", "64"]), ("C2", ["--cpu-sample", "240"]),
-                 ("C4", ["--splits", "592", "--no-cpu-baseline"]), ("C5", ["--masks-k", "20", "--cpu-sample", "2048"])]
+OTHER_CONFIGS = [("C1", "C1", ["--cpu-sample", "64"]), ("C2", "C2", ["--cpu-sample", "240"]),
+                 ("C4", "C4", ["--splits", "592", "--no-cpu-baseline"]),
+                 ("C5", "C5", ["--masks-k", "20", "--cpu-sample", "2048"]),
+                 ("C4-ibk", "C4", ["--splits", "16", "--learner", "ibk", "--no-cpu-baseline"])]
 
 
 def run_other_configs(args):
@@ -157,8 +159,8 @@ def run_other_configs(args):
     (same GPU, after the headline measurement), summarised into the headline
     JSON line under "other_configs"."""
     res = {}
-    for name, extra in OTHER_CONFIGS:
-        cmd = [sys.executable, os.path.abspath(__file__), "--config", name, "--steps", "5", "--warmup", "3",
+    for name, cname, extra in OTHER_CONFIGS:
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", cname, "--steps", "5", "--warmup", "3",
                "--no-e2e", "--no-extra", "--learner", args.learner] + extra
         try:
             out = subprocess.run(cmd, capture_output=True, text=True, timeout=600).stdout.strip().splitlines()
