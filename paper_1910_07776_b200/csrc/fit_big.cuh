@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
     }
     // ---- A1: pair counts per group, then deterministic positions ----
     uint64_t fptr = 0, fpte = 0;
+    #pragma unroll 4
     for (int g = warp; g < G; g += kBigThreads / 32) {
       const int b = A.opt_bit[(g / A.IR) * O + o];
       int ntr = 0, nte = 0;
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       // (t > 0 and n > 0 never happens here; the rank kernel needs no model)
       continue;
     }
+    #pragma unroll 4
     for (int g = warp; g < G; g += kBigThreads / 32) {
       const int b = A.opt_bit[(g / A.IR) * O + o];
       if (b < 0) continue;
