@@ -136,3 +136,35 @@ def test_fit_rejects_ibk_and_bad_state(S):
     with pytest.raises(S.SpeedrecError):
         ctx.fit(64)                                             # out of range
     ctx.close()
+
+
+@pytest.mark.gpu
+def test_tier1_ingested_dataset_end_to_end(S):
+    """NEXT-4: the C2 lattice exported to canonical CSV and ingested again
+    (paper_1910_07776_b200.tier1) gives the same batched results as the
+    generated arrays (all 240 Table-2 scenarios, bit-identical), and the
+    single-profile tool path (sr_fit -> sr_predict -> sr_recommend) runs on it."""
+    from paper_1910_07776_b200 import Context, predict, recommend
+    from paper_1910_07776_b200 import tier1 as T
+    cfg = gen.make_config("C2")
+    ds2, info = T.to_dataset(T.parse_canonical_csv(T.serialize_canonical_csv(T.dataset_to_records(cfg.dataset))))
+    outs = []
+    for ds in (cfg.dataset, ds2):
+        ctx = Context(0)
+        ctx.load(ds)
+        n = ctx.define_scenarios(cfg.scenarios)
+        outs.append(ctx.evaluate(0, n, want_ex=True, want_recs=True))
+        if ds is ds2:
+            coef = ctx.fit(0)
+            prof = ds2.counters[5]
+            ex = predict(coef, prof, float(ds2.cycles[5]))
+            rec = recommend(ex)
+            assert np.all(np.isfinite(ex[coef[:, 0] == coef[:, 0]]))
+            assert len(rec) <= 3
+        ctx.close()
+    a, b = outs
+    for k in ("ex", "recs"):
+        assert np.array_equal(a[k], b[k]), k
+    for part in ("opt", "scn"):
+        for f in a[part].dtype.names:
+            assert np.array_equal(a[part][f], b[part][f]), (part, f)
