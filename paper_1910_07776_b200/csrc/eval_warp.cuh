@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
       // two rows per pass into separate accumulators (independent min/max chains)
       double nb1 = mn1, xb1 = mx1, tb1 = 0.0, nb2 = mn2, xb2 = mx2, tb2 = 0.0;
       int i = 1;
-      #pragma unroll 1
+      SR_UNROLL(SR_UNROLL_STATS)
       for (; i + 1 < n; i += 2) {
         const double* xr = X + trs[i] * ldx;
         const double* xq = X + trs[i + 1] * ldx;
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
         const double* xr = X + (long long)tes[j] * ldx;
         double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;   // 4 independent chains
         int c = 0;
-        #pragma unroll 1
+        SR_UNROLL(SR_UNROLL_PRED)
         for (; c + 3 < C; c += 4) {
           const double2 u01 = *reinterpret_cast<const double2*>(ufull + c);
           const double2 u23 = *reinterpret_cast<const double2*>(ufull + c + 2);

@@ -70,7 +70,7 @@ __device__ SR_FAST_FN void gram_fast(const FastView& f, int m, double lambda, do
     }
   }
   const int kend = DUAL ? f.deff : f.n;
-#pragma unroll 1
+  SR_UNROLL(SR_UNROLL_GRAM)
   for (int k0 = 0; k0 < kend; k0 += 4) {
     // fragments of block-rows >= nb are never formed (warp-uniform branches)
     double fr[NB];
@@ -190,7 +190,7 @@ __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv, bo
   for (int j = 0; j < m; j += 2) {
     const double* rj1 = j + 1 < m ? rj + j + 2 : rj;   // row j+1 (row j has padded length j+2)
     double s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
-    #pragma unroll 2
+    SR_UNROLL(SR_UNROLL_CHOL)
     for (int k = 0; k < j; k += 2) {              // j even: pairs cover k < j exactly
       const double2 a = *reinterpret_cast<const double2*>(ri + k);
       const double2 b = *reinterpret_cast<const double2*>(rj + k);
@@ -258,7 +258,7 @@ __device__ SR_FAST_FN void xt_alpha_lanes(const FastView& f, double alpha, doubl
     const int c1 = f.col[a1 < f.deff ? a1 : 0], c2 = f.col[a2 < f.deff ? a2 : 0];
     const double x1 = f.xb[a1 < f.deff ? a1 : 0], x2 = f.xb[a2 < f.deff ? a2 : 0];
     double acc1 = 0.0, acc2 = 0.0;
-    #pragma unroll 2
+    SR_UNROLL(SR_UNROLL_XTA)
     for (int i = 0; i < f.n; ++i) {
       const double ai = abuf[i];
       const double* xr = f.X + f.trs[i] * f.ldx;

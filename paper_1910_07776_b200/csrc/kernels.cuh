@@ -223,6 +223,25 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return y;
 }
 
+// Unroll factors of the warp path's hot loops (A/B knobs, -DSR_UNROLL_*=n).
+#define SR_PRAGMA_(x) _Pragma(#x)
+#define SR_UNROLL(n) SR_PRAGMA_(unroll n)
+#ifndef SR_UNROLL_GRAM
+#define SR_UNROLL_GRAM 1
+#endif
+#ifndef SR_UNROLL_STATS
+#define SR_UNROLL_STATS 1
+#endif
+#ifndef SR_UNROLL_PRED
+#define SR_UNROLL_PRED 1
+#endif
+#ifndef SR_UNROLL_CHOL
+#define SR_UNROLL_CHOL 2
+#endif
+#ifndef SR_UNROLL_XTA
+#define SR_UNROLL_XTA 2
+#endif
+
 __device__ __forceinline__ bool near_tol(double a, double b, double tol) {
   double s = fabs(a) > 1.0 ? fabs(a) : 1.0;
   return fabs(a - b) <= tol * s;
