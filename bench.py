@@ -140,6 +140,43 @@ def run_reference(args, cfg, rank, world):
 LEARNERS = {"linreg": 0, "ibk": 1}
 
 
+def run_sweep(args, cfg, count):
+    """--sweep T: the Tier-3 rule sweep (sr_sweep, NEXT-3) over the config's
+    scenarios, T thresholds in [0.8, 1.4] x list lengths {1, 2, 3, 6}; one
+    step = fits + the sweep kernel.  Single GPU."""
+    import torch
+    from paper_1910_07776_b200 import Context
+    from paper_1910_07776_b200.speedrec import default_params
+    torch.cuda.set_device(0)
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    thr = np.linspace(0.8, 1.4, args.sweep)
+    cnt = np.array([1, 2, 3, 6])
+    prm = default_params(learner=LEARNERS[args.learner])
+    for _ in range(args.warmup):
+        ctx.sweep(thr, cnt, 0, count, params=prm)
+    ctx.set_timing(True)
+    ctx.reset_kernel_stats()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        rec, hit = ctx.sweep(thr, cnt, 0, count, params=prm)
+    dt = (time.perf_counter() - t0) / args.steps
+    stats = ctx.kernel_stats()
+    ctx.close()
+    i = int(np.argmin(abs(thr - 1.05)))
+    print(json.dumps({
+        "metric": "Tier-3 rule sweep: scenario evals/sec (fits + rule grid)", "value": count / dt,
+        "unit": "scenario_evals/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.description}", "scenarios": count,
+                   "thresholds": int(args.sweep), "list_lengths": cnt.tolist()},
+        "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in stats.items()},
+        "precision_at_theta_%.3f" % thr[i]: {str(int(k)): float(hit[i, j] / max(rec[i, j], 1))
+                                            for j, k in enumerate(cnt)},
+    }), flush=True)
+
+
 def knn_flops(n: np.ndarray, t: np.ndarray, d: int) -> float:
     """IBk (NEXT-1): per fit n*t*d distance terms, each a subtract and an FMA
     (3 flop); the scaling divisions and the k-best inserts are not counted."""
@@ -205,6 +242,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg (tuning runs)")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the secondary per-config lines (C1, C2, C4, C5) of the default run")
+    ap.add_argument("--sweep", type=int, default=0,
+                    help="NEXT-3: time sr_sweep with this many thresholds x 4 list lengths instead of sr_evaluate")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -219,6 +258,8 @@ def main():
 
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
+    if args.sweep:
+        return run_sweep(args, cfg, per_gpu)
 
     import torch
     from paper_1910_07776_b200 import dist as D

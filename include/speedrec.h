@@ -205,6 +205,25 @@ typedef struct {
 sr_status sr_evaluate(sr_ctx* ctx, const sr_params* params, int64_t first, int64_t count,
                       sr_outputs* out);
 
+/* Tier-3 rule sweep ("recommend the top choices
+ * if their benefit is above a preset threshold ... the user can select how
+ * many"): the fits of scenarios [first, first + count) run once (same
+ * kernels and learner as sr_evaluate); then for every test version the
+ * scored, trained candidates (R13) are ordered by (EX desc, id asc) (R10) and,
+ * for each threshold thresholds[i] and list length max_counts[j], the first
+ * min(#{EX >= thresholds[i]}, max_counts[j]) are recommended (R8, R9).
+ *   thresholds  host [n_thr], strictly ascending, finite, 1 <= n_thr <= 256
+ *   max_counts  host [n_cnt], each in [1, 16], 1 <= n_cnt <= 16
+ *   out_rec, out_hit  host int64 [n_thr][n_cnt]: recommendations made, and
+ *               those whose actual speedup AC > 1 (R11), summed over the range.
+ * params->threshold / max_count are ignored.  Warp path only (<= 64 groups;
+ * feature-mask batches run their masks on the warp path here).  Caller owns
+ * every buffer.  Errors: SR_E_ARG, SR_E_STATE, SR_E_UNSUPPORTED (> 64
+ * groups), and sr_evaluate's. */
+sr_status sr_sweep(sr_ctx* ctx, const sr_params* params, int64_t first, int64_t count, int32_t n_thr,
+                   const double* thresholds, int32_t n_cnt, const int32_t* max_counts, int64_t* out_rec,
+                   int64_t* out_hit);
+
 /* ---------------------------------------------------------------------- */
 /* Tool path: one scenario, one user profile (SPEC train_all S:282,        */
 /* predict_all S:291, rank_and_filter S:300; P:60-62 Tiers 2 and 3).        */

@@ -712,6 +712,126 @@ __global__ void __launch_bounds__(256) k_rank_warp(const EvalArgs A) {
   }
 }
 
+// ---------------------------------------------------------------- sweep
+// NEXT-3 (sr_sweep): per test version the candidates of rank_scenario,
+// sorted by (EX desc, id asc); candidate at position p with EX e is
+// recommended for (theta_i, K_j) iff p < K_j and theta_i <= e.  With u =
+// #{theta_i <= e} (thresholds ascending) that is i < u: a difference array per
+// list length, D_j[0] += 1, D_j[u] -= 1, accumulated in shared memory (integer
+// atomics: exact, order-free) and prefix-summed into the int64 totals.
+struct SweepArgs {
+  const double* thr;     // [n_thr] ascending
+  const int* cnt;        // [n_cnt]
+  int n_thr, n_cnt;
+  unsigned long long* out;   // [2][n_thr][n_cnt]: recommendations, hits
+};
+
+template <int CMAX>
+__global__ void __launch_bounds__(256) k_sweep_warp(const EvalArgs A, const SweepArgs W) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* thr = reinterpret_cast<double*>(smem);                          // [n_thr]
+  int* cnt = reinterpret_cast<int*>(thr + W.n_thr);                       // [n_cnt]
+  int* D = cnt + W.n_cnt;                                                 // [2][n_cnt][n_thr + 1]
+  const int nd = 2 * W.n_cnt * (W.n_thr + 1);
+  for (int i = threadIdx.x; i < W.n_thr; i += blockDim.x) thr[i] = W.thr[i];
+  for (int i = threadIdx.x; i < W.n_cnt; i += blockDim.x) cnt[i] = W.cnt[i];
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) D[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int G = A.G, O = A.O;
+  for (long long sl = gwarp; sl < A.count; sl += nwarps) {
+    const long long s = A.first + sl;
+    const long long split = s % A.sd.n_splits;
+    const uint32_t om = scored_mask(A.sd, split, O);
+    const uint32_t trained = A.trained[sl];
+    int olist[CMAX];
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q) olist[q] = -1;
+    {
+      uint32_t mm = om;
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q)
+        if (mm) {
+          olist[q] = __ffs(mm) - 1;
+          mm &= mm - 1;
+        }
+    }
+    const double* ext = A.extab + sl * A.ex_stride;
+    #pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+      uint64_t tr, te;
+      member_words(A.sd, split, g, tr, te);
+      if (te == 0ull) continue;
+      const int gi = test_group_index(A.sd, split, g);
+      const int p = g / A.IR;
+      for (int h = 0; h < 2; ++h) {
+        const int v = h * 32 + lane;
+        if (!((te >> v) & 1ull)) continue;
+        // candidates in id order, then a stable insertion sort on EX desc
+        double ce[CMAX];
+        int hit[CMAX];
+        int nc = 0;
+#pragma unroll
+        for (int q = 0; q < CMAX; ++q) {
+          const int o = olist[q];
+          const int b = o >= 0 ? A.opt_bit[p * O + o] : -1;
+          if (o >= 0 && b >= 0 && !((v >> b) & 1) && ((trained >> o) & 1u)) {
+            const int k = rmv(v, b);
+            ce[nc] = fabs(ext[q * A.tg_stride + gi * 32 + k]);
+            hit[nc] = A.ylab[(g * O + o) * 32 + k] > 1.0 ? 1 : 0;
+            ++nc;
+          }
+        }
+        for (int a = 1; a < nc; ++a) {
+          const double e = ce[a];
+          const int hh = hit[a];
+          int z = a;
+          while (z > 0 && ce[z - 1] < e) {     // strict: equal EX keep id order
+            ce[z] = ce[z - 1];
+            hit[z] = hit[z - 1];
+            --z;
+          }
+          ce[z] = e;
+          hit[z] = hh;
+        }
+        for (int pos = 0; pos < nc; ++pos) {
+          int lo = 0, hi = W.n_thr;               // u = #{theta <= e}
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (thr[mid] <= ce[pos]) lo = mid + 1;
+            else hi = mid;
+          }
+          if (lo == 0) break;                     // below every threshold, and so is the rest
+          for (int j = 0; j < W.n_cnt; ++j) {
+            if (pos >= cnt[j]) continue;
+            int* Dr = D + j * (W.n_thr + 1);
+            atomicAdd(Dr, 1);
+            atomicAdd(Dr + lo, -1);
+            if (hit[pos]) {
+              int* Dh = D + (W.n_cnt + j) * (W.n_thr + 1);
+              atomicAdd(Dh, 1);
+              atomicAdd(Dh + lo, -1);
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // prefix sums over thresholds -> totals
+  for (int r = threadIdx.x; r < 2 * W.n_cnt; r += blockDim.x) {
+    const int* Dr = D + r * (W.n_thr + 1);
+    const int kind = r / W.n_cnt, j = r % W.n_cnt;
+    long long run = 0;
+    for (int i = 0; i < W.n_thr; ++i) {
+      run += Dr[i];
+      if (run) atomicAdd(&W.out[((long long)kind * W.n_thr + i) * W.n_cnt + j], (unsigned long long)run);
+    }
+  }
+}
+
 // C5: per-mask rows + ranking keys (O8) from the integer accumulators.
 __global__ void k_mask_final(const EvalArgs A) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < A.n_mask_range;

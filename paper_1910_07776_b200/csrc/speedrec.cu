@@ -82,6 +82,8 @@ struct sr_ctx {
   int splan_groups = 0;
   std::vector<int> splan_doff;   // [kSchurU + 2] start of each suffix-size group in mp_order
   double* coef_req = nullptr;   // set by sr_fit for the duration of its evaluate
+  const SweepArgs* sweep = nullptr;   // set by sr_sweep for the duration of its evaluate
+  DevBuf sw_buf;
   DevBuf extab, trained, guard_acc, mask_acc, done;   // fit -> rank exchange (warp path)
   // accounting
   bool timing = false;
@@ -260,7 +262,7 @@ void sr_destroy(sr_ctx* c) {
                     &c->out_top, &c->keys_a, &c->keys_b, &c->big_lists, &c->big_y, &c->big_U, &c->big_c0,
                     &c->big_flag, &c->extab, &c->trained, &c->guard_acc, &c->mask_acc, &c->done, &c->fit_coef,
                     &c->mp_G, &c->mp_r, &c->mp_z, &c->mp_meta, &c->mp_perm, &c->mp_rec, &c->mp_order,
-                    &c->mp_units, &c->mp_pfx, &c->ibk_lists, &c->ibk_xs, &c->ibk_meta})
+                    &c->mp_units, &c->mp_pfx, &c->sw_buf, &c->ibk_lists, &c->ibk_xs, &c->ibk_meta})
     release(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -574,6 +576,7 @@ sr_status run_mask_path(sr_ctx* c, const sr_params* prm, long long first, long l
   const int O = c->O, C = c->C;
   if (const char* e = getenv("SPEEDREC_MASK_PATH"))
     if (atoi(e) == 0) return SR_OK;
+  if (c->sweep) return SR_OK;   // sr_sweep ranks on the warp path
   if (c->sc.kind != SR_SPLIT_LOO || C > kMaskMaxC || O > kMaskMaxO || prm->learner != SR_LINREG ||
       prm->debug_mcap > 0 || count <= 0 || first % S || count % S || c->sc.n_masks < 2)
     return SR_OK;
@@ -1117,6 +1120,13 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     const long long fblocks = std::max(1LL, std::min(max_fit_blocks, (cc * O + wpb - 1) / wpb));
     if ((st = launch(c, "k_fit_warp", [&] { kfit<<<(unsigned)fblocks, wpb * 32, smem, c->stream>>>(A); }))) return st;
     const long long rblocks = std::max(1LL, std::min<long long>((long long)c->sm_count * 8, (cc + 7) / 8));
+    if (c->sweep) {   // NEXT-3 rule sweep instead of the single-rule ranking
+      const SweepArgs W = *c->sweep;
+      const int sm = W.n_thr * 8 + W.n_cnt * 4 + 2 * W.n_cnt * (W.n_thr + 1) * 4;
+      if ((st = launch(c, "k_sweep_warp", [&] { k_sweep_warp<8><<<(unsigned)rblocks, 256, sm, c->stream>>>(A, W); })))
+        return st;
+      continue;
+    }
     if (A.fuse_rank) continue;
     if (cmax == 8) {
       if ((st = launch(c, "k_rank_warp", [&] { k_rank_warp<8><<<(unsigned)rblocks, 256, 0, c->stream>>>(A); })))
@@ -1192,6 +1202,61 @@ sr_status sr_rates(sr_ctx* c, double* x_out, int32_t on_device) {
 // ---------------------------------------------------------------- tool path
 // SPEC train_all / predict_all / rank_and_filter for
 // one scenario and one user profile (include/speedrec.h).
+sr_status sr_sweep(sr_ctx* c, const sr_params* prm, int64_t first, int64_t count, int32_t n_thr,
+                   const double* thresholds, int32_t n_cnt, const int32_t* max_counts, int64_t* out_rec,
+                   int64_t* out_hit) {
+  if (!c) return SR_E_ARG;
+  c->err.clear();
+  if (!prm || !thresholds || !max_counts || !out_rec || !out_hit) return fail(c, SR_E_ARG, "sweep: null pointer");
+  if (n_thr < 1 || n_thr > 256 || n_cnt < 1 || n_cnt > 16)
+    return fail(c, SR_E_ARG, "sweep: n_thr=%d (1..256), n_cnt=%d (1..16)", n_thr, n_cnt);
+  for (int i = 0; i < n_thr; ++i)
+    if (!std::isfinite(thresholds[i]) || (i > 0 && !(thresholds[i] > thresholds[i - 1])))
+      return fail(c, SR_E_ARG, "sweep: thresholds must be finite and strictly ascending (index %d)", i);
+  for (int j = 0; j < n_cnt; ++j)
+    if (max_counts[j] < 1 || max_counts[j] > 16) return fail(c, SR_E_ARG, "sweep: max_counts[%d]=%d", j, max_counts[j]);
+  if (!c->have_ds || !c->have_sc) return fail(c, SR_E_STATE, "sweep: dataset and scenarios must be defined first");
+  if (c->G > kMaxGroups) return fail(c, SR_E_UNSUPPORTED, "sweep: needs <= %d groups", kMaxGroups);
+  if (c->n_os > 8) return fail(c, SR_E_UNSUPPORTED, "sweep: needs <= 8 scored optimizations");
+  cudaSetDevice(c->device);
+  sr_status st;
+  const size_t b_out = (size_t)2 * n_thr * n_cnt * 8;
+  const size_t b = b_out + (size_t)n_thr * 8 + (size_t)n_cnt * 4;
+  if ((st = ensure(c, c->sw_buf, b))) return st;
+  unsigned char* base = (unsigned char*)c->sw_buf.p;
+  SweepArgs W{};
+  W.out = (unsigned long long*)base;
+  W.thr = (const double*)(base + b_out);
+  W.cnt = (const int*)(base + b_out + (size_t)n_thr * 8);
+  W.n_thr = n_thr;
+  W.n_cnt = n_cnt;
+  CU(cudaMemsetAsync(base, 0, b_out, c->stream));
+  CU(cudaMemcpyAsync(base + b_out, thresholds, (size_t)n_thr * 8, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(base + b_out + (size_t)n_thr * 8, max_counts, (size_t)n_cnt * 4, cudaMemcpyHostToDevice,
+                     c->stream));
+  // per-scenario rows land in device scratch (not returned)
+  const int O = c->O;
+  if ((st = ensure(c, c->out_opt, (size_t)count * O * sizeof(sr_opt_score))) ||
+      (st = ensure(c, c->out_scn, (size_t)count * sizeof(sr_scn_score))))
+    return st;
+  sr_outputs o{};
+  o.opt_scores = (sr_opt_score*)c->out_opt.p;
+  o.scn_scores = (sr_scn_score*)c->out_scn.p;
+  o.on_device = 1;
+  c->sweep = &W;
+  st = sr_evaluate(c, prm, first, count, &o);
+  c->sweep = nullptr;
+  if (st) return st;
+  std::vector<unsigned long long> h((size_t)2 * n_thr * n_cnt);
+  CU(cudaMemcpyAsync(h.data(), W.out, b_out, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (size_t i = 0; i < (size_t)n_thr * n_cnt; ++i) {
+    out_rec[i] = (int64_t)h[i];
+    out_hit[i] = (int64_t)h[(size_t)n_thr * n_cnt + i];
+  }
+  return SR_OK;
+}
+
 sr_status sr_fit(sr_ctx* c, const sr_params* prm, int64_t scenario, double* coef_out) {
   if (!c) return SR_E_ARG;
   c->err.clear();

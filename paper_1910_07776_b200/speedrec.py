@@ -72,7 +72,7 @@ MASK_SCORE_DTYPE = np.dtype([("n_correct", "<i4"), ("n_test", "<i4"), ("n_rec", 
 EXPORTS = ["sr_create", "sr_destroy", "sr_last_error", "sr_version", "sr_load_dataset",
            "sr_define_scenarios", "sr_default_params", "sr_evaluate", "sr_rates", "sr_synchronize",
            "sr_set_timing", "sr_kernel_stats", "sr_reset_kernel_stats", "sr_last_launch_count",
-           "sr_fit", "sr_predict", "sr_recommend"]
+           "sr_fit", "sr_predict", "sr_recommend", "sr_sweep"]
 
 _lib = None
 
@@ -114,6 +114,9 @@ def lib() -> ct.CDLL:
         L.sr_last_launch_count.argtypes = [ct.c_void_p]
         L.sr_last_launch_count.restype = ct.c_int32
         L.sr_fit.argtypes = [ct.c_void_p, ct.POINTER(sr_params), ct.c_int64, ct.c_void_p]
+        L.sr_sweep.argtypes = [ct.c_void_p, ct.POINTER(sr_params), ct.c_int64, ct.c_int64, ct.c_int32, ct.c_void_p,
+                               ct.c_int32, ct.c_void_p, ct.c_void_p, ct.c_void_p]
+        L.sr_sweep.restype = ct.c_int32
         L.sr_fit.restype = ct.c_int32
         L.sr_predict.argtypes = [ct.POINTER(sr_params), ct.c_void_p, ct.c_int32, ct.c_int32, ct.c_void_p,
                                  ct.c_double, ct.c_void_p]
@@ -247,6 +250,21 @@ class Context:
                        _ptr(out.get("totals")), _ptr(out.get("masks")), _ptr(out.get("top")), 1)
         self._check(lib().sr_evaluate(self._h, ct.byref(p), first, count, ct.byref(o)))
         return out
+
+    def sweep(self, thresholds, max_counts, first: int = 0, count: Optional[int] = None,
+              params: Optional[sr_params] = None):
+        """sr_sweep (NEXT-3): pooled (recommendations, hits) [n_thr][n_cnt] of the
+        Tier-3 rule for every (threshold, list length) over scenarios [first, first+count)."""
+        thr = np.ascontiguousarray(thresholds, dtype=np.float64)
+        cnt = np.ascontiguousarray(max_counts, dtype=np.int32)
+        if count is None:
+            count = self.n_scenarios - first
+        rec = np.zeros((len(thr), len(cnt)), dtype=np.int64)
+        hit = np.zeros_like(rec)
+        p = params or default_params()
+        self._check(lib().sr_sweep(self._h, ct.byref(p), int(first), int(count), len(thr), _ptr(thr), len(cnt),
+                                   _ptr(cnt), _ptr(rec), _ptr(hit)))
+        return rec, hit
 
     def fit(self, scenario: int, params: Optional[sr_params] = None) -> np.ndarray:
         """sr_fit: [O][1 + C] raw-counter models (c0, u) of one scenario; NaN c0 = no model."""
