@@ -72,7 +72,7 @@ def table2_scenarios(ds: Dataset, opt_names) -> Scenarios:
     Order: Exp 1..6, then loops in the order written above (reading R15).
     """
     P, I, R = ds.n_programs, ds.n_inputs, ds.n_runs
-    assert P == 2
+    assert P in (1, 2)          # 1: BH alone (config BH6, Exp 1-4)
     G = P * I * R
     W = (G + 63) // 64
     gid = lambda p, i, r: (p * I + i) * R + r
@@ -104,7 +104,7 @@ def table2_scenarios(ds: Dataset, opt_names) -> Scenarios:
                     continue
                 for r2 in range(R):
                     rows.append(([gid(p, i, rr) for rr in range(R)], [gid(p, i2, r2)], prog_mask[p], 4))
-    for ptrain, ptest, e in ((0, 1, 5), (1, 0, 6)):
+    for ptrain, ptest, e in (((0, 1, 5), (1, 0, 6)) if P == 2 else ()):
         for i in range(I):
             for i2 in range(I):
                 for r2 in range(R):
@@ -126,7 +126,7 @@ def table2_scenarios(ds: Dataset, opt_names) -> Scenarios:
 def make_config(name: str, n_splits: Optional[int] = None, n_masks_k: Optional[int] = None,
                 n_programs: Optional[int] = None) -> Config:
     """Build config C1..C5; optional overrides shrink it for tests."""
-    c = int(name[1])
+    c = int(name[1]) if name[1].isdigit() else 6
     dseed, sseed = 1910 + c, 7776 + c
     if name == "C1":
         ds = generate(n_programs=1, n_inputs=1, n_runs=1, n_counters=32, seed=dseed,
@@ -141,6 +141,13 @@ def make_config(name: str, n_splits: Optional[int] = None, n_masks_k: Optional[i
                       input_sizes=[TABLE1["BH"][:4], TABLE1["NB"]], small_opt="FTZ")
         sc = table2_scenarios(ds, OPT_NAMES_C2)
         desc = "BH+NB x 4 inputs x 3 runs x 64 variants, 32 counters, all 240 Table-2 instantiations"
+    elif name == "BH6":
+        # NEXT-3: Barnes-Hut with all six Table-1 inputs, Table-2 Exp 1-4
+        ds = generate(n_programs=1, n_inputs=6, n_runs=3, n_counters=32, seed=1910 + 6,
+                      opt_names=OPT_NAMES_C2, program_opts=[BH_OPTS], program_names=["BH"],
+                      input_sizes=[TABLE1["BH"]], small_opt="FTZ")
+        sc = table2_scenarios(ds, OPT_NAMES_C2)
+        desc = "BH x 6 inputs (Table 1) x 3 runs x 64 variants, 32 counters, Table-2 Exp 1-4 (144)"
     elif name == "C3":
         ds = generate(n_programs=2, n_inputs=1, n_runs=1, n_counters=64, seed=dseed,
                       opt_names=GENERIC_OPTS, program_opts=[GENERIC_OPTS, GENERIC_OPTS],

@@ -313,3 +313,23 @@ def test_errors_name_the_entity(Context):
     r = ctx.evaluate(0, 0)                           # empty batch is valid
     assert r["opt"].shape[0] == 0
     ctx.close()
+
+
+def test_bh6_all_table2_and_strip_chart(Context):
+    """NEXT-3: Barnes-Hut with all six Table-1 inputs (144 Exp 1-4
+    scenarios) vs the oracle, and the strip-chart rows (report.ratio_rows)
+    of the GPU result against the oracle's, case by case."""
+    from paper_1910_07776_b200 import report
+    from tests.parity import rel_err
+    cfg = gen.make_config("BH6")
+    got, ref = _run(Context, cfg, 0, 144)
+    print("BH6", compare(got, ref, max_guard_frac=0.05))
+    guarded = ref["scn"]["n_guard"] != 0
+    exp = cfg.scenarios.experiment
+    g_rows = report.ratio_rows(cfg.dataset, got, exp)
+    r_rows = report.ratio_rows(cfg.dataset, ref, exp)
+    assert len(g_rows) == len(r_rows)
+    for a, b in zip(g_rows, r_rows):
+        assert {k: a[k] for k in a if k != "ratio"} == {k: b[k] for k in b if k != "ratio"}
+    e = rel_err(np.array([a["ratio"] for a in g_rows]), np.array([b["ratio"] for b in r_rows]))
+    assert guarded.any() or e.max() <= 1e-9
