@@ -104,6 +104,52 @@ def parse_canonical_csv(text: str) -> list:
     return out
 
 
+def import_nvprof_csv(text: str, program: str, input_id: str, run_id: int, version_mask: int,
+                      runtime_ms: float | None = None, kernel: str | None = None,
+                      cycles_event: str = "elapsed_cycles_sm") -> list:
+    """Best-effort import of an nvprof event / metric CSV export (SPEC S:56-63,
+    P:175 "nvprof from the Visual Profiler"): `==` comment lines skipped; a
+    header row with a "Kernel" column and a value column (Avg preferred, else
+    Value / Max); one Record per kernel with the caller's identity labels.
+    `cycles_event` names the cycle counter (stored as elapsed_cycles); the
+    runtime comes from `runtime_ms` (nvprof's event export has none).
+    Errors: no recognizable header -> Tier1Error; missing cycles -> incomplete."""
+    rows = [r for r in csv.reader(io.StringIO(text)) if r and not r[0].lstrip().startswith("==")]
+    hdr_i = next((i for i, r in enumerate(rows) if any(c.strip() == "Kernel" for c in r)), None)
+    if hdr_i is None:
+        raise Tier1Error("nvprof: no header row with a Kernel column")
+    hdr = [c.strip() for c in rows[hdr_i]]
+    k_col = hdr.index("Kernel")
+    n_col = next((hdr.index(h) for h in ("Event Name", "Metric Name") if h in hdr), None)
+    v_col = next((hdr.index(h) for h in ("Avg", "Value", "Max") if h in hdr), None)
+    if n_col is None or v_col is None:
+        raise Tier1Error("nvprof: header lacks an event/metric name or value column")
+    recs: dict = {}
+    for ln, r in enumerate(rows[hdr_i + 1:], start=hdr_i + 2):
+        if len(r) <= max(k_col, n_col, v_col):
+            continue
+        kern = r[k_col].strip()
+        if kernel is not None and kern != kernel:
+            continue
+        name, val = r[n_col].strip(), r[v_col].strip().rstrip("%")
+        try:
+            v = float(val)
+        except ValueError:
+            raise Tier1Error(f"nvprof line {ln}: non-numeric value {val!r}") from None
+        rec = recs.setdefault(kern, Record(program, input_id, int(run_id), int(version_mask), kern))
+        if name == cycles_event:
+            rec.cycles = v
+        else:
+            rec.counters[name] = v
+    out = list(recs.values())
+    for r in out:
+        if runtime_ms is not None:
+            r.runtime = float(runtime_ms)
+        if math.isnan(r.cycles):
+            raise Tier1Error(f"incomplete record {r.key}: no {cycles_event} event")
+    return out
+
+
 def serialize_canonical_csv(records) -> str:
     """Canonical CSV of the records (counters in name order, then the two
     reserved rows); repr() floats, so parse(serialize(r)) == r exactly."""

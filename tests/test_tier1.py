@@ -78,3 +78,27 @@ def test_lattice_errors():
              for r in recs if r.version_mask < 8]
     with pytest.raises(T.Tier1Error, match="optimizations"):
         T.to_dataset(recs + other)
+
+
+NVPROF = """==PROF== Connected to process 1234
+==1234== Profiling application: ./bh 500000 10
+==1234== Event result:
+"Device","Kernel","Invocations","Event Name","Min","Max","Avg","Total"
+"Tesla K20c (0)","ForceCalculationKernel","10","inst_executed","900","1100","1000","10000"
+"Tesla K20c (0)","ForceCalculationKernel","10","elapsed_cycles_sm","1900","2100","2000","20000"
+"Tesla K20c (0)","SortKernel","10","inst_executed","40","60","50","500"
+"""
+
+
+def test_nvprof_import_spec_examples():
+    # S:60: Device,Kernel,Event Name,Min,Max,Avg -> the event's Avg value; "==" lines skipped
+    recs = T.import_nvprof_csv(NVPROF, "BH", "in5", 0, 0b1011, runtime_ms=2.5, kernel="ForceCalculationKernel")
+    assert len(recs) == 1
+    r = recs[0]
+    assert r.counters == {"inst_executed": 1000.0} and r.cycles == 2000.0 and r.runtime == 2.5
+    assert r.key == ("BH", "in5", 0, 0b1011, "ForceCalculationKernel")
+    # S:61: an export lacking the cycles event -> incomplete-record error
+    with pytest.raises(T.Tier1Error, match="incomplete"):
+        T.import_nvprof_csv(NVPROF, "BH", "in5", 0, 0, runtime_ms=1.0, kernel="SortKernel")
+    with pytest.raises(T.Tier1Error, match="header"):
+        T.import_nvprof_csv("==PROF== nothing\n1,2,3\n", "BH", "i", 0, 0)
