@@ -665,20 +665,33 @@ __device__ __forceinline__ void rank_scenario(const EvalArgs& A, long long sl, i
         for (int r = q + 1; r < CMAX; ++r)
           if (cv[r] && !(cc[q] && cc[r]) && near_tol(ce[q], ce[r], A.guard_tol)) ++guard;
       }
-      // rank among candidates with EX >= threshold: (EX desc, id asc)
+      // rank among candidates with EX >= threshold: (EX desc, id asc) by
+      // selection -- round rk takes the best remaining candidate, whose rank
+      // is rk; only the first max_count rounds recommend
+      unsigned left = 0u;
 #pragma unroll
-      for (int q = 0; q < CMAX; ++q) {
-        if (!cv[q] || !(ce[q] >= A.threshold)) continue;
-        int rk = 0;
+      for (int q = 0; q < CMAX; ++q)
+        if (cv[q] && ce[q] >= A.threshold) left |= 1u << q;
+      for (int rk = 0; rk < A.max_count && left; ++rk) {
+        int best = -1;
+        double be = -INFINITY;
 #pragma unroll
-        for (int r = 0; r < CMAX; ++r)
-          if (r != q && cv[r] && ce[r] >= A.threshold && (ce[r] > ce[q] || (ce[r] == ce[q] && r < q))) ++rk;
-        if (rk < A.max_count) {
-          ++nrec;
-          const int o = olist[q];
-          if (A.ylab[(g * O + o) * 32 + ck[q]] > 1.0) ++nhit;
-          if (A.rec_out) A.rec_out[(so * G * 64 + g * 64 + v) * A.max_count + rk] = (int8_t)o;
-        }
+        for (int q = 0; q < CMAX; ++q)
+          if (((left >> q) & 1u) && ce[q] > be) {     // strict: ties keep the lower id
+            be = ce[q];
+            best = q;
+          }
+        left &= ~(1u << best);
+        ++nrec;
+        int kb = 0, ob = 0;
+#pragma unroll
+        for (int q = 0; q < CMAX; ++q)
+          if (q == best) {
+            kb = ck[q];
+            ob = olist[q];
+          }
+        if (A.ylab[(g * O + ob) * 32 + kb] > 1.0) ++nhit;
+        if (A.rec_out) A.rec_out[(so * G * 64 + g * 64 + v) * A.max_count + rk] = (int8_t)ob;
       }
     }
   }

@@ -1128,7 +1128,10 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
       continue;
     }
     if (A.fuse_rank) continue;
-    if (cmax == 8) {
+    if (c->n_os <= 6) {   // the paper's six optimizations: no empty candidate slots
+      if ((st = launch(c, "k_rank_warp", [&] { k_rank_warp<6><<<(unsigned)rblocks, 256, 0, c->stream>>>(A); })))
+        return st;
+    } else if (cmax == 8) {
       if ((st = launch(c, "k_rank_warp", [&] { k_rank_warp<8><<<(unsigned)rblocks, 256, 0, c->stream>>>(A); })))
         return st;
     } else {
