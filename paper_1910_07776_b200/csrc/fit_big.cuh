@@ -493,16 +493,78 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       }
       __syncthreads();
       SR_PT(2);
-      // ---- A4: LDL-form Cholesky (unscaled columns), CTA-wide ----
-      for (int j = 0; j < deff; ++j) {
-        const double djj = Gbuf[j * kBigGLd + j];
-        if (!(djj > 0.0)) ok = false;
-        const double r = rsqrt_nr(djj);
-        if (t == 0) invd[j] = r;
-        const double q = r * r;
-        for (int i = j + 1 + warp; i < deff; i += kBigThreads / 32) {
-          const double sij = Gbuf[i * kBigGLd + j] * q;
-          for (int k = j + 1 + lane; k <= i; k += 32) Gbuf[i * kBigGLd + k] = fma(-sij, Gbuf[k * kBigGLd + j], Gbuf[i * kBigGLd + k]);
+      // ---- A4: blocked Cholesky, 8-column panels ----
+      // per panel: warp 0 factors the 8x8 diagonal block (lanes = rows),
+      // one thread per row solves the panel below it (TRSM), and the warps
+      // update the trailing lower triangle on DMMA (C -= L21 L21^T, two
+      // k-steps per 8x8 tile, C loaded from and stored to shared memory).
+      // Rows / columns in [deff, 8 nb) are identity padding.  The result is
+      // turned into the solves' form: Gbuf[i][j] = L_ij L_jj (i > j), invd.
+      {
+        const int nbk = (deff + 7) >> 3, dpad = nbk * 8;
+        for (int e = t; e < dpad * dpad; e += kBigThreads) {
+          const int r = e / dpad, c = e - r * dpad;
+          if ((r >= deff || c >= deff) && c <= r) Gbuf[r * kBigGLd + c] = (r == c) ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        const int rl = lane >> 2, kl = lane & 3;
+        for (int pb = 0; pb < nbk; ++pb) {
+          const int c0 = pb * 8;
+          if (warp == 0) {                       // diagonal block, lanes 0..7 = rows c0 + lane
+            double* ri = Gbuf + (c0 + (lane & 7)) * kBigGLd + c0;
+            for (int j = 0; j < 8; ++j) {
+              const double* rj = Gbuf + (c0 + j) * kBigGLd + c0;
+              double v = ri[j];
+              for (int k = 0; k < j; ++k) v = fma(-ri[k], rj[k], v);
+              const double r = __shfl_sync(FULL, rsqrt_nr(v), j);   // 1/L_jj from lane j
+              if (lane < 8 && lane >= j) ri[j] = v * r;            // L_ij (lane j: L_jj = v / sqrt(v))
+              if (lane == j) invd[c0 + j] = r;
+              __syncwarp();
+            }
+          }
+          __syncthreads();
+          // TRSM: rows below the panel, L21 = A21 L11^-T
+          for (int i = c0 + 8 + t; i < dpad; i += kBigThreads) {
+            double* ri = Gbuf + i * kBigGLd + c0;
+            double x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const double* rj = Gbuf + (c0 + j) * kBigGLd + c0;
+              double v = ri[j];
+#pragma unroll
+              for (int k = 0; k < j; ++k) v = fma(-x[k], rj[k], v);
+              x[j] = v * invd[c0 + j];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ri[j] = x[j];
+          }
+          __syncthreads();
+          // SYRK on DMMA: trailing tiles (I, J), pb < J <= I < nbk
+          const int nt = nbk - pb - 1, ntiles = nt * (nt + 1) / 2;
+          for (int tt = warp; tt < ntiles; tt += kBigThreads / 32) {
+            int I = 0;
+            while ((I + 1) * (I + 2) / 2 <= tt) ++I;
+            const int J = tt - I * (I + 1) / 2;
+            const int gi = (pb + 1 + I) * 8, gj = (pb + 1 + J) * 8;
+            double* cp = Gbuf + (gi + rl) * kBigGLd + gj + 2 * kl;
+            double d0 = cp[0], d1 = cp[1];
+#pragma unroll
+            for (int ks = 0; ks < 8; ks += 4) {
+              const double a = -Gbuf[(gi + rl) * kBigGLd + c0 + ks + kl];
+              const double b = Gbuf[(gj + rl) * kBigGLd + c0 + ks + kl];
+              dmma(d0, d1, a, b);
+            }
+            cp[0] = d0;
+            cp[1] = d1;
+          }
+          __syncthreads();
+        }
+        for (int j = 0; j < deff; ++j)
+          if (!(invd[j] > 0.0 && invd[j] < INFINITY)) ok = false;
+        // solves' form: strictly lower entries scaled by their column's L_jj
+        for (int e = t; e < deff * deff; e += kBigThreads) {
+          const int r = e / deff, c = e - r * deff;
+          if (c < r) Gbuf[r * kBigGLd + c] /= invd[c];
         }
         __syncthreads();
       }
