@@ -36,7 +36,10 @@ constexpr int kSchurT = 12;                 // largest prefix (counters before t
 constexpr int kSchurQ = kSchurU * (kSchurU + 1) / 2;
 constexpr int kRec = 80;                    // doubles per record: Q[55] r~[10] z~[10] base flags pad
 constexpr int kRecR = kSchurQ, kRecZ = kSchurQ + kSchurU, kRecBase = kSchurQ + 2 * kSchurU, kRecFlag = kRecBase + 1;
-constexpr int kSfitThreads = 256;
+#ifndef SPEEDREC_SFIT_THREADS
+#define SPEEDREC_SFIT_THREADS 256
+#endif
+constexpr int kSfitThreads = SPEEDREC_SFIT_THREADS;
 #ifndef SPEEDREC_SFIT_MINB        // CTAs per SM the register budget of k_mask_sfit<D> targets
 #define SPEEDREC_SFIT_MINB(D) ((D) <= 3 ? 3 : (D) <= 6 ? 2 : 1)
 #endif
