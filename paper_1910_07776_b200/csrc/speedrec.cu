@@ -49,6 +49,8 @@ struct sr_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t cstream = nullptr;        // copy stream: D2H of finished chunks overlaps later ones
+  std::vector<cudaEvent_t> cp_events;
   std::string err;
   int sm_count = 0;
   int max_smem_optin = 0;
@@ -265,6 +267,11 @@ void sr_destroy(sr_ctx* c) {
                     &c->mp_units, &c->mp_pfx, &c->sw_buf, &c->ibk_lists, &c->ibk_xs, &c->ibk_meta})
     release(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->cp_events) cudaEventDestroy(e);
+  if (c->cstream) {
+    cudaStreamSynchronize(c->cstream);
+    cudaStreamDestroy(c->cstream);
+  }
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1103,6 +1110,11 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   const int cmax = c->n_os <= 8 ? 8 : 16;
   bool mask_path = false;
   if ((st = run_mask_path(c, prm, first, count, A, &mask_path))) return st;
+  // host rows of the warp path: each chunk's rows are copied on the copy
+  // stream as soon as its ranking is done (overlaps the next chunk's fits)
+  const bool early_rows = !out->on_device && out->opt_scores && out->scn_scores && !mask_path && !c->sweep;
+  if (early_rows && !c->cstream) CU(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+  int n_cp = 0;
   for (long long c0 = 0; c0 < (mask_path ? 0 : count); c0 += chunk) {
     const long long cc = std::min(chunk, count - c0);
     A.first = first + c0;
@@ -1138,7 +1150,22 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
       if ((st = launch(c, "k_rank_warp", [&] { k_rank_warp<16><<<(unsigned)rblocks, 256, 0, c->stream>>>(A); })))
         return st;
     }
+    if (early_rows && !A.fuse_rank) {
+      if ((int)c->cp_events.size() <= n_cp) {
+        cudaEvent_t e;
+        CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->cp_events.push_back(e);
+      }
+      cudaEvent_t e = c->cp_events[n_cp++];
+      CU(cudaEventRecord(e, c->stream));
+      CU(cudaStreamWaitEvent(c->cstream, e, 0));
+      CU(cudaMemcpyAsync(out->opt_scores + c0 * O, (const sr_opt_score*)c->out_opt.p + c0 * O,
+                         (size_t)cc * O * sizeof(sr_opt_score), cudaMemcpyDeviceToHost, c->cstream));
+      CU(cudaMemcpyAsync(out->scn_scores + c0, (const sr_scn_score*)c->out_scn.p + c0, (size_t)cc * sizeof(sr_scn_score),
+                         cudaMemcpyDeviceToHost, c->cstream));
+    }
   }
+  const bool rows_copied = early_rows && n_cp > 0;
   if (agg) {
     if ((st = launch(c, "k_mask_final",
                      [&] { k_mask_final<<<grid_for(c, nm, 256), 256, 0, c->stream>>>(A); })))
@@ -1167,10 +1194,11 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
       CU(cudaMemcpyAsync(out->top_masks, tm, (size_t)K * 8, cudaMemcpyDeviceToHost, c->stream));
   }
   if (!out->on_device) {
-    if (out->opt_scores)
+    if (out->opt_scores && !rows_copied)
       CU(cudaMemcpyAsync(out->opt_scores, c->out_opt.p, b_opt, cudaMemcpyDeviceToHost, c->stream));
-    if (out->scn_scores)
+    if (out->scn_scores && !rows_copied)
       CU(cudaMemcpyAsync(out->scn_scores, c->out_scn.p, b_scn, cudaMemcpyDeviceToHost, c->stream));
+    if (rows_copied) CU(cudaStreamSynchronize(c->cstream));
     if (out->mask_scores)
       CU(cudaMemcpyAsync(out->mask_scores, c->out_mask.p, (size_t)nm * sizeof(sr_mask_score),
                          cudaMemcpyDeviceToHost, c->stream));
