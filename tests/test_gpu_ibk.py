@@ -123,3 +123,21 @@ def test_ibk_large_batch_feature_mask():
     sc.n_masks = 1
     got, ref = _run(cfg, 0, 6)
     print("IBK C4 masked", _exact(got, ref))
+
+
+def test_ibk_large_batch_full_size_sampled():
+    """IBK at the full C4 lattice (1024 programs, n ~ 8,192 training rows and
+    t ~ 16,384 test rows per fit: 256 test tiles x 256 row tiles) in the
+    bench's launch shape: a sampled scenario is bit-exact against the oracle."""
+    from paper_1910_07776_b200 import Context, default_params
+    cfg = gen.make_config("C4", n_splits=16)
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    got = ctx.evaluate(0, 16, params=default_params(learner=1), want_ex=True, want_recs=True)
+    ctx.close()
+    s = 11
+    ref = oracle.evaluate(cfg.dataset, cfg.scenarios, s, 1, want_ex=True, want_recs=True, learner=1, k_nn=10,
+                          n_threads=16)
+    one = {k: (v[s:s + 1] if v is not None else None) for k, v in got.items() if k in ("opt", "scn", "ex", "recs")}
+    print("IBK C4 full, scenario", s, _exact(one, ref))
