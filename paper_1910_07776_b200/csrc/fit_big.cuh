@@ -19,7 +19,11 @@
 namespace speedrec {
 
 constexpr int kBigThreads = 256;
-constexpr int kBigChunk = 32;   // training rows per staged chunk (8 k-steps)
+constexpr int kBigChunk = 32;   // training rows per refinement chunk (8 k-steps)
+#ifndef SPEEDREC_GRAM_CHUNK
+#define SPEEDREC_GRAM_CHUNK 32
+#endif
+constexpr int kGramChunk = SPEEDREC_GRAM_CHUNK;   // rows per Gram-pass ring stage (3 stages in Gbuf + rch)
 constexpr int kBigLd = 132;     // chunk row stride in doubles: conflict-free 4x8 fragments
 constexpr int kBigMaxD = 128;
 constexpr int kBigGLd = 129;    // Gram row stride (odd: conflict-free columns)
@@ -359,35 +363,47 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       const bool fin = fa < d;
       const double cshift = fin ? A.x[(long long)trs[0] * C + Fl[fa]] : 0.0;
       double pmn = INFINITY, pmx = -INFINITY, psm = 0.0, prh = 0.0;
-      double* ring = Gbuf;                                  // [3][32][kBigLd]
-      double* yring = rpt;                                  // [3][32] centred labels of the stage rows
-      const int nchunks = (n + kBigChunk - 1) / kBigChunk;
+      double* ring = Gbuf;                                  // [3][kGramChunk][kBigLd] (spills into the free rch space)
+      double* yring = rpt;                                  // [3][kGramChunk] centred labels of the stage rows
+      const int nchunks = (n + kGramChunk - 1) / kGramChunk;
       const int crow = t >> 3, ca0 = t & 7;
       // copy mapping: thread (row crow, features ca0 + 8q); rows >= n and
       // features >= d are zero-filled
-      auto issue = [&](int ch, int slot) {
-        double* dst = ring + (ch % 3) * kBigChunk * kBigLd + crow * kBigLd + ca0;
-        const double* xr = A.x + (slot >= 0 ? (long long)slot * C : 0);
+      // rows crow (all threads) and 32 + crow (t < 128) of the chunk
+      auto issue = [&](int ch, int slot, int slot2) {
+        double* st = ring + (ch % 3) * kGramChunk * kBigLd;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int a = ca0 + 8 * q;
-          const bool ok_ = slot >= 0 && a < d;
-          cp_async8(dst + 8 * q, xr + (ok_ ? Fl[a] : 0), ok_);
+        for (int h = 0; h < 2; ++h) {
+          const int row = crow + 32 * h;
+          if (row >= kGramChunk) break;
+          const int sl_ = h ? slot2 : slot;
+          double* dst = st + row * kBigLd + ca0;
+          const double* xr = A.x + (sl_ >= 0 ? (long long)sl_ * C : 0);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int a = ca0 + 8 * q;
+            const bool ok_ = sl_ >= 0 && a < d;
+            cp_async8(dst + 8 * q, xr + (ok_ ? Fl[a] : 0), ok_);
+          }
+          if (ca0 == 0) {
+            const int r = ch * kGramChunk + row;
+            cp_async8(yring + (ch % 3) * kGramChunk + row, yl + (r < n ? r : 0), r < n);
+          }
         }
-        if (ca0 == 0) {
-          const int r = ch * kBigChunk + crow;
-          cp_async8(yring + (ch % 3) * kBigChunk + crow, yl + (r < n ? r : 0), r < n);
-        }
+      };
+      auto gslot = [&](int ch, int row) {
+        const int r = ch * kGramChunk + row;
+        return (row < kGramChunk && r < n) ? trs[r] : -1;
       };
       // fold chunk cc's raw values into the statistics and shift them in
       // place (thread: feature fa, rows fh + 2j)
       auto shift_rows = [&](int cc, int j0, int j1) {
-        double* st = ring + (cc % 3) * kBigChunk * kBigLd;
-        const double* ys = yring + (cc % 3) * kBigChunk;
+        double* st = ring + (cc % 3) * kGramChunk * kBigLd;
+        const double* ys = yring + (cc % 3) * kGramChunk;
 #pragma unroll
         for (int j = j0; j < j1; ++j) {
           const int r = fh + 2 * j;
-          const bool live = fin && cc * kBigChunk + r < n;
+          const bool live = fin && cc * kGramChunk + r < n;
           double xv = st[r * kBigLd + fa];
           if (live) {
             pmn = fmin(pmn, xv);
@@ -399,14 +415,14 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
           prh = fma(xv, ys[r], prh);
         }
       };
-      issue(0, big_slot(trs, n, 0));
+      issue(0, gslot(0, crow), gslot(0, crow + 32));
       cp_commit();
-      if (nchunks > 1) issue(1, big_slot(trs, n, 1));
+      if (nchunks > 1) issue(1, gslot(1, crow), gslot(1, crow + 32));
       cp_commit();
-      int slot_pf = big_slot(trs, n, 2);
+      int slot_pf = gslot(2, crow), slot_pf2 = gslot(2, crow + 32);
       cp_wait<1>();
       __syncthreads();
-      shift_rows(0, 0, 16);
+      shift_rows(0, 0, kGramChunk / 2);
       const int rl = lane >> 2, kl = lane & 3;
       // iteration ch: contract chunk ch on DMMA while the same warps fold and
       // shift chunk ch+1 (two rows per k-step); one barrier per chunk
@@ -414,14 +430,15 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
         cp_wait<0>();                                       // this thread's copies of chunk ch+1 landed
         __syncthreads();                                    // chunk ch shifted, ch+1 visible, ch-1 free
         if (ch + 2 < nchunks) {
-          issue(ch + 2, slot_pf);
-          slot_pf = big_slot(trs, n, ch + 3);
+          issue(ch + 2, slot_pf, slot_pf2);
+          slot_pf = gslot(ch + 3, crow);
+          slot_pf2 = gslot(ch + 3, crow + 32);
         }
         cp_commit();
-        const double* cur = ring + (ch % 3) * kBigChunk * kBigLd;
+        const double* cur = ring + (ch % 3) * kGramChunk * kBigLd;
         const bool nxt = ch + 1 < nchunks;
 #pragma unroll
-        for (int k0 = 0; k0 < kBigChunk; k0 += 4) {
+        for (int k0 = 0; k0 < kGramChunk; k0 += 4) {
           if (nxt) shift_rows(ch + 1, k0 / 2, k0 / 2 + 2);
           const double* base = cur + (k0 + kl) * kBigLd + rl;
           double f[16];
