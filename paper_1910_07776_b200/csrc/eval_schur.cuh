@@ -41,7 +41,7 @@ constexpr int kRecR = kSchurQ, kRecZ = kSchurQ + kSchurU, kRecBase = kSchurQ + 2
 #endif
 constexpr int kSfitThreads = SPEEDREC_SFIT_THREADS;
 #ifndef SPEEDREC_SFIT_MINB        // CTAs per SM the register budget of k_mask_sfit<D> targets
-#define SPEEDREC_SFIT_MINB(D) ((D) <= 3 ? 3 : (D) <= 6 ? 2 : 1)
+#define SPEEDREC_SFIT_MINB(D) ((D) <= 3 ? 4 : (D) <= 8 ? 2 : 1)
 #endif
 
 struct SchurArgs {
