@@ -142,6 +142,115 @@ static __global__ void __launch_bounds__(128) k_mask_sprep(const SchurArgs SA) {
   R[kRecFlag] = __longlong_as_double((long long)flags);
 }
 
+// k_mask_sprep_p<P>: the same record for groups whose prefix has P counters,
+// everything in registers (compile-time sizes).  Inactive prefix counters
+// stay in the factor: their G row and column, r and z are exactly zero, so
+// their pivot is lambda and every quantity they touch gets exact zeros --
+// the record equals the one without them (D3).  glist: the launch's groups.
+template <int P>
+__global__ void __launch_bounds__(128) k_mask_sprep_p(const SchurArgs SA, const int32_t* glist, int ng) {
+  const MaskArgs& M = SA.M;
+  const long long S = M.sd.n_splits;
+  const int O = M.O, C = M.C, T = SA.T, U = SA.U;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)ng * S * O) return;
+  const int o = (int)(idx % O);
+  const long long split = (idx / O) % S;
+  const int j = glist[idx / (O * S)];
+  const long long item = ((long long)j * S + split) * O + o;
+  double* R = SA.rec + item * kRec;
+  const PrepMeta pm = M.pm[split * O + o];
+  if (pm.n <= 0) {
+    R[kRecFlag] = 0.0;
+    return;
+  }
+  const double* Gm = M.pG + (split * O + o) * C * C;
+  const double* rv = M.pr + (split * O + o) * C;
+  const double* zv = M.pz + (split * O + o) * C;
+  const uint32_t act = (uint32_t)pm.active;
+  int pf[P > 0 ? P : 1];
+  {
+    uint32_t mm = SA.pfx[j] & ((1u << T) - 1u);
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      pf[i] = __ffs(mm) - 1;
+      mm &= mm - 1u;
+    }
+  }
+  double L[P * (P + 1) / 2 + 1], V[kSchurU][P > 0 ? P : 1], yv[P > 0 ? P : 1], uv[P > 0 ? P : 1];
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+#pragma unroll
+    for (int k = 0; k <= i; ++k) L[i * (i + 1) / 2 + k] = Gm[pf[i] * C + pf[k]] + (i == k ? M.lambda : 0.0);
+    yv[i] = rv[pf[i]];
+    uv[i] = zv[pf[i]];
+#pragma unroll
+    for (int b = 0; b < kSchurU; ++b) V[b][i] = b < U ? Gm[(T + b) * C + pf[i]] : 0.0;
+  }
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < P; ++c) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int jc = c * (c + 1) / 2;
+    double d = L[jc + c];
+#pragma unroll
+    for (int k = 0; k < c; ++k) d = fma(-L[jc + k], L[jc + k], d);
+    ok &= d > 0.0;
+    const double r = rsqrt_nr(d);
+    L[jc + c] = r;
+#pragma unroll
+    for (int i = c + 1; i < P; ++i) {
+      const int ji = i * (i + 1) / 2;
+      double a = L[ji + c];
+#pragma unroll
+      for (int k = 0; k < c; ++k) a = fma(-L[ji + k], L[jc + k], a);
+      L[ji + c] = a * r;
+    }
+    double a = yv[c], e = uv[c];
+#pragma unroll
+    for (int k = 0; k < c; ++k) {
+      a = fma(-yv[k], L[jc + k], a);
+      e = fma(-uv[k], L[jc + k], e);
+    }
+    yv[c] = a * r;
+    uv[c] = e * r;
+#pragma unroll
+    for (int b = 0; b < kSchurU; ++b) {
+      double v = V[b][c];
+#pragma unroll
+      for (int k = 0; k < c; ++k) v = fma(-V[b][k], L[jc + k], v);
+      V[b][c] = v * r;
+    }
+  }
+  double base = 0.0;
+#pragma unroll
+  for (int k = 0; k < P; ++k) base = fma(yv[k], uv[k], base);
+#pragma unroll
+  for (int b = 0; b < kSchurU; ++b) {
+    if (b >= U) break;
+#pragma unroll
+    for (int c = 0; c <= b; ++c) {
+      double q = Gm[(T + b) * C + (T + c)] + (b == c ? M.lambda : 0.0);
+#pragma unroll
+      for (int k = 0; k < P; ++k) q = fma(-V[b][k], V[c][k], q);
+      R[b * (b + 1) / 2 + c] = q;
+    }
+    double a = rv[T + b], e = zv[T + b];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      a = fma(-V[b][k], yv[k], a);
+      e = fma(-V[b][k], uv[k], e);
+    }
+    R[kRecR + b] = a;
+    R[kRecZ + b] = e;
+  }
+  R[kRecBase] = base;
+  const unsigned long long flags = 1ull | ((unsigned long long)((act >> T) & ((1u << U) - 1u)) << 8) |
+                                   (ok ? 0ull : 2ull);
+  R[kRecFlag] = __longlong_as_double((long long)flags);
+}
+
 // EX - ybar - base of one suffix system of compile-time size D from a staged
 // record: gather Q_SS (f ascending, so the packed lower layout is preserved),
 // factor with r~ and z~ carried as augmented rows, y~.u~.
@@ -337,5 +446,6 @@ __global__ void __launch_bounds__(kSfitThreads, SPEEDREC_SFIT_MINB(D)) k_mask_sf
 
 cudaError_t mask_sfit_launch(int D, unsigned grid, cudaStream_t st, const SchurArgs& SA, int off, int n_items,
                              int fold_chunks);
+cudaError_t mask_sprep_launch(int P, unsigned grid, cudaStream_t st, const SchurArgs& SA, const int32_t* glist, int ng);
 
 }  // namespace speedrec

@@ -79,7 +79,8 @@ struct sr_ctx {
   std::vector<int> perm_off;     // [kMaskMaxD + 2] start of each popcount group in mp_perm
   unsigned mask_or = 0;          // union of the call's masks (with the perm cache)
   // prefix-shared mask path (eval_schur.cuh): plan cached per (definition, range)
-  DevBuf mp_rec, mp_order, mp_units, mp_pfx;
+  DevBuf mp_rec, mp_order, mp_units, mp_pfx, mp_glist;
+  std::vector<int> splan_goff;   // [kSchurU + 2] groups of each prefix popcount in mp_glist
   long long splan_key[4] = {-1, -1, -1, -1};
   int splan_groups = 0;
   std::vector<int> splan_doff;   // [kSchurU + 2] start of each suffix-size group in mp_order
@@ -264,7 +265,7 @@ void sr_destroy(sr_ctx* c) {
                     &c->out_top, &c->keys_a, &c->keys_b, &c->big_lists, &c->big_y, &c->big_U, &c->big_c0,
                     &c->big_flag, &c->extab, &c->trained, &c->guard_acc, &c->mask_acc, &c->done, &c->fit_coef,
                     &c->mp_G, &c->mp_r, &c->mp_z, &c->mp_meta, &c->mp_perm, &c->mp_rec, &c->mp_order,
-                    &c->mp_units, &c->mp_pfx, &c->sw_buf, &c->ibk_lists, &c->ibk_xs, &c->ibk_meta})
+                    &c->mp_units, &c->mp_pfx, &c->mp_glist, &c->sw_buf, &c->ibk_lists, &c->ibk_xs, &c->ibk_meta})
     release(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->cp_events) cudaEventDestroy(e);
@@ -540,6 +541,20 @@ sr_status run_schur_path(sr_ctx* c, const MaskArgs& M, long long S, int T, int U
     CU(cudaMemcpyAsync(c->mp_pfx.p, pfx.data(), pfx.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CU(cudaStreamSynchronize(c->stream));   // host vectors go out of scope
     c->splan_groups = (int)pfx.size();
+    // groups by prefix popcount (k_mask_sprep_p<P> launches)
+    {
+      std::vector<int32_t> gl;
+      c->splan_goff.assign(kSchurU + 2, 0);
+      for (int pp = 0; pp <= kSchurU; ++pp) {
+        c->splan_goff[pp] = (int)gl.size();
+        for (size_t j = 0; j < pfx.size(); ++j)
+          if (__builtin_popcount(pfx[j]) == pp) gl.push_back((int32_t)j);
+      }
+      c->splan_goff[kSchurU + 1] = (int)gl.size();
+      if ((st = ensure(c, c->mp_glist, std::max<size_t>(gl.size(), 1) * 4))) return st;
+      CU(cudaMemcpyAsync(c->mp_glist.p, gl.data(), gl.size() * 4, cudaMemcpyHostToDevice, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+    }
     c->splan_key[0] = c->sc_gen;
     c->splan_key[1] = mask0;
     c->splan_key[2] = nm;
@@ -556,9 +571,23 @@ sr_status run_schur_path(sr_ctx* c, const MaskArgs& M, long long S, int T, int U
   SA.rec = (double*)c->mp_rec.p;
   SA.order = (const int32_t*)c->mp_order.p;
   SA.group = (const int32_t*)c->mp_units.p;
-  if ((st = launch(c, "k_mask_sprep",
-                   [&] { k_mask_sprep<<<(unsigned)((nrec + 127) / 128), 128, 0, c->stream>>>(SA); })))
+  if (T <= kSchurU && (int)c->splan_goff.size() == kSchurU + 2 &&
+      c->splan_goff[kSchurU + 1] == c->splan_groups) {   // register records per prefix size
+    for (int pp = 0; pp <= kSchurU; ++pp) {
+      const int g0 = c->splan_goff[pp], ng = c->splan_goff[pp + 1] - g0;
+      if (ng == 0) continue;
+      const long long nth = (long long)ng * S * O;
+      cudaError_t ce = cudaSuccess;
+      const sr_status s2 = launch(c, "k_mask_sprep", [&] {
+        ce = mask_sprep_launch(pp, (unsigned)((nth + 127) / 128), c->stream, SA, (const int32_t*)c->mp_glist.p + g0, ng);
+      });
+      if (ce != cudaSuccess) return fail(c, SR_E_CUDA, "k_mask_sprep_p<%d>: %s", pp, cudaGetErrorString(ce));
+      if (s2) return s2;
+    }
+  } else if ((st = launch(c, "k_mask_sprep",
+                          [&] { k_mask_sprep<<<(unsigned)((nrec + 127) / 128), 128, 0, c->stream>>>(SA); }))) {
     return st;
+  }
   for (int d = 0; d <= kSchurU; ++d) {
     const int off = c->splan_doff[d], n_it = c->splan_doff[d + 1] - off;
     if (n_it == 0) continue;
