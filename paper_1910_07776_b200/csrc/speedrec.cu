@@ -909,6 +909,22 @@ sr_status evaluate_big(sr_ctx* c, const sr_params* prm, long long first, long lo
                     16 + 8) * 8 + (2 * kBigMaxD + 2 * G + 20) * 4;
   CU(cudaFuncSetAttribute(k_fit_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (c->n_os > 8) return fail(c, SR_E_UNSUPPORTED, "evaluate: > 64 groups supports <= 8 scored optimizations");
+  // optional (SPEEDREC_L2_PERSIST=1): an L2 persisting access window over the
+  // rates, which every fit gathers from (A/B knob)
+  if (const char* e = getenv("SPEEDREC_L2_PERSIST")) {
+    if (atoi(e) != 0) {
+      const size_t xb = (size_t)N * C * 8;
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, xb);
+      cudaStreamAttrValue av{};
+      av.accessPolicyWindow.base_ptr = c->x.p;
+      av.accessPolicyWindow.num_bytes = xb;
+      av.accessPolicyWindow.hitRatio = 1.0f;
+      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &av);
+      cudaGetLastError();
+    }
+  }
   if (prm->learner == SR_IBK) return evaluate_big_ibk(c, prm, first, count, B, opt, scn, ex, rec, tot, out);
   for (long long b0 = 0; b0 < count; b0 += batch) {
     const long long bc = std::min(batch, count - b0);
