@@ -36,8 +36,10 @@
  *     first, count), independent of launch configuration and GPU count
  *     (FP sums inside one (scenario, optimization) row use a fixed order).
  *   Limits: n_opt_bits == 6 (the paper's lattice), n_counters <= 128,
- *     n_opt_ids <= 16, groups <= 64 per scenario batch, max_count <= 8.
- *     Violations return SR_E_UNSUPPORTED.
+ *     n_opt_ids <= 16, max_count <= 8.  Up to 64 groups run on the warp path
+ *     (all features); more groups on the large-batch path (config C4), which
+ *     needs <= 8 scored optimizations and supports neither mask aggregation
+ *     nor sr_sweep.  Violations return SR_E_UNSUPPORTED.
  */
 #ifndef SPEEDREC_H_
 #define SPEEDREC_H_
@@ -139,7 +141,8 @@ typedef enum { SR_LINREG = 0, SR_IBK = 1 } sr_learner;
 
 typedef struct {
   int32_t learner;       /* SR_LINREG (ridge LS, reading D1) or SR_IBK (k-nearest neighbours,
-                            P:147-149, reading R22; <= 64 groups only, else SR_E_UNSUPPORTED) */
+                            P:147-149, reading R22; bit-exact, both the <= 64-group and the
+                            large-batch path) */
   int32_t max_count;     /* Tier-3 max recommendations, 3 */
   int32_t refine_steps;  /* iterative-refinement steps of the solve, 2 */
   int32_t debug_mcap;    /* 0 = auto; >0 caps the shared-memory Cholesky size so larger
