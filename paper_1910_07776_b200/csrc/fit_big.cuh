@@ -188,19 +188,12 @@ __device__ __forceinline__ void big_scale_chunk(int n, int r0, const double* xb,
   }
 }
 
-__device__ __forceinline__ void big_store_chunk(double* buf, const double (&v)[16]) {
-  const int r = threadIdx.x >> 3, a0 = threadIdx.x & 7;
-#pragma unroll
-  for (int q = 0; q < 16; ++q) buf[r * kBigLd + a0 + 8 * q] = v[q];
-}
 
 __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  // layout: Gbuf (union with two chunk buffers) | vectors | scan arrays
+  // layout: Gbuf (union with the Gram-pass cp.async ring, which extends into rch) | rpt | vectors | scan arrays
   double* Gbuf = reinterpret_cast<double*>(smem);                       // [128][129]
-  double* chunk0 = Gbuf;                                                // [32][132]
-  double* chunk1 = Gbuf + kBigChunk * kBigLd;                           // [32][132]
-  double* rch = Gbuf + kBigMaxD * kBigGLd;                              // [32][132] refinement chunk
+  double* rch = Gbuf + kBigMaxD * kBigGLd;                              // [32][132] tail of the Gram ring
   double* rpt = rch + kBigChunk * kBigLd;                               // [32][128] refinement partials
   double* xb = rpt + kBigChunk * kBigMaxD;                              // [128]
   double* sv = xb + kBigMaxD;                                           // [128]
@@ -208,8 +201,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
   double* wv = rhs + kBigMaxD;                                          // [128]
   double* zv = wv + kBigMaxD;                                           // [128]
   double* invd = zv + kBigMaxD;                                         // [128]
-  double* ych = invd + kBigMaxD;                                        // [2][32] yc of the chunk rows
-  double* red = ych + 2 * kBigChunk;                                    // [16]
+  double* red = invd + kBigMaxD + 2 * kBigChunk;                        // [16] (after 64 spare doubles)
   uint64_t* xred = reinterpret_cast<uint64_t*>(red + 16);               // [8]
   int* col = reinterpret_cast<int*>(xred + 8);                          // [128]
   int* Fl = col + kBigMaxD;                                             // [128]
