@@ -1,8 +1,8 @@
 #!/bin/bash
-# Launch-shape sweep of k_eval_warp on the bench workload (run under gpurun).
+# Launch-shape sweep of k_fit_warp on the bench workload (run under gpurun).
 # Prints kernel ms per step for each (stage, wmax, smem cap) setting.
 cd "$(dirname "$0")/.."
-for cfg in "1 12 0" "1 16 0" "1 24 0" "0 12 0" "0 16 0" "0 24 0" "0 16 160" "0 24 160" "0 24 120"; do
+for cfg in "1 12 0" "1 16 0" "0 12 0" "0 16 0" "0 16 160" "0 12 120"; do
   set -- $cfg
   export SPEEDREC_STAGE=$1 SPEEDREC_WMAX=$2
   if [ "$3" != "0" ]; then export SPEEDREC_SMEM_KB=$3; else unset SPEEDREC_SMEM_KB; fi
