@@ -108,8 +108,16 @@ class ClockSampler:
 def oracle_rate(cfg, first: int, count: int, threads: int, learner: int = 0):
     import oracle
     t0 = time.perf_counter()
-    oracle.evaluate(cfg.dataset, cfg.scenarios, first, count, n_threads=threads, learner=learner)
+    if learner == 2:    # M5P: the exact-rational Python oracle (oracle/m5.py), one core
+        from oracle import m5
+        m5.evaluate(cfg.dataset, cfg.scenarios, first, count)
+    else:
+        oracle.evaluate(cfg.dataset, cfg.scenarios, first, count, n_threads=threads, learner=learner)
     return count / (time.perf_counter() - t0)
+
+
+def oracle_cores(threads: int, learner: int) -> int:
+    return 1 if learner == 2 else threads
 
 
 def run_reference(args, cfg, rank, world):
@@ -129,7 +137,8 @@ def run_reference(args, cfg, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sample / v,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+quad",
         "data": "synthetic", "config": workload_config(cfg, args, sample),
-        "cpu_baseline": {"value": v, "unit": "scenario_evals/s", "cores": threads, "kind": "oracle",
+        "cpu_baseline": {"value": v, "unit": "scenario_evals/s", "cores": oracle_cores(threads, LEARNERS[args.learner]),
+                         "kind": "oracle",
                          "sample": f"{sample} scenarios of {args.config} per step (splits "
                                    f"[k*{sample}, (k+1)*{sample}))"},
         "e2e": {"value": v, "unit": "scenario_evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -137,7 +146,7 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
-LEARNERS = {"linreg": 0, "ibk": 1}
+LEARNERS = {"linreg": 0, "ibk": 1, "m5": 2}
 
 
 def run_sweep(args, cfg, count):
@@ -185,10 +194,21 @@ def knn_flops(n: np.ndarray, t: np.ndarray, d: int) -> float:
     return float(3.0 * np.where((n > 0) & (t > 0), n * t * d, 0.0).sum())
 
 
+def m5_flops(n: np.ndarray, t: np.ndarray, d: int) -> float:
+    """M5P (NEXT-2) yardstick: the root split search alone -- d features x
+    (n - 1) candidate thresholds x two passes over the n rows (an add, and a
+    subtract + multiply + add: 4 flop per row); the deeper nodes, the node
+    models and the prediction are not counted."""
+    n = n.astype(np.float64)
+    t = t.astype(np.float64)
+    return float(np.where((n > 1) & (t > 0), 4.0 * d * (n - 1) * n, 0.0).sum())
+
+
 OTHER_CONFIGS = [("C1", "C1", ["--cpu-sample", "64"]), ("C2", "C2", ["--cpu-sample", "240"]),
                  ("C4", "C4", ["--splits", "592", "--no-cpu-baseline"]),
                  ("C5", "C5", ["--masks-k", "20", "--cpu-sample", "2048"]),
-                 ("C4-ibk", "C4", ["--splits", "16", "--learner", "ibk", "--no-cpu-baseline"])]
+                 ("C4-ibk", "C4", ["--splits", "16", "--learner", "ibk", "--no-cpu-baseline"]),
+                 ("C3-m5", "C3", ["--splits", "65536", "--learner", "m5", "--cpu-sample", "32"])]
 
 
 def run_other_configs(args):
@@ -235,7 +255,8 @@ def main():
     ap.add_argument("--masks-k", type=int, default=10,
                     help="C5: all 2^k subsets of counters [0, k) (the full config is k = 20)")
     ap.add_argument("--learner", default="linreg", choices=list(LEARNERS),
-                    help="linreg = ridge LS (the paper's model); ibk = the NEXT-1 k-NN learner")
+                    help="linreg = ridge LS (the paper's model); ibk = the NEXT-1 k-NN learner; "
+                         "m5 = the NEXT-2 M5P model tree")
     ap.add_argument("--ref-sample", type=int, default=4000)
     ap.add_argument("--cpu-sample", type=int, default=4000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -356,6 +377,8 @@ def main():
             ff = lambda d: n_fit * 2.0 * (d ** 3 / 6 + d ** 2 + d)
         elif args.learner == "ibk":
             ff = lambda d: knn_flops(n_tr, n_te, d)
+        elif args.learner == "m5":
+            ff = lambda d: m5_flops(n_tr, n_te, d)
         else:
             ff = lambda d: fit_flops(n_tr, n_te, d, refine=2)
         flops_launch = sum(float(np.sum(pcs == d)) * ff(int(d)) for d in np.unique(pcs))
@@ -364,6 +387,8 @@ def main():
         n_tr, n_te = opt["n_train"].ravel(), opt["n_test"].ravel()
         if args.learner == "ibk":
             flops_launch = knn_flops(n_tr, n_te, ds.n_counters)
+        elif args.learner == "m5":
+            flops_launch = m5_flops(n_tr, n_te, ds.n_counters)
         elif big:
             flops_launch = fit_flops_big(n_tr, n_te, ds.n_counters)
         else:
@@ -438,7 +463,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         v = oracle_rate(cfg, 0, args.cpu_sample, threads, LEARNERS[args.learner])
-        cpu = {"value": v, "unit": "scenario_evals/s", "cores": threads, "kind": "oracle",
+        cpu = {"value": v, "unit": "scenario_evals/s", "cores": oracle_cores(threads, LEARNERS[args.learner]),
+               "kind": "oracle",
                "sample": f"first {args.cpu_sample} scenarios of {args.config} (same splits the GPU evaluates)"}
 
     top_global = None
@@ -465,6 +491,8 @@ def main():
                          "flops_note": ("SURVEY 8(d) C5 yardstick p^3/6+p^2+p per fit on the precomputed "
                                         "Gram; the prefix-shared path (DESIGN 5.8) executes fewer flops, "
                                         "so frac is an effective fraction" if name_dom == "k_mask_sfit"
+                                        else "M5P yardstick: the root split search only, 4 d (n-1) n flop "
+                                        "per fit (DESIGN 6)" if args.learner == "m5"
                                         else "algorithmic flops of the fits (DESIGN 6)")},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk_sum,

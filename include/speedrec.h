@@ -137,12 +137,13 @@ sr_status sr_define_scenarios(sr_ctx* ctx, const sr_scenarios* sc, int64_t* n_sc
 /* ---------------------------------------------------------------------- */
 /* Parameters (defaults from sr_default_params).                           */
 /* ---------------------------------------------------------------------- */
-typedef enum { SR_LINREG = 0, SR_IBK = 1 } sr_learner;
+typedef enum { SR_LINREG = 0, SR_IBK = 1, SR_M5P = 2 } sr_learner;
 
 typedef struct {
-  int32_t learner;       /* SR_LINREG (ridge LS, reading D1) or SR_IBK (k-nearest neighbours,
+  int32_t learner;       /* SR_LINREG (ridge LS, reading D1), SR_IBK (k-nearest neighbours,
                             P:147-149, reading R22; bit-exact, both the <= 64-group and the
-                            large-batch path) */
+                            large-batch path) or SR_M5P (model tree, readings M1-M6;
+                            <= 64 groups and <= 64 counters, else SR_E_UNSUPPORTED) */
   int32_t max_count;     /* Tier-3 max recommendations, 3 */
   int32_t refine_steps;  /* iterative-refinement steps of the solve, 2 */
   int32_t debug_mcap;    /* 0 = auto; >0 caps the shared-memory Cholesky size so larger

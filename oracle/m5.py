@@ -43,12 +43,20 @@ RIDGE = 1e-8
 
 
 def sd_pop(y) -> float:
-    """Population standard deviation, two-pass (M1)."""
+    """Population standard deviation, two-pass, sums accumulated left to right
+    in FP64 (M1; explicit loops, since builtin sum() compensates on 3.12+)."""
     n = len(y)
     if n == 0:
         return 0.0
-    m = sum(y) / n
-    return math.sqrt(sum((v - m) * (v - m) for v in y) / n)
+    s = 0.0
+    for v in y:
+        s += v
+    m = s / n
+    q = 0.0
+    for v in y:
+        dv = v - m
+        q += dv * dv
+    return math.sqrt(q / n)
 
 
 def sdr(y, left) -> float:
@@ -100,7 +108,10 @@ def ridge_fit(X, y, idx, feats, lam=RIDGE):
 
 def model_value(model, x) -> float:
     b, w = model
-    return b + sum(wa * x[a] for a, wa in w.items())
+    s = 0.0
+    for a, wa in w.items():                        # ascending feature order
+        s += wa * x[a]
+    return b + s
 
 
 class Node:
@@ -133,41 +144,51 @@ def _grow(X, y, idx, sd_root):
     return node
 
 
-def _models(node, X, y):
-    """Post-order: allowed features = splits in the subtree (M3), models, M4 pruning."""
+def _models(node, X, y, tol):
+    """Post-order: allowed features = splits in the subtree (M3), models, M4
+    pruning.  Returns the number of pruning decisions within tol of their
+    boundary (guard cases, reading R21)."""
+    guard = 0
     if node.leaf:
         node.allowed = []
     else:
-        _models(node.left, X, y)
-        _models(node.right, X, y)
+        guard += _models(node.left, X, y, tol)
+        guard += _models(node.right, X, y, tol)
         node.allowed = sorted({node.feature, *node.left.allowed, *node.right.allowed})
     node.model = ridge_fit(X, y, node.idx, node.allowed)
-    resid = sum(abs(y[i] - model_value(node.model, X[i])) for i in node.idx) / node.n
+    rs = 0.0
+    for i in node.idx:
+        rs += abs(y[i] - model_value(node.model, X[i]))
+    resid = rs / node.n
     v = len(node.allowed) + 1
     f = (node.n + v) / (node.n - v) if node.n > v else 10.0
     own = resid * f
     if node.leaf:
         node.err = own
-        return
+        return guard
     sub = (node.left.n * node.left.err + node.right.n * node.right.err) / node.n
+    if abs(own - sub) <= tol * max(1.0, abs(own)):
+        guard += 1
     if own <= sub:                                  # prune to the node's model
         node.left = node.right = None
         node.feature = node.thr = None
         node.err = own
     else:
         node.err = sub
+    return guard
 
 
-def m5_build(X, y):
-    """X: list of feature rows (floats), y: labels.  Returns the root Node."""
+def m5_build(X, y, guard_tol=1e-9, counted=False):
+    """X: list of feature rows (floats), y: labels.  Returns the root Node
+    (counted=True: (root, number of pruning guard cases))."""
     if not y:
         raise ValueError("m5_build: empty dataset")
     if not all(math.isfinite(v) for v in y):
         raise ValueError("m5_build: non-finite labels")
     idx = list(range(len(y)))
     root = _grow(X, y, idx, sd_pop(list(y)))
-    _models(root, X, y)
-    return root
+    guard = _models(root, X, y, guard_tol)
+    return (root, guard) if counted else root
 
 
 def m5_predict(root, x, k: float = SMOOTH_K) -> float:
@@ -306,7 +327,8 @@ def evaluate(ds, sc, first=0, count=None, learner="m5", threshold=1.05, max_coun
                 Xs, Xts = np.zeros((len(rows), 0)), np.zeros((len(tests), 0))
             Xs_l, Xts_l = Xs.tolist(), Xts.tolist()
             if learner == "m5":
-                root = m5_build(Xs_l, ys)
+                root, gd = m5_build(Xs_l, ys, guard_tol, counted=True)
+                guard += gd
                 pred = [m5_predict(root, xt) for xt in Xts_l]
             else:
                 mdl = ridge_fit(Xs_l, ys, list(range(len(ys))), list(range(Xs.shape[1])), lam=ridge)

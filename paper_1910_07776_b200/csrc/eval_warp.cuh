@@ -179,6 +179,10 @@ __device__ __noinline__ bool fit_generic(const FitView& f, const double* yc, dou
   return true;
 }
 
+}  // namespace speedrec
+#include "m5_warp.cuh"
+namespace speedrec {
+
 // ------------------------------------------------------------- IBK (NEXT-1)
 // EX of one test case under IBk (reading R22): the mean training
 // label of the min(k, n) training befores nearest in min-max scaled counter
@@ -265,7 +269,7 @@ __device__ __forceinline__ void rank_scenario(const EvalArgs& A, long long sl, i
 
 // ---------------------------------------------------------------- fit kernel
 // MODE 0: ridge LS (the paper's model); 1: IBK (NEXT-1); 2: ridge LS + the
-// sr_fit coefficient store.  Separate instantiations keep the hot code lean.
+// sr_fit coefficient store; 3: M5P model tree (NEXT-2, m5_warp.cuh).  Separate instantiations keep the hot code lean.
 // STAGED: x staged in shared memory (compile-time, so every x access is an
 // LDS rather than a generic load).
 template <int WMAX, int MODE, bool STAGED>
@@ -402,7 +406,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
     }
 
     // ---- A2: per-fit min-max statistics over the training befores (D3) ----
-    constexpr bool ibk = MODE == 1;
+    constexpr bool ibk = MODE == 1, m5 = MODE == 3;
     int deff = 0;
     for (int a0 = 0; a0 < d; a0 += 64) {       // two features per lane per row pass
       const int a1 = a0 + lane, a2 = a0 + 32 + lane;
@@ -457,7 +461,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
           col[p] = (int16_t)(h ? c2 : c1);
           xb[p] = sm / (double)n;
           sv[p] = 1.0 / (mx - mn);
-          if (ibk) {
+          if (ibk || m5) {
             uv[p] = mn;
             wv[p] = mx - mn;
           }
@@ -475,7 +479,7 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
     }
     double c0 = 0.0;
     bool ok = true;
-    if (!ibk) {
+    if (!ibk && !m5) {
       double ysum = 0.0;
       #pragma unroll 1
       for (int i = lane; i < n; i += 32) ysum += yc[i];
@@ -537,7 +541,19 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
       ext[test_group_index(A.sd, split, gk >> 5) * 32 + (gk & 31)] = cl ? -e : e;
       if (A.ex_out) A.ex_out[(so * O + o) * (long long)G * 32 + gk] = e;
     };
-    if (ibk) {   // NEXT-1: IBk prediction, all lanes sweep together (knn_ex)
+    if (m5) {    // NEXT-2: grow + prune the tree in the warp's scratch slab, then lanes over tests
+      const M5Work W = m5_carve(scr, L.np_tr, A.C);
+      for (int e = lane; e < n * deff; e += 32) {
+        const int r = e / deff, a = e - r * deff;
+        W.Xs[r * W.ld + a] = (X[(long long)trs[r] * ldx + col[a]] - uv[a]) / wv[a];
+      }
+      __syncwarp();
+      int tg = 0;
+      bool tok = true;
+      m5_build(W, n, deff, yc, A.lambda, A.refine, A.guard_tol, lane, &tg, &tok);
+      guard += tg + (tok ? 0 : 1000000);
+      for (int j = lane; j < nt; j += 32) score(j, m5_predict(W, X + (long long)tes[j] * ldx, col, uv, wv));
+    } else if (ibk) {   // NEXT-1: IBk prediction, all lanes sweep together (knn_ex)
       const int kk = min(A.k_nn, n);
       #pragma unroll 1
       for (int j0 = 0; j0 < nt; j0 += 32) {

@@ -1,0 +1,479 @@
+// m5_warp.cuh -- the M5P model-tree learner (NEXT-2) on the warp path:
+// one warp grows, fits, prunes and evaluates the tree of one (scenario,
+// optimization) fit.  DESIGN.md §5.11; readings M1-M6.
+//
+// "an induction algorithm is used to construct a standard decision
+// tree.  Then a multivariate regression model is constructed for each node
+// ... only the features that appear in the subtree that contains the node are
+// used ... the leaf nodes ... are replaced with the newly constructed
+// regression models ... standard pruning and smoothing techniques are applied"
+// (Quinlan's M5, [10]); constants S:219-228.
+//
+// Tree growth is decided by floating point (the SDR argmax, the sd stop rule):
+// both sides take those decisions with the same IEEE operations in the same
+// order (__d*_rn: no FMA contraction), over the same bit-identical scaled
+// features and labels, so the grown tree is identical to the oracle's.  The
+// node models are ridge LS (FP64 here, exact rationals in the oracle); the one
+// decision they feed (pruning, M4) is counted as a guard case when it falls
+// within guard_tol of its boundary (reading R21).
+//
+// Workspace: a per-warp slab of global scratch (L1/L2 resident), carved by
+// M5Work.  Nodes are numbered in creation order; children have larger ids
+// than their parent, so one ascending pass grows the tree (the order in which
+// nodes are split does not change any node's result) and one descending pass
+// is a valid post-order for the models and pruning.
+#pragma once
+#include "kernels.cuh"
+
+namespace speedrec {
+
+constexpr int kM5MinSplit = 4;        // M2: |T| < 4 -> leaf
+constexpr double kM5SdFrac = 0.05;    // M2: sd(T) < 5 % of sd(root) -> leaf
+constexpr double kM5SmoothK = 15.0;   // M5: Quinlan's smoothing constant
+constexpr int kM5MaxFeatures = 64;    // allowed-feature sets are 64-bit masks
+
+// Scratch doubles one warp needs for fits of <= np training pairs, <= d features.
+__host__ __device__ inline long long m5_scratch_doubles(int np, int d) {
+  const long long nn = np > 0 ? 2LL * np - 1 : 1;
+  const long long pm = (d < np ? d : np) + 1;
+  long long t = (long long)np * d;                 // Xs
+  t += (2LL * np + 8 * nn + 1 + 64) / 2 + 1;       // perm, tmp, 8 node ints, feature list
+  t += 3 * nn;                                     // thr, err, allowed
+  t += nn * pm;                                    // model pool
+  t += pm * (pm + 1) / 2 + 4 * pm + np;            // factor, invd, xbar, c, delta, residuals
+  return t + 8;
+}
+
+struct M5Work {
+  double* Xs;       // [n][ld] scaled training rows
+  int ld;
+  double* thr;      // [nn]
+  double* err;      // [nn]
+  unsigned long long* allow;  // [nn] features split on in the (grown) subtree
+  double* pool;     // models: b, w[popc(allow)]
+  double* M;        // packed Cholesky factor
+  double* invd;
+  double* xbar;
+  double* cv;
+  double* dv;
+  double* ev;       // [n]
+  int *perm, *tmp, *nlo, *nhi, *feat, *left, *right, *par, *leaf, *moff, *fl;
+};
+
+__device__ __forceinline__ M5Work m5_carve(double* base, int np, int d) {
+  M5Work W;
+  const int nn = np > 0 ? 2 * np - 1 : 1;
+  const int pm = (d < np ? d : np) + 1;
+  double* p = base;
+  W.Xs = p;
+  W.ld = d;
+  p += (long long)np * d;
+  W.thr = p;
+  p += nn;
+  W.err = p;
+  p += nn;
+  W.allow = reinterpret_cast<unsigned long long*>(p);
+  p += nn;
+  W.pool = p;
+  p += (long long)nn * pm;
+  W.M = p;
+  p += (long long)pm * (pm + 1) / 2;
+  W.invd = p;
+  p += pm;
+  W.xbar = p;
+  p += pm;
+  W.cv = p;
+  p += pm;
+  W.dv = p;
+  p += pm;
+  W.ev = p;
+  p += np;
+  int* q = reinterpret_cast<int*>(p);
+  W.perm = q;
+  q += np;
+  W.tmp = q;
+  q += np;
+  W.nlo = q;
+  q += nn;
+  W.nhi = q;
+  q += nn;
+  W.feat = q;
+  q += nn;
+  W.left = q;
+  q += nn;
+  W.right = q;
+  q += nn;
+  W.par = q;
+  q += nn;
+  W.leaf = q;
+  q += nn;
+  W.moff = q;
+  q += nn;
+  W.fl = q;
+  return W;
+}
+
+// Population sd of the labels of perm[lo, hi), two passes, left to right (M1).
+__device__ __forceinline__ double m5_sd(const int* perm, int lo, int hi, const double* y) {
+  double s = 0.0;
+  for (int k = lo; k < hi; ++k) s = __dadd_rn(s, y[perm[k]]);
+  const double cnt = (double)(hi - lo);
+  const double m = __ddiv_rn(s, cnt);
+  double q = 0.0;
+  for (int k = lo; k < hi; ++k) {
+    const double dv = __dsub_rn(y[perm[k]], m);
+    q = __dadd_rn(q, __dmul_rn(dv, dv));
+  }
+  return __dsqrt_rn(__ddiv_rn(q, cnt));
+}
+
+// SDR of splitting perm[lo, hi) on feature a at thr (x <= thr left), M1:
+// sd(T) - |L|/|T| sd(L) - |R|/|T| sd(R), each sd two-pass in segment order.
+__device__ __forceinline__ double m5_sdr(const M5Work& W, int lo, int hi, int a, double thr, const double* y,
+                                         double sdT) {
+  double sL = 0.0, sR = 0.0;
+  int nL = 0;
+  for (int k = lo; k < hi; ++k) {
+    const int r = W.perm[k];
+    const double yk = y[r];
+    if (W.Xs[r * W.ld + a] <= thr) {
+      sL = __dadd_rn(sL, yk);
+      ++nL;
+    } else {
+      sR = __dadd_rn(sR, yk);
+    }
+  }
+  const int m = hi - lo, nR = m - nL;
+  const double mL = __ddiv_rn(sL, (double)nL), mR = __ddiv_rn(sR, (double)nR);
+  double qL = 0.0, qR = 0.0;
+  for (int k = lo; k < hi; ++k) {
+    const int r = W.perm[k];
+    if (W.Xs[r * W.ld + a] <= thr) {
+      const double dv = __dsub_rn(y[r], mL);
+      qL = __dadd_rn(qL, __dmul_rn(dv, dv));
+    } else {
+      const double dv = __dsub_rn(y[r], mR);
+      qR = __dadd_rn(qR, __dmul_rn(dv, dv));
+    }
+  }
+  const double sdL = __dsqrt_rn(__ddiv_rn(qL, (double)nL)), sdR = __dsqrt_rn(__ddiv_rn(qR, (double)nR));
+  const double fL = __ddiv_rn((double)nL, (double)m), fR = __ddiv_rn((double)nR, (double)m);
+  return __dsub_rn(__dsub_rn(sdT, __dmul_rn(fL, sdL)), __dmul_rn(fR, sdR));
+}
+
+__device__ __forceinline__ bool m5_better(double s, int a, double t, double bs, int ba, double bt) {
+  return s > bs || (s == bs && (a < ba || (a == ba && t < bt)));
+}
+
+// Best split of node segment [lo, hi) (M1): lanes over features, candidates =
+// midpoints between adjacent distinct values, key (SDR desc, feature asc,
+// threshold asc) -- the oracle's first strict maximum in (feature, threshold)
+// order.  Returns the SDR (-inf: no candidate); ba / bt the split.
+__device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const double* y, double sdT, int lane,
+                                int& ba, double& bt) {
+  double bs = -INFINITY;
+  ba = 0x7fffffff;
+  bt = INFINITY;
+  for (int a = lane; a < deff; a += 32) {
+    #pragma unroll 1
+    for (int j = lo; j < hi; ++j) {
+      const double u = W.Xs[W.perm[j] * W.ld + a];
+      bool dup = false;
+      double nx = INFINITY;
+      #pragma unroll 1
+      for (int k = lo; k < hi; ++k) {
+        const double v = W.Xs[W.perm[k] * W.ld + a];
+        dup |= (k < j) & (v == u);
+        if (v > u && v < nx) nx = v;
+      }
+      if (dup || nx == INFINITY) continue;
+      const double t = __dmul_rn(__dadd_rn(u, nx), 0.5);   // (lo + hi) / 2
+      const double s = m5_sdr(W, lo, hi, a, t, y, sdT);
+      if (m5_better(s, a, t, bs, ba, bt)) {
+        bs = s;
+        ba = a;
+        bt = t;
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double os = __shfl_xor_sync(FULL, bs, off), ot = __shfl_xor_sync(FULL, bt, off);
+    const int oa = __shfl_xor_sync(FULL, ba, off);
+    if (m5_better(os, oa, ot, bs, ba, bt)) {
+      bs = os;
+      ba = oa;
+      bt = ot;
+    }
+  }
+  return bs;
+}
+
+// Stable partition of perm[lo, hi) by Xs[.][a] <= thr (left first, both
+// halves in their original order, as the oracle's filtered index lists).
+__device__ int m5_partition(const M5Work& W, int lo, int hi, int a, double thr, int lane) {
+  const unsigned lt = (1u << lane) - 1u;
+  int nL = 0;
+  for (int k0 = lo; k0 < hi; k0 += 32) {
+    const int k = k0 + lane;
+    const bool l = k < hi && W.Xs[W.perm[k] * W.ld + a] <= thr;
+    nL += __popc(__ballot_sync(FULL, l));
+  }
+  int cl = 0, cr = 0;
+  for (int k0 = lo; k0 < hi; k0 += 32) {
+    const int k = k0 + lane;
+    const bool in = k < hi;
+    const int r = in ? W.perm[k] : 0;
+    const bool l = in && W.Xs[r * W.ld + a] <= thr;
+    const unsigned bl = __ballot_sync(FULL, l), br = __ballot_sync(FULL, in && !l);
+    if (l) W.tmp[lo + cl + __popc(bl & lt)] = r;
+    else if (in) W.tmp[lo + nL + cr + __popc(br & lt)] = r;
+    cl += __popc(bl);
+    cr += __popc(br);
+  }
+  __syncwarp();
+  for (int k = lo + lane; k < hi; k += 32) W.perm[k] = W.tmp[k];
+  __syncwarp();
+  return nL;
+}
+
+// Model value b + sum_j w_j x_fl[j] (ascending feature order, M3) on a scaled
+// training row.
+__device__ __forceinline__ double m5_row_value(const M5Work& W, const double* mdl, unsigned long long al,
+                                               const double* xs) {
+  double s = 0.0;
+  int j = 0;
+  while (al) {
+    const int a = __ffsll((long long)al) - 1;
+    al &= al - 1;
+    s = fma(mdl[1 + j], xs[a], s);
+    ++j;
+  }
+  return mdl[0] + s;
+}
+
+// Node model (M3): ridge LS over perm[lo, hi) on the features of `al`,
+// intercept unpenalised: centred normal equations (X_c'X_c + lambda I) w =
+// X_c'y_c by Cholesky, nref refinement steps from the rows, b = ybar - w.xbar.
+// Writes b, w into mdl; returns false if the factorisation broke down.
+__device__ bool m5_node_fit(const M5Work& W, int lo, int hi, unsigned long long al, const double* y, double lambda,
+                            int nref, double* mdl, int lane) {
+  const int m = hi - lo;
+  const int p = __popcll(al);
+  if (lane == 0) {
+    unsigned long long t = al;
+    for (int j = 0; j < p; ++j) {
+      W.fl[j] = __ffsll((long long)t) - 1;
+      t &= t - 1;
+    }
+  }
+  double ys = 0.0;
+  for (int k = lo + lane; k < hi; k += 32) ys += y[W.perm[k]];
+  const double ybar = warp_sum(ys) / (double)m;
+  __syncwarp();
+  if (p == 0) {
+    if (lane == 0) mdl[0] = ybar;
+    __syncwarp();
+    return true;
+  }
+  for (int j = lane; j < p; j += 32) {
+    const int a = W.fl[j];
+    double s = 0.0;
+    for (int k = lo; k < hi; ++k) s += W.Xs[W.perm[k] * W.ld + a];
+    W.xbar[j] = s / (double)m;
+  }
+  __syncwarp();
+  const int ne = p * (p + 1) / 2;
+  for (int e = lane; e < ne; e += 32) {
+    int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while ((i + 1) * (i + 2) / 2 <= e) ++i;
+    while (i * (i + 1) / 2 > e) --i;
+    const int j = e - i * (i + 1) / 2;
+    const int ai = W.fl[i], aj = W.fl[j];
+    const double xi = W.xbar[i], xj = W.xbar[j];
+    double s = 0.0;
+    for (int k = lo; k < hi; ++k) {
+      const double* xr = W.Xs + W.perm[k] * W.ld;
+      s = fma(xr[ai] - xi, xr[aj] - xj, s);
+    }
+    W.M[e] = s + (i == j ? lambda : 0.0);
+  }
+  for (int j = lane; j < p; j += 32) {
+    const int a = W.fl[j];
+    const double xj = W.xbar[j];
+    double s = 0.0;
+    for (int k = lo; k < hi; ++k) {
+      const int r = W.perm[k];
+      s = fma(W.Xs[r * W.ld + a] - xj, y[r] - ybar, s);
+    }
+    W.cv[j] = s;
+  }
+  __syncwarp();
+  if (!chol_packed(W.M, W.invd, p, lane)) return false;
+  chol_solve(W.M, W.invd, W.cv, p, lane);     // cv <- w
+  for (int it = 0; it < nref; ++it) {
+    for (int k = lo + lane; k < hi; k += 32) {   // residual of the centred system
+      const int r = W.perm[k];
+      const double* xr = W.Xs + r * W.ld;
+      double s = y[r] - ybar;
+      for (int j = 0; j < p; ++j) s = fma(-(xr[W.fl[j]] - W.xbar[j]), W.cv[j], s);
+      W.ev[k - lo] = s;
+    }
+    __syncwarp();
+    for (int j = lane; j < p; j += 32) {
+      const int a = W.fl[j];
+      const double xj = W.xbar[j];
+      double s = -lambda * W.cv[j];
+      for (int k = lo; k < hi; ++k) s = fma(W.Xs[W.perm[k] * W.ld + a] - xj, W.ev[k - lo], s);
+      W.dv[j] = s;
+    }
+    __syncwarp();
+    chol_solve(W.M, W.invd, W.dv, p, lane);
+    for (int j = lane; j < p; j += 32) W.cv[j] += W.dv[j];
+    __syncwarp();
+  }
+  double bp = 0.0;
+  for (int j = lane; j < p; j += 32) bp = fma(W.cv[j], W.xbar[j], bp);
+  const double b = ybar - warp_sum(bp);
+  for (int j = lane; j < p; j += 32) mdl[1 + j] = W.cv[j];
+  if (lane == 0) mdl[0] = b;
+  __syncwarp();
+  return true;
+}
+
+// Grow (M1, M2), fit + prune (M3, M4) the tree of one fit: n training rows
+// (scaled in W.Xs, labels y), deff features.  Returns the node count; *guard
+// gets the pruning decisions within tol of their boundary; *ok false if a
+// node factorisation broke down.
+__device__ int m5_build(const M5Work& W, int n, int deff, const double* y, double lambda, int nref, double tol,
+                        int lane, int* guard, bool* ok) {
+  for (int i = lane; i < n; i += 32) W.perm[i] = i;
+  if (lane == 0) {
+    W.nlo[0] = 0;
+    W.nhi[0] = n;
+    W.par[0] = -1;
+  }
+  __syncwarp();
+  const double sd_root = m5_sd(W.perm, 0, n, y);
+  const double sd_min = __dmul_rn(kM5SdFrac, sd_root);
+  int nn = 1;
+  #pragma unroll 1
+  for (int i = 0; i < nn; ++i) {
+    const int lo = W.nlo[i], hi = W.nhi[i];
+    bool split = false;
+    int ba = 0;
+    double bt = 0.0;
+    if (hi - lo >= kM5MinSplit) {
+      const double sdT = m5_sd(W.perm, lo, hi, y);
+      if (!(sdT < sd_min)) split = m5_best_split(W, lo, hi, deff, y, sdT, lane, ba, bt) > 0.0;
+    }
+    if (split) {
+      const int nL = m5_partition(W, lo, hi, ba, bt, lane);
+      if (lane == 0) {
+        W.feat[i] = ba;
+        W.thr[i] = bt;
+        W.left[i] = nn;
+        W.right[i] = nn + 1;
+        W.nlo[nn] = lo;
+        W.nhi[nn] = lo + nL;
+        W.par[nn] = i;
+        W.nlo[nn + 1] = lo + nL;
+        W.nhi[nn + 1] = hi;
+        W.par[nn + 1] = i;
+      }
+      nn += 2;
+    }
+    if (lane == 0) W.leaf[i] = split ? 0 : 1;
+    __syncwarp();
+  }
+  // allowed features (M3: split features of the grown subtree), pool offsets
+  if (lane == 0) {
+    for (int i = nn - 1; i >= 0; --i)
+      W.allow[i] = W.leaf[i] ? 0ull : (1ull << W.feat[i]) | W.allow[W.left[i]] | W.allow[W.right[i]];
+    int off = 0;
+    for (int i = 0; i < nn; ++i) {
+      W.moff[i] = off;
+      off += 1 + __popcll(W.allow[i]);
+    }
+  }
+  __syncwarp();
+  // models + pruning, post-order (M3, M4)
+  int g = 0;
+  bool good = true;
+  #pragma unroll 1
+  for (int i = nn - 1; i >= 0; --i) {
+    const int lo = W.nlo[i], hi = W.nhi[i], m = hi - lo;
+    const unsigned long long al = W.allow[i];
+    double* mdl = W.pool + W.moff[i];
+    good &= m5_node_fit(W, lo, hi, al, y, lambda, nref, mdl, lane);
+    double rs = 0.0;
+    for (int k = lo + lane; k < hi; k += 32) {
+      const int r = W.perm[k];
+      rs += fabs(y[r] - m5_row_value(W, mdl, al, W.Xs + r * W.ld));
+    }
+    const double resid = warp_sum(rs) / (double)m;
+    const int v = __popcll(al) + 1;
+    const double f = m > v ? (double)(m + v) / (double)(m - v) : 10.0;
+    const double own = resid * f;
+    if (lane == 0) {
+      if (W.leaf[i]) {
+        W.err[i] = own;
+      } else {
+        const int L = W.left[i], R = W.right[i];
+        const double sub = ((double)(W.nhi[L] - W.nlo[L]) * W.err[L] + (double)(W.nhi[R] - W.nlo[R]) * W.err[R]) /
+                           (double)m;
+        if (near_tol(own, sub, tol)) ++g;
+        if (own <= sub) {
+          W.leaf[i] = 1;     // prune to the node's model
+          W.err[i] = own;
+        } else {
+          W.err[i] = sub;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  *guard = __shfl_sync(FULL, g, 0);
+  *ok = good;
+  return nn;
+}
+
+// Value of node i's model at a raw test row xq (scaled on the fly exactly as
+// the training rows: (x - mn) / rg, reading D3).
+__device__ __forceinline__ double m5_test_value(const M5Work& W, int i, const double* xq, const int16_t* col,
+                                                const double* mnv, const double* rgv) {
+  const double* mdl = W.pool + W.moff[i];
+  unsigned long long al = W.allow[i];
+  double s = 0.0;
+  int j = 0;
+  while (al) {
+    const int a = __ffsll((long long)al) - 1;
+    al &= al - 1;
+    s = fma(mdl[1 + j], (xq[col[a]] - mnv[a]) / rgv[a], s);
+    ++j;
+  }
+  return mdl[0] + s;
+}
+
+// M5P prediction (M5): route x (x' <= thr left) to a leaf of the
+// pruned tree, then smooth root-ward p <- (n p + k q)/(n + k), n the count of
+// the node p came from, k = 15.
+__device__ double m5_predict(const M5Work& W, const double* xq, const int16_t* col, const double* mnv,
+                             const double* rgv) {
+  int i = 0;
+  while (!W.leaf[i]) {
+    const int a = W.feat[i];
+    const double xs = (xq[col[a]] - mnv[a]) / rgv[a];
+    i = xs <= W.thr[i] ? W.left[i] : W.right[i];
+  }
+  double p = m5_test_value(W, i, xq, col, mnv, rgv);
+  int nb = W.nhi[i] - W.nlo[i];
+  for (int a = W.par[i]; a >= 0; a = W.par[a]) {
+    const double q = m5_test_value(W, a, xq, col, mnv, rgv);
+    p = ((double)nb * p + kM5SmoothK * q) / ((double)nb + kM5SmoothK);
+    nb = W.nhi[a] - W.nlo[a];
+  }
+  return p;
+}
+
+}  // namespace speedrec

@@ -979,7 +979,7 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     return fail(c, SR_E_ARG, "evaluate: mask aggregation needs first/count multiples of n_splits=%lld",
                 (long long)c->sc.n_splits);
   if (agg && (prm->top_k < 1 || prm->top_k > 512)) return fail(c, SR_E_ARG, "evaluate: top_k=%d", prm->top_k);
-  if (prm->learner != SR_LINREG && prm->learner != SR_IBK)
+  if (prm->learner != SR_LINREG && prm->learner != SR_IBK && prm->learner != SR_M5P)
     return fail(c, SR_E_ARG, "evaluate: learner %d", prm->learner);
   if (prm->learner == SR_IBK && (prm->k_nn < 1 || prm->k_nn > kKnnMax))
     return fail(c, SR_E_ARG, "evaluate: k_nn=%d outside [1, %d]", prm->k_nn, kKnnMax);
@@ -1006,6 +1006,9 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
        })))
     return st;
   if (count == 0) return SR_OK;
+  if (prm->learner == SR_M5P && (G > kMaxGroups || C > kM5MaxFeatures))
+    return fail(c, SR_E_UNSUPPORTED, "evaluate: learner M5P needs <= %d groups and <= %d counters (G=%d, C=%d)",
+                kMaxGroups, kM5MaxFeatures, G, C);
   if (G > kMaxGroups) {
     if (agg) return fail(c, SR_E_UNSUPPORTED, "evaluate: mask aggregation needs <= %d groups", kMaxGroups);
     return evaluate_big(c, prm, first, count, out);
@@ -1024,7 +1027,7 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   if (const char* e = getenv("SPEEDREC_STAGE")) stage = atoi(e) && stage_bytes <= 96 * 1024;
   int wmax = kMaxWarpsPerBlock;
   if (const char* e = getenv("SPEEDREC_WMAX")) wmax = atoi(e) >= 16 ? 16 : 12;
-  if (prm->learner == SR_IBK || c->coef_req) wmax = 16;   // the one IBK / sr_fit instantiation
+  if (prm->learner != SR_LINREG || c->coef_req) wmax = 16;   // the one IBK / M5P / sr_fit instantiation
   int budget_cap = budget;
   if (const char* e = getenv("SPEEDREC_SMEM_KB")) budget_cap = std::min(budget, std::max(16, atoi(e)) * 1024);
   int mcap = std::min(mmax, 32);
@@ -1039,7 +1042,9 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   }
   if (wpb < 1) return fail(c, SR_E_UNSUPPORTED, "evaluate: per-warp workspace %d B exceeds shared memory", L.bytes);
   // global scratch for systems beyond the shared-memory factor: packed factor + 2 vectors
-  const long long mscr = (mmax > std::min(mcap, 32)) ? (long long)mmax * (mmax + 1) / 2 + 2LL * L.vmax : 0;
+  long long mscr = (mmax > std::min(mcap, 32)) ? (long long)mmax * (mmax + 1) / 2 + 2LL * L.vmax : 0;
+  // M5P: the tree workspace (scaled rows, nodes, model pool, node systems) per warp
+  if (prm->learner == SR_M5P) mscr = std::max(mscr, m5_scratch_doubles(c->np_tr, C));
 
   EvalArgs A{};
   A.x = (const double*)c->x.p;
@@ -1067,6 +1072,7 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.off_warps = head + (stage ? align16((int)stage_bytes) : 0);
   const int smem = A.off_warps + wpb * L.bytes;
   auto kfit = prm->learner == SR_IBK ? (stage ? k_fit_warp<16, 1, true> : k_fit_warp<16, 1, false>)
+              : prm->learner == SR_M5P ? (stage ? k_fit_warp<16, 3, true> : k_fit_warp<16, 3, false>)
               : c->coef_req      ? (stage ? k_fit_warp<16, 2, true> : k_fit_warp<16, 2, false>)
               : wmax == 16       ? (stage ? k_fit_warp<16, 0, true> : k_fit_warp<16, 0, false>)
                                  : (stage ? k_fit_warp<12, 0, true> : k_fit_warp<12, 0, false>);
@@ -1338,7 +1344,7 @@ sr_status sr_fit(sr_ctx* c, const sr_params* prm, int64_t scenario, double* coef
   c->err.clear();
   if (!prm || !coef_out) return fail(c, SR_E_ARG, "fit: null params or output");
   if (prm->learner != SR_LINREG)
-    return fail(c, SR_E_UNSUPPORTED, "fit: learner %d has no coefficients (IBK keeps its training set)", prm->learner);
+    return fail(c, SR_E_UNSUPPORTED, "fit: learner %d has no coefficient vector (IBK keeps its training set, M5P a tree)", prm->learner);
   if (!c->have_ds) return fail(c, SR_E_STATE, "fit: no dataset loaded");
   if (!c->have_sc) return fail(c, SR_E_STATE, "fit: no scenarios defined");
   const int O = c->O, C = c->C;

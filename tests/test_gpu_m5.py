@@ -1,0 +1,69 @@
+"""GPU parity of the NEXT-2 learner (M5P model tree, readings M1-M6)
+against the oracle (oracle/m5.py: exact-rational node models).
+
+The grown tree is decided with the same IEEE operations in the same order on
+both sides, so splits agree exactly; node models are FP64 Cholesky +
+refinement on the GPU vs exact rationals in the oracle, so EX and the ratio
+sums keep the 1e-9 relative bar, and scenarios with a pruning decision (or an
+EX) within 1e-9 of its boundary are guard cases (reading R21)."""
+import numpy as np
+import pytest
+
+import gen
+from oracle import m5
+from tests.parity import compare
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(cfg, first, count):
+    from paper_1910_07776_b200 import Context, default_params
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    got = ctx.evaluate(first, count, params=default_params(learner=2), want_ex=True)
+    ctx.close()
+    ref = m5.evaluate(cfg.dataset, cfg.scenarios, first, count)
+    return got, ref
+
+
+def _sub(r, idx):
+    return dict(opt=r["opt"][idx], scn=r["scn"][idx], ex=r["ex"][idx])
+
+
+def test_m5_c1_loo_all_folds():
+    cfg = gen.make_config("C1")
+    got, ref = _run(cfg, 0, 64)
+    print("M5P C1", compare(got, ref, max_guard_frac=0.05))
+
+
+def test_m5_c2_table2_sample():
+    cfg = gen.make_config("C2")
+    idx = list(range(0, 240, 9))
+    from paper_1910_07776_b200 import Context, default_params
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    got = ctx.evaluate(0, 240, params=default_params(learner=2), want_ex=True)
+    ctx.close()
+    refs = [m5.evaluate(cfg.dataset, cfg.scenarios, s, 1) for s in idx]
+    ref = dict(opt=np.concatenate([r["opt"] for r in refs]), scn=np.concatenate([r["scn"] for r in refs]),
+               ex=np.concatenate([r["ex"] for r in refs]))
+    print("M5P C2", compare(_sub(got, idx), ref, max_guard_frac=0.1))
+
+
+def test_m5_c3_ragged():
+    cfg = gen.make_config("C3", n_splits=2001)
+    got, ref = _run(cfg, 1931, 70)
+    print("M5P C3", compare(got, ref, max_guard_frac=0.05))
+
+
+def test_m5_needs_the_warp_path():
+    from paper_1910_07776_b200 import Context, SpeedrecError, default_params
+    cfg = gen.make_config("C4", n_splits=2)
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    with pytest.raises(SpeedrecError, match="M5P"):
+        ctx.evaluate(0, 1, params=default_params(learner=2))
+    ctx.close()
