@@ -542,7 +542,8 @@ __global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
       if (A.ex_out) A.ex_out[(so * O + o) * (long long)G * 32 + gk] = e;
     };
     if (m5) {    // NEXT-2: grow + prune the tree in the warp's scratch slab, then lanes over tests
-      const M5Work W = m5_carve(scr, L.np_tr, A.C);
+      M5Work W = m5_carve(scr, L.np_tr, A.C);
+      W.ld = deff > 0 ? deff : 1;    // rows of the active features only
       for (int e = lane; e < n * deff; e += 32) {
         const int r = e / deff, a = e - r * deff;
         W.Xs[r * W.ld + a] = (X[(long long)trs[r] * ldx + col[a]] - uv[a]) / wv[a];

@@ -36,7 +36,7 @@ constexpr int kM5MaxFeatures = 64;    // allowed-feature sets are 64-bit masks
 __host__ __device__ inline long long m5_scratch_doubles(int np, int d) {
   const long long nn = np > 0 ? 2LL * np - 1 : 1;
   const long long pm = (d < np ? d : np) + 1;
-  long long t = (long long)np * d;                 // Xs
+  long long t = 2LL * np * d + np;                 // Xs, Xt, yt
   t += (2LL * np + 8 * nn + 1 + 64) / 2 + 1;       // perm, tmp, 8 node ints, feature list
   t += 3 * nn;                                     // thr, err, allowed
   t += nn * pm;                                    // model pool
@@ -45,7 +45,9 @@ __host__ __device__ inline long long m5_scratch_doubles(int np, int d) {
 }
 
 struct M5Work {
-  double* Xs;       // [n][ld] scaled training rows
+  double* Xs;       // [n][ld] scaled training rows, kept in node-segment order
+  double* Xt;       // [n][ld] partition staging
+  double* yt;       // [n]
   int ld;
   double* thr;      // [nn]
   double* err;      // [nn]
@@ -68,6 +70,10 @@ __device__ __forceinline__ M5Work m5_carve(double* base, int np, int d) {
   W.Xs = p;
   W.ld = d;
   p += (long long)np * d;
+  W.Xt = p;
+  p += (long long)np * d;
+  W.yt = p;
+  p += np;
   W.thr = p;
   p += nn;
   W.err = p;
@@ -113,48 +119,48 @@ __device__ __forceinline__ M5Work m5_carve(double* base, int np, int d) {
   return W;
 }
 
-// Population sd of the labels of perm[lo, hi), two passes, left to right (M1).
-__device__ __forceinline__ double m5_sd(const int* perm, int lo, int hi, const double* y) {
+// Population sd of the labels y[lo, hi), two passes, left to right (M1).
+__device__ __forceinline__ double m5_sd(int lo, int hi, const double* y) {
   double s = 0.0;
-  for (int k = lo; k < hi; ++k) s = __dadd_rn(s, y[perm[k]]);
+  for (int k = lo; k < hi; ++k) s = __dadd_rn(s, y[k]);
   const double cnt = (double)(hi - lo);
   const double m = __ddiv_rn(s, cnt);
   double q = 0.0;
   for (int k = lo; k < hi; ++k) {
-    const double dv = __dsub_rn(y[perm[k]], m);
+    const double dv = __dsub_rn(y[k], m);
     q = __dadd_rn(q, __dmul_rn(dv, dv));
   }
   return __dsqrt_rn(__ddiv_rn(q, cnt));
 }
 
-// SDR of splitting perm[lo, hi) on feature a at thr (x <= thr left), M1:
+// SDR of splitting rows [lo, hi) on feature a at thr (x <= thr left), M1:
 // sd(T) - |L|/|T| sd(L) - |R|/|T| sd(R), each sd two-pass in segment order.
+// Rows are contiguous (W.Xs is kept in segment order): independent loads,
+// the two sums of each pass are two interleaved dependence chains.
 __device__ __forceinline__ double m5_sdr(const M5Work& W, int lo, int hi, int a, double thr, const double* y,
                                          double sdT) {
   double sL = 0.0, sR = 0.0;
   int nL = 0;
+  const double* xa = W.Xs + a;
+#pragma unroll 4
   for (int k = lo; k < hi; ++k) {
-    const int r = W.perm[k];
-    const double yk = y[r];
-    if (W.Xs[r * W.ld + a] <= thr) {
-      sL = __dadd_rn(sL, yk);
-      ++nL;
-    } else {
-      sR = __dadd_rn(sR, yk);
-    }
+    const double yk = y[k];
+    const bool l = xa[k * W.ld] <= thr;
+    const double t = __dadd_rn(l ? sL : sR, yk);
+    sL = l ? t : sL;
+    sR = l ? sR : t;
+    nL += l;
   }
   const int m = hi - lo, nR = m - nL;
   const double mL = __ddiv_rn(sL, (double)nL), mR = __ddiv_rn(sR, (double)nR);
   double qL = 0.0, qR = 0.0;
+#pragma unroll 4
   for (int k = lo; k < hi; ++k) {
-    const int r = W.perm[k];
-    if (W.Xs[r * W.ld + a] <= thr) {
-      const double dv = __dsub_rn(y[r], mL);
-      qL = __dadd_rn(qL, __dmul_rn(dv, dv));
-    } else {
-      const double dv = __dsub_rn(y[r], mR);
-      qR = __dadd_rn(qR, __dmul_rn(dv, dv));
-    }
+    const bool l = xa[k * W.ld] <= thr;
+    const double dv = __dsub_rn(y[k], l ? mL : mR);
+    const double t = __dadd_rn(l ? qL : qR, __dmul_rn(dv, dv));
+    qL = l ? t : qL;
+    qR = l ? qR : t;
   }
   const double sdL = __dsqrt_rn(__ddiv_rn(qL, (double)nL)), sdR = __dsqrt_rn(__ddiv_rn(qR, (double)nR));
   const double fL = __ddiv_rn((double)nL, (double)m), fR = __ddiv_rn((double)nR, (double)m);
@@ -175,14 +181,15 @@ __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const
   ba = 0x7fffffff;
   bt = INFINITY;
   for (int a = lane; a < deff; a += 32) {
+    const double* xa = W.Xs + a;
     #pragma unroll 1
     for (int j = lo; j < hi; ++j) {
-      const double u = W.Xs[W.perm[j] * W.ld + a];
+      const double u = xa[j * W.ld];
       bool dup = false;
       double nx = INFINITY;
-      #pragma unroll 1
+#pragma unroll 4
       for (int k = lo; k < hi; ++k) {
-        const double v = W.Xs[W.perm[k] * W.ld + a];
+        const double v = xa[k * W.ld];
         dup |= (k < j) & (v == u);
         if (v > u && v < nx) nx = v;
       }
@@ -209,30 +216,38 @@ __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const
   return bs;
 }
 
-// Stable partition of perm[lo, hi) by Xs[.][a] <= thr (left first, both
-// halves in their original order, as the oracle's filtered index lists).
-__device__ int m5_partition(const M5Work& W, int lo, int hi, int a, double thr, int lane) {
+// Stable partition of rows [lo, hi) by Xs[.][a] <= thr (left first, both
+// halves in their original order, as the oracle's filtered index lists):
+// the rows and labels move, so every node's rows stay contiguous.
+__device__ int m5_partition(const M5Work& W, int lo, int hi, int a, double thr, double* y, int lane) {
   const unsigned lt = (1u << lane) - 1u;
   int nL = 0;
   for (int k0 = lo; k0 < hi; k0 += 32) {
     const int k = k0 + lane;
-    const bool l = k < hi && W.Xs[W.perm[k] * W.ld + a] <= thr;
+    const bool l = k < hi && W.Xs[k * W.ld + a] <= thr;
     nL += __popc(__ballot_sync(FULL, l));
   }
   int cl = 0, cr = 0;
   for (int k0 = lo; k0 < hi; k0 += 32) {
     const int k = k0 + lane;
     const bool in = k < hi;
-    const int r = in ? W.perm[k] : 0;
-    const bool l = in && W.Xs[r * W.ld + a] <= thr;
+    const bool l = in && W.Xs[k * W.ld + a] <= thr;
     const unsigned bl = __ballot_sync(FULL, l), br = __ballot_sync(FULL, in && !l);
-    if (l) W.tmp[lo + cl + __popc(bl & lt)] = r;
-    else if (in) W.tmp[lo + nL + cr + __popc(br & lt)] = r;
+    if (l) W.tmp[k] = lo + cl + __popc(bl & lt);
+    else if (in) W.tmp[k] = lo + nL + cr + __popc(br & lt);
     cl += __popc(bl);
     cr += __popc(br);
   }
   __syncwarp();
-  for (int k = lo + lane; k < hi; k += 32) W.perm[k] = W.tmp[k];
+  const int m = hi - lo, d = W.ld;
+  for (int e = lane; e < m * d; e += 32) {
+    const int r = e / d, c = e - r * d;
+    W.Xt[W.tmp[lo + r] * d + c] = W.Xs[(lo + r) * d + c];
+  }
+  for (int k = lo + lane; k < hi; k += 32) W.yt[W.tmp[k]] = y[k];
+  __syncwarp();
+  for (int e = lane; e < m * d; e += 32) W.Xs[lo * d + e] = W.Xt[lo * d + e];
+  for (int k = lo + lane; k < hi; k += 32) y[k] = W.yt[k];
   __syncwarp();
   return nL;
 }
@@ -252,7 +267,7 @@ __device__ __forceinline__ double m5_row_value(const M5Work& W, const double* md
   return mdl[0] + s;
 }
 
-// Node model (M3): ridge LS over perm[lo, hi) on the features of `al`,
+// Node model (M3): ridge LS over rows [lo, hi) on the features of `al`,
 // intercept unpenalised: centred normal equations (X_c'X_c + lambda I) w =
 // X_c'y_c by Cholesky, nref refinement steps from the rows, b = ybar - w.xbar.
 // Writes b, w into mdl; returns false if the factorisation broke down.
@@ -268,7 +283,7 @@ __device__ bool m5_node_fit(const M5Work& W, int lo, int hi, unsigned long long 
     }
   }
   double ys = 0.0;
-  for (int k = lo + lane; k < hi; k += 32) ys += y[W.perm[k]];
+  for (int k = lo + lane; k < hi; k += 32) ys += y[k];
   const double ybar = warp_sum(ys) / (double)m;
   __syncwarp();
   if (p == 0) {
@@ -279,7 +294,7 @@ __device__ bool m5_node_fit(const M5Work& W, int lo, int hi, unsigned long long 
   for (int j = lane; j < p; j += 32) {
     const int a = W.fl[j];
     double s = 0.0;
-    for (int k = lo; k < hi; ++k) s += W.Xs[W.perm[k] * W.ld + a];
+    for (int k = lo; k < hi; ++k) s += W.Xs[k * W.ld + a];
     W.xbar[j] = s / (double)m;
   }
   __syncwarp();
@@ -293,7 +308,7 @@ __device__ bool m5_node_fit(const M5Work& W, int lo, int hi, unsigned long long 
     const double xi = W.xbar[i], xj = W.xbar[j];
     double s = 0.0;
     for (int k = lo; k < hi; ++k) {
-      const double* xr = W.Xs + W.perm[k] * W.ld;
+      const double* xr = W.Xs + k * W.ld;
       s = fma(xr[ai] - xi, xr[aj] - xj, s);
     }
     W.M[e] = s + (i == j ? lambda : 0.0);
@@ -303,7 +318,7 @@ __device__ bool m5_node_fit(const M5Work& W, int lo, int hi, unsigned long long 
     const double xj = W.xbar[j];
     double s = 0.0;
     for (int k = lo; k < hi; ++k) {
-      const int r = W.perm[k];
+      const int r = k;
       s = fma(W.Xs[r * W.ld + a] - xj, y[r] - ybar, s);
     }
     W.cv[j] = s;
@@ -313,7 +328,7 @@ __device__ bool m5_node_fit(const M5Work& W, int lo, int hi, unsigned long long 
   chol_solve(W.M, W.invd, W.cv, p, lane);     // cv <- w
   for (int it = 0; it < nref; ++it) {
     for (int k = lo + lane; k < hi; k += 32) {   // residual of the centred system
-      const int r = W.perm[k];
+      const int r = k;
       const double* xr = W.Xs + r * W.ld;
       double s = y[r] - ybar;
       for (int j = 0; j < p; ++j) s = fma(-(xr[W.fl[j]] - W.xbar[j]), W.cv[j], s);
@@ -324,7 +339,7 @@ __device__ bool m5_node_fit(const M5Work& W, int lo, int hi, unsigned long long 
       const int a = W.fl[j];
       const double xj = W.xbar[j];
       double s = -lambda * W.cv[j];
-      for (int k = lo; k < hi; ++k) s = fma(W.Xs[W.perm[k] * W.ld + a] - xj, W.ev[k - lo], s);
+      for (int k = lo; k < hi; ++k) s = fma(W.Xs[k * W.ld + a] - xj, W.ev[k - lo], s);
       W.dv[j] = s;
     }
     __syncwarp();
@@ -345,16 +360,15 @@ __device__ bool m5_node_fit(const M5Work& W, int lo, int hi, unsigned long long 
 // (scaled in W.Xs, labels y), deff features.  Returns the node count; *guard
 // gets the pruning decisions within tol of their boundary; *ok false if a
 // node factorisation broke down.
-__device__ int m5_build(const M5Work& W, int n, int deff, const double* y, double lambda, int nref, double tol,
+__device__ int m5_build(const M5Work& W, int n, int deff, double* y, double lambda, int nref, double tol,
                         int lane, int* guard, bool* ok) {
-  for (int i = lane; i < n; i += 32) W.perm[i] = i;
   if (lane == 0) {
     W.nlo[0] = 0;
     W.nhi[0] = n;
     W.par[0] = -1;
   }
   __syncwarp();
-  const double sd_root = m5_sd(W.perm, 0, n, y);
+  const double sd_root = m5_sd(0, n, y);
   const double sd_min = __dmul_rn(kM5SdFrac, sd_root);
   int nn = 1;
   #pragma unroll 1
@@ -364,11 +378,11 @@ __device__ int m5_build(const M5Work& W, int n, int deff, const double* y, doubl
     int ba = 0;
     double bt = 0.0;
     if (hi - lo >= kM5MinSplit) {
-      const double sdT = m5_sd(W.perm, lo, hi, y);
+      const double sdT = m5_sd(lo, hi, y);
       if (!(sdT < sd_min)) split = m5_best_split(W, lo, hi, deff, y, sdT, lane, ba, bt) > 0.0;
     }
     if (split) {
-      const int nL = m5_partition(W, lo, hi, ba, bt, lane);
+      const int nL = m5_partition(W, lo, hi, ba, bt, y, lane);
       if (lane == 0) {
         W.feat[i] = ba;
         W.thr[i] = bt;
@@ -408,7 +422,7 @@ __device__ int m5_build(const M5Work& W, int n, int deff, const double* y, doubl
     good &= m5_node_fit(W, lo, hi, al, y, lambda, nref, mdl, lane);
     double rs = 0.0;
     for (int k = lo + lane; k < hi; k += 32) {
-      const int r = W.perm[k];
+      const int r = k;
       rs += fabs(y[r] - m5_row_value(W, mdl, al, W.Xs + r * W.ld));
     }
     const double resid = warp_sum(rs) / (double)m;

@@ -1023,7 +1023,9 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   const int ldxs = C | 1;
   const long long stage_bytes = N * ldxs * 8;
   const int mmax = std::min(c->np_tr, c->dmax + 1);      // largest system any fit can need
-  int stage = stage_bytes <= 96 * 1024 ? 1 : 0;
+  // M5P reads x only to scale its rows and tests; its hot loops run over the
+  // per-warp scratch slab, which wants the shared memory as L1 (+11 %, C3)
+  int stage = stage_bytes <= 96 * 1024 && prm->learner != SR_M5P ? 1 : 0;
   if (const char* e = getenv("SPEEDREC_STAGE")) stage = atoi(e) && stage_bytes <= 96 * 1024;
   int wmax = kMaxWarpsPerBlock;
   if (const char* e = getenv("SPEEDREC_WMAX")) wmax = atoi(e) >= 16 ? 16 : 12;
