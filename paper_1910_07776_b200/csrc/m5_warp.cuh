@@ -171,6 +171,65 @@ __device__ __forceinline__ bool m5_better(double s, int a, double t, double bs, 
   return s > bs || (s == bs && (a < ba || (a == ba && t < bt)));
 }
 
+// SDR (as m5_sdr) of NC candidate thresholds of one feature in one pair of
+// passes: the row loads are shared and the 2 NC sums of a pass are
+// independent dependence chains (latency, not issue, bounds this loop).
+template <int NC>
+__device__ __forceinline__ void m5_sdr_n(const M5Work& W, int lo, int hi, int a, const double (&t)[NC],
+                                         const double* y, double sdT, double (&s)[NC]) {
+  double sL[NC], sR[NC], mL[NC], mR[NC];
+  int nL[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    sL[c] = sR[c] = 0.0;
+    nL[c] = 0;
+  }
+  const double* xa = W.Xs + a;
+#pragma unroll 2
+  for (int k = lo; k < hi; ++k) {
+    const double yk = y[k], x = xa[k * W.ld];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const bool l = x <= t[c];
+      const double u = __dadd_rn(l ? sL[c] : sR[c], yk);
+      sL[c] = l ? u : sL[c];
+      sR[c] = l ? sR[c] : u;
+      nL[c] += l;
+    }
+  }
+  const int m = hi - lo;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    mL[c] = __ddiv_rn(sL[c], (double)nL[c]);
+    mR[c] = __ddiv_rn(sR[c], (double)(m - nL[c]));
+    sL[c] = sR[c] = 0.0;     // now the squared-deviation sums
+  }
+#pragma unroll 2
+  for (int k = lo; k < hi; ++k) {
+    const double yk = y[k], x = xa[k * W.ld];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const bool l = x <= t[c];
+      const double dv = __dsub_rn(yk, l ? mL[c] : mR[c]);
+      const double u = __dadd_rn(l ? sL[c] : sR[c], __dmul_rn(dv, dv));
+      sL[c] = l ? u : sL[c];
+      sR[c] = l ? sR[c] : u;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int nR = m - nL[c];
+    const double sdL = __dsqrt_rn(__ddiv_rn(sL[c], (double)nL[c])), sdR = __dsqrt_rn(__ddiv_rn(sR[c], (double)nR));
+    const double fL = __ddiv_rn((double)nL[c], (double)m), fR = __ddiv_rn((double)nR, (double)m);
+    s[c] = __dsub_rn(__dsub_rn(sdT, __dmul_rn(fL, sdL)), __dmul_rn(fR, sdR));
+  }
+}
+
+#ifndef SR_M5_CAND
+#define SR_M5_CAND 1
+#endif
+constexpr int kM5Cand = SR_M5_CAND;   // candidate thresholds per pass pair (A/B: -DSR_M5_CAND; 1 is fastest, profiles/r1u_ab_m5_cand.txt)
+
 // Best split of node segment [lo, hi) (M1): lanes over features, candidates =
 // midpoints between adjacent distinct values, key (SDR desc, feature asc,
 // threshold asc) -- the oracle's first strict maximum in (feature, threshold)
@@ -183,24 +242,40 @@ __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const
   for (int a = lane; a < deff; a += 32) {
     const double* xa = W.Xs + a;
     #pragma unroll 1
-    for (int j = lo; j < hi; ++j) {
-      const double u = xa[j * W.ld];
-      bool dup = false;
-      double nx = INFINITY;
+    for (int j = lo; j < hi; j += kM5Cand) {
+      double u[kM5Cand], nx[kM5Cand], t[kM5Cand], s[kM5Cand];
+      bool dup[kM5Cand];
+#pragma unroll
+      for (int c = 0; c < kM5Cand; ++c) {
+        u[c] = j + c < hi ? xa[(j + c) * W.ld] : INFINITY;   // INFINITY: no candidate
+        nx[c] = INFINITY;
+        dup[c] = false;
+      }
 #pragma unroll 4
       for (int k = lo; k < hi; ++k) {
         const double v = xa[k * W.ld];
-        dup |= (k < j) & (v == u);
-        if (v > u && v < nx) nx = v;
+#pragma unroll
+        for (int c = 0; c < kM5Cand; ++c) {
+          dup[c] |= (k < j + c) & (v == u[c]);
+          if (v > u[c] && v < nx[c]) nx[c] = v;
+        }
       }
-      if (dup || nx == INFINITY) continue;
-      const double t = __dmul_rn(__dadd_rn(u, nx), 0.5);   // (lo + hi) / 2
-      const double s = m5_sdr(W, lo, hi, a, t, y, sdT);
-      if (m5_better(s, a, t, bs, ba, bt)) {
-        bs = s;
-        ba = a;
-        bt = t;
+      bool any = false;
+#pragma unroll
+      for (int c = 0; c < kM5Cand; ++c) {
+        dup[c] = dup[c] || nx[c] == INFINITY;       // not a candidate
+        t[c] = dup[c] ? u[0] : __dmul_rn(__dadd_rn(u[c], nx[c]), 0.5);   // (lo + hi) / 2
+        any |= !dup[c];
       }
+      if (!any) continue;
+      m5_sdr_n<kM5Cand>(W, lo, hi, a, t, y, sdT, s);
+#pragma unroll
+      for (int c = 0; c < kM5Cand; ++c)
+        if (!dup[c] && m5_better(s[c], a, t[c], bs, ba, bt)) {
+          bs = s[c];
+          ba = a;
+          bt = t[c];
+        }
     }
   }
 #pragma unroll
