@@ -67,3 +67,31 @@ def test_m5_needs_the_warp_path():
     with pytest.raises(SpeedrecError, match="M5P"):
         ctx.evaluate(0, 1, params=default_params(learner=2))
     ctx.close()
+
+
+def test_m5_c5_feature_masks_and_aggregation():
+    """C5 under M5P (warp path with per-mask aggregation): sampled scenarios
+    (feature subsets of counters 0..3, LOO folds) vs the oracle, and the fused
+    per-mask sums / top-K ranking equal to the aggregation of the per-scenario
+    rows."""
+    import oracle
+    from paper_1910_07776_b200 import Context, default_params
+    cfg = gen.make_config("C5", n_masks_k=4)          # 16 masks x 128 folds
+    folds, n = cfg.scenarios.n_splits, cfg.scenarios.n_scenarios
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    p = default_params(learner=2, top_k=8)
+    got = ctx.evaluate(0, n, params=p, want_ex=True)
+    agg = ctx.evaluate(0, n, params=p, want_masks=True, per_scenario=False, n_folds=folds)
+    ctx.close()
+    idx = sorted({int(v) for v in np.random.default_rng(5).integers(0, n, size=40)} | {0, n - 1})
+    refs = [m5.evaluate(cfg.dataset, cfg.scenarios, s, 1) for s in idx]
+    ref = dict(opt=np.concatenate([r["opt"] for r in refs]), scn=np.concatenate([r["scn"] for r in refs]),
+               ex=np.concatenate([r["ex"] for r in refs]))
+    print("M5P C5", compare(_sub(got, idx), ref, max_guard_frac=0.1))
+    assert got["scn"]["n_guard"].sum() == 0
+    rows, top = oracle.aggregate_masks(got["opt"], got["scn"], folds, top_k=8)
+    for f in rows.dtype.names:
+        assert np.array_equal(agg["masks"][f], rows[f]), f
+    assert list(agg["top"][:len(top)]) == list(top)
