@@ -273,7 +273,13 @@ __device__ __forceinline__ void rank_scenario(const EvalArgs& A, long long sl, i
 // STAGED: x staged in shared memory (compile-time, so every x access is an
 // LDS rather than a generic load).
 template <int WMAX, int MODE, bool STAGED>
-__global__ void __launch_bounds__(WMAX * 32, 1) k_fit_warp(const EvalArgs A) {
+#ifndef SR_M5_MINB
+#define SR_M5_MINB 1      // M5P: resident CTAs per SM the register budget is cut for (A/B knob)
+#endif
+#ifndef SR_M5_WMAX
+#define SR_M5_WMAX 16     // M5P: warps per CTA
+#endif
+__global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_warp(const EvalArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const WarpLayout& L = A.L;
   int8_t* obit = reinterpret_cast<int8_t*>(smem);

@@ -1030,6 +1030,7 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   int wmax = kMaxWarpsPerBlock;
   if (const char* e = getenv("SPEEDREC_WMAX")) wmax = atoi(e) >= 16 ? 16 : 12;
   if (prm->learner != SR_LINREG || c->coef_req) wmax = 16;   // the one IBK / M5P / sr_fit instantiation
+  if (prm->learner == SR_M5P) wmax = SR_M5_WMAX;
   int budget_cap = budget;
   if (const char* e = getenv("SPEEDREC_SMEM_KB")) budget_cap = std::min(budget, std::max(16, atoi(e)) * 1024);
   int mcap = std::min(mmax, 32);
@@ -1074,7 +1075,7 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.off_warps = head + (stage ? align16((int)stage_bytes) : 0);
   const int smem = A.off_warps + wpb * L.bytes;
   auto kfit = prm->learner == SR_IBK ? (stage ? k_fit_warp<16, 1, true> : k_fit_warp<16, 1, false>)
-              : prm->learner == SR_M5P ? (stage ? k_fit_warp<16, 3, true> : k_fit_warp<16, 3, false>)
+              : prm->learner == SR_M5P ? (stage ? k_fit_warp<SR_M5_WMAX, 3, true> : k_fit_warp<SR_M5_WMAX, 3, false>)
               : c->coef_req      ? (stage ? k_fit_warp<16, 2, true> : k_fit_warp<16, 2, false>)
               : wmax == 16       ? (stage ? k_fit_warp<16, 0, true> : k_fit_warp<16, 0, false>)
                                  : (stage ? k_fit_warp<12, 0, true> : k_fit_warp<12, 0, false>);
