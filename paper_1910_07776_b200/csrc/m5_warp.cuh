@@ -133,149 +133,88 @@ __device__ __forceinline__ double m5_sd(int lo, int hi, const double* y) {
   return __dsqrt_rn(__ddiv_rn(q, cnt));
 }
 
-// SDR of splitting rows [lo, hi) on feature a at thr (x <= thr left), M1:
-// sd(T) - |L|/|T| sd(L) - |R|/|T| sd(R), each sd two-pass in segment order.
-// Rows are contiguous (W.Xs is kept in segment order): independent loads,
-// the two sums of each pass are two interleaved dependence chains.
-__device__ __forceinline__ double m5_sdr(const M5Work& W, int lo, int hi, int a, double thr, const double* y,
-                                         double sdT) {
-  double sL = 0.0, sR = 0.0;
-  int nL = 0;
-  const double* xa = W.Xs + a;
-#pragma unroll 4
-  for (int k = lo; k < hi; ++k) {
-    const double yk = y[k];
-    const bool l = xa[k * W.ld] <= thr;
-    const double t = __dadd_rn(l ? sL : sR, yk);
-    sL = l ? t : sL;
-    sR = l ? sR : t;
-    nL += l;
-  }
-  const int m = hi - lo, nR = m - nL;
-  const double mL = __ddiv_rn(sL, (double)nL), mR = __ddiv_rn(sR, (double)nR);
-  double qL = 0.0, qR = 0.0;
-#pragma unroll 4
-  for (int k = lo; k < hi; ++k) {
-    const bool l = xa[k * W.ld] <= thr;
-    const double dv = __dsub_rn(y[k], l ? mL : mR);
-    const double t = __dadd_rn(l ? qL : qR, __dmul_rn(dv, dv));
-    qL = l ? t : qL;
-    qR = l ? qR : t;
-  }
-  const double sdL = __dsqrt_rn(__ddiv_rn(qL, (double)nL)), sdR = __dsqrt_rn(__ddiv_rn(qR, (double)nR));
-  const double fL = __ddiv_rn((double)nL, (double)m), fR = __ddiv_rn((double)nR, (double)m);
-  return __dsub_rn(__dsub_rn(sdT, __dmul_rn(fL, sdL)), __dmul_rn(fR, sdR));
-}
-
 __device__ __forceinline__ bool m5_better(double s, int a, double t, double bs, int ba, double bt) {
   return s > bs || (s == bs && (a < ba || (a == ba && t < bt)));
 }
-
-// SDR (as m5_sdr) of NC candidate thresholds of one feature in one pair of
-// passes: the row loads are shared and the 2 NC sums of a pass are
-// independent dependence chains (latency, not issue, bounds this loop).
-template <int NC>
-__device__ __forceinline__ void m5_sdr_n(const M5Work& W, int lo, int hi, int a, const double (&t)[NC],
-                                         const double* y, double sdT, double (&s)[NC]) {
-  double sL[NC], sR[NC], mL[NC], mR[NC];
-  int nL[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    sL[c] = sR[c] = 0.0;
-    nL[c] = 0;
-  }
-  const double* xa = W.Xs + a;
-#pragma unroll 2
-  for (int k = lo; k < hi; ++k) {
-    const double yk = y[k], x = xa[k * W.ld];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const bool l = x <= t[c];
-      const double u = __dadd_rn(l ? sL[c] : sR[c], yk);
-      sL[c] = l ? u : sL[c];
-      sR[c] = l ? sR[c] : u;
-      nL[c] += l;
-    }
-  }
-  const int m = hi - lo;
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    mL[c] = __ddiv_rn(sL[c], (double)nL[c]);
-    mR[c] = __ddiv_rn(sR[c], (double)(m - nL[c]));
-    sL[c] = sR[c] = 0.0;     // now the squared-deviation sums
-  }
-#pragma unroll 2
-  for (int k = lo; k < hi; ++k) {
-    const double yk = y[k], x = xa[k * W.ld];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const bool l = x <= t[c];
-      const double dv = __dsub_rn(yk, l ? mL[c] : mR[c]);
-      const double u = __dadd_rn(l ? sL[c] : sR[c], __dmul_rn(dv, dv));
-      sL[c] = l ? u : sL[c];
-      sR[c] = l ? sR[c] : u;
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int nR = m - nL[c];
-    const double sdL = __dsqrt_rn(__ddiv_rn(sL[c], (double)nL[c])), sdR = __dsqrt_rn(__ddiv_rn(sR[c], (double)nR));
-    const double fL = __ddiv_rn((double)nL[c], (double)m), fR = __ddiv_rn((double)nR, (double)m);
-    s[c] = __dsub_rn(__dsub_rn(sdT, __dmul_rn(fL, sdL)), __dmul_rn(fR, sdR));
-  }
-}
-
-#ifndef SR_M5_CAND
-#define SR_M5_CAND 1
-#endif
-constexpr int kM5Cand = SR_M5_CAND;   // candidate thresholds per pass pair (A/B: -DSR_M5_CAND; 1 is fastest, profiles/r1u_ab_m5_cand.txt)
 
 // Best split of node segment [lo, hi) (M1): lanes over features, candidates =
 // midpoints between adjacent distinct values, key (SDR desc, feature asc,
 // threshold asc) -- the oracle's first strict maximum in (feature, threshold)
 // order.  Returns the SDR (-inf: no candidate); ba / bt the split.
+//
+// Row j's value u is a candidate's lower end iff it is its value's first
+// occurrence and some value exceeds it; the threshold is (u + next)/2.  No
+// value lies strictly between u and next, so "x <= u" is the same partition
+// as "x <= threshold" whenever the rounded threshold is below next (always,
+// unless u and next are adjacent doubles: then the pass is redone with the
+// threshold itself, as the oracle compares): the first SDR pass (left/right label sums in segment
+// order) runs fused with the distinct / next-greater scan, and the second
+// (squared deviations) only for real candidates -- two O(m) passes per row
+// instead of three, the same IEEE operations in the same order as the
+// oracle's sd_pop over the filtered lists.
 __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const double* y, double sdT, int lane,
                                 int& ba, double& bt) {
   double bs = -INFINITY;
   ba = 0x7fffffff;
   bt = INFINITY;
+  const int m = hi - lo;
+  const double* yv = y + lo;
   for (int a = lane; a < deff; a += 32) {
-    const double* xa = W.Xs + a;
+    const double* xa = W.Xs + lo * W.ld + a;
+    const int ld = W.ld;
     #pragma unroll 1
-    for (int j = lo; j < hi; j += kM5Cand) {
-      double u[kM5Cand], nx[kM5Cand], t[kM5Cand], s[kM5Cand];
-      bool dup[kM5Cand];
-#pragma unroll
-      for (int c = 0; c < kM5Cand; ++c) {
-        u[c] = j + c < hi ? xa[(j + c) * W.ld] : INFINITY;   // INFINITY: no candidate
-        nx[c] = INFINITY;
-        dup[c] = false;
+    for (int j = 0; j < m; ++j) {
+      const double u = xa[j * ld];
+      bool dup = false;
+      double nx = INFINITY, sL = 0.0, sR = 0.0;
+      int nL = 0;
+#pragma unroll 2
+      for (int k = 0; k < m; ++k) {
+        const double v = xa[k * ld], yk = yv[k];
+        dup |= (k < j) & (v == u);
+        nx = (v > u && v < nx) ? v : nx;
+        const bool l = v <= u;
+        const double t = __dadd_rn(l ? sL : sR, yk);
+        sL = l ? t : sL;
+        sR = l ? sR : t;
+        nL += l;
       }
-#pragma unroll 4
-      for (int k = lo; k < hi; ++k) {
-        const double v = xa[k * W.ld];
-#pragma unroll
-        for (int c = 0; c < kM5Cand; ++c) {
-          dup[c] |= (k < j + c) & (v == u[c]);
-          if (v > u[c] && v < nx[c]) nx[c] = v;
+      if (dup || nx == INFINITY) continue;
+      const double thr = __dmul_rn(__dadd_rn(u, nx), 0.5);   // (lo + hi) / 2
+      double cut = u;
+      if (!(thr < nx)) {   // u, nx adjacent doubles and the midpoint rounded up: x <= thr takes nx too
+        cut = thr;
+        sL = sR = 0.0;
+        nL = 0;
+        for (int k = 0; k < m; ++k) {
+          const bool l = xa[k * ld] <= cut;
+          const double t = __dadd_rn(l ? sL : sR, yv[k]);
+          sL = l ? t : sL;
+          sR = l ? sR : t;
+          nL += l;
         }
+        if (nL == m) continue;   // unreachable for distinct finite values; keeps the sds defined
       }
-      bool any = false;
-#pragma unroll
-      for (int c = 0; c < kM5Cand; ++c) {
-        dup[c] = dup[c] || nx[c] == INFINITY;       // not a candidate
-        t[c] = dup[c] ? u[0] : __dmul_rn(__dadd_rn(u[c], nx[c]), 0.5);   // (lo + hi) / 2
-        any |= !dup[c];
+      const int nR = m - nL;
+      const double mL = __ddiv_rn(sL, (double)nL), mR = __ddiv_rn(sR, (double)nR);
+      double qL = 0.0, qR = 0.0;
+#pragma unroll 2
+      for (int k = 0; k < m; ++k) {
+        const double v = xa[k * ld];
+        const bool l = v <= cut;
+        const double dv = __dsub_rn(yv[k], l ? mL : mR);
+        const double t = __dadd_rn(l ? qL : qR, __dmul_rn(dv, dv));
+        qL = l ? t : qL;
+        qR = l ? qR : t;
       }
-      if (!any) continue;
-      m5_sdr_n<kM5Cand>(W, lo, hi, a, t, y, sdT, s);
-#pragma unroll
-      for (int c = 0; c < kM5Cand; ++c)
-        if (!dup[c] && m5_better(s[c], a, t[c], bs, ba, bt)) {
-          bs = s[c];
-          ba = a;
-          bt = t[c];
-        }
+      const double sdL = __dsqrt_rn(__ddiv_rn(qL, (double)nL)), sdR = __dsqrt_rn(__ddiv_rn(qR, (double)nR));
+      const double fL = __ddiv_rn((double)nL, (double)m), fR = __ddiv_rn((double)nR, (double)m);
+      const double sdr = __dsub_rn(__dsub_rn(sdT, __dmul_rn(fL, sdL)), __dmul_rn(fR, sdR));
+      if (m5_better(sdr, a, thr, bs, ba, bt)) {
+        bs = sdr;
+        ba = a;
+        bt = thr;
+      }
     }
   }
 #pragma unroll
