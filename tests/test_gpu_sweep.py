@@ -16,7 +16,11 @@ pytestmark = pytest.mark.gpu
 
 def _oracle_sweep(cfg, first, count, thr, cnt, learner=0, k=10):
     ds, sc = cfg.dataset, cfg.scenarios
-    ref = oracle.evaluate(ds, sc, first, count, want_ex=True, learner=learner, k_nn=k)
+    if learner == 2:      # M5P (NEXT-2): the model-tree oracle
+        from oracle import m5
+        ref = m5.evaluate(ds, sc, first, count)
+    else:
+        ref = oracle.evaluate(ds, sc, first, count, want_ex=True, learner=learner, k_nn=k)
     assert ref["scn"]["n_guard"].sum() == 0
     G, O = ds.n_groups, ds.n_opt_ids
     rt = ds.runtime_ms
@@ -53,6 +57,7 @@ def _oracle_sweep(cfg, first, count, thr, cnt, learner=0, k=10):
     ("C2", {}, 240, 0),
     ("C3", dict(n_splits=300), 300, 0),
     ("C1", {}, 64, 1),
+    ("C1", {}, 64, 2),
 ])
 def test_sweep_matches_the_rule_applied_per_setting(name, kw, count, learner):
     from paper_1910_07776_b200 import Context, default_params
