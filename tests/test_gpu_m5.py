@@ -123,3 +123,21 @@ def test_m5_adjacent_double_thresholds():
     st = compare(got, ref, max_guard_frac=0.5)
     assert st["n"] - st["guarded"] >= 32
     print("M5P adjacent", st)
+
+
+def test_m5_bh6_sampled():
+    """Barnes-Hut with all six Table-1 inputs (config BH6, Table-2 Exp 1-4,
+    training sets of 32-96 pairs): sampled scenarios vs the oracle."""
+    from paper_1910_07776_b200 import Context, default_params
+    cfg = gen.make_config("BH6")
+    n = cfg.scenarios.n_scenarios
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    got = ctx.evaluate(0, n, params=default_params(learner=2), want_ex=True)
+    ctx.close()
+    idx = [0, 1, 37, 71, 100, 143]
+    refs = [m5.evaluate(cfg.dataset, cfg.scenarios, s, 1) for s in idx]
+    ref = dict(opt=np.concatenate([r["opt"] for r in refs]), scn=np.concatenate([r["scn"] for r in refs]),
+               ex=np.concatenate([r["ex"] for r in refs]))
+    print("M5P BH6", compare(_sub(got, idx), ref, max_guard_frac=0.2))
