@@ -135,7 +135,8 @@ def run_reference(args, cfg, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "scenario_evals/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sample / v,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+quad",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64+rational" if args.learner == "m5" else "f64+quad",
         "data": "synthetic", "config": workload_config(cfg, args, sample),
         "cpu_baseline": {"value": v, "unit": "scenario_evals/s", "cores": oracle_cores(threads, LEARNERS[args.learner]),
                          "kind": "oracle",
@@ -257,8 +258,10 @@ def main():
     ap.add_argument("--learner", default="linreg", choices=list(LEARNERS),
                     help="linreg = ridge LS (the paper's model); ibk = the NEXT-1 k-NN learner; "
                          "m5 = the NEXT-2 M5P model tree")
-    ap.add_argument("--ref-sample", type=int, default=4000)
-    ap.add_argument("--cpu-sample", type=int, default=4000)
+    ap.add_argument("--ref-sample", type=int, default=None,
+                    help="scenarios per reference-arm step (default 4000; 32 for the Python M5P oracle)")
+    ap.add_argument("--cpu-sample", type=int, default=None,
+                    help="scenarios of the cpu_baseline sample (default 4000; 32 for the Python M5P oracle)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg (tuning runs)")
     ap.add_argument("--no-extra", action="store_true",
@@ -266,6 +269,11 @@ def main():
     ap.add_argument("--sweep", type=int, default=0,
                     help="NEXT-3: time sr_sweep with this many thresholds x 4 list lengths instead of sr_evaluate")
     args = ap.parse_args()
+    small = args.learner == "m5"            # the exact-rational Python oracle is ~1e4x slower
+    if args.ref_sample is None:
+        args.ref_sample = 32 if small else 4000
+    if args.cpu_sample is None:
+        args.cpu_sample = 32 if small else 4000
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
