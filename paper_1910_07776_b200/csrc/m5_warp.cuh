@@ -31,6 +31,9 @@ constexpr int kM5MinSplit = 4;        // M2: |T| < 4 -> leaf
 constexpr double kM5SdFrac = 0.05;    // M2: sd(T) < 5 % of sd(root) -> leaf
 constexpr double kM5SmoothK = 15.0;   // M5: Quinlan's smoothing constant
 constexpr int kM5MaxFeatures = 64;    // allowed-feature sets are 64-bit masks
+#ifndef SR_M5_UNROLL
+#define SR_M5_UNROLL 2                // split-search row loops (A/B knob)
+#endif
 
 // Scratch doubles one warp needs for fits of <= np training pairs, <= d features.
 __host__ __device__ inline long long m5_scratch_doubles(int np, int d) {
@@ -168,7 +171,7 @@ __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const
       bool dup = false;
       double nx = INFINITY, sL = 0.0, sR = 0.0;
       int nL = 0;
-#pragma unroll 2
+SR_UNROLL(SR_M5_UNROLL)
       for (int k = 0; k < m; ++k) {
         const double v = xa[k * ld], yk = yv[k];
         dup |= (k < j) & (v == u);
@@ -198,7 +201,7 @@ __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const
       const int nR = m - nL;
       const double mL = __ddiv_rn(sL, (double)nL), mR = __ddiv_rn(sR, (double)nR);
       double qL = 0.0, qR = 0.0;
-#pragma unroll 2
+SR_UNROLL(SR_M5_UNROLL)
       for (int k = 0; k < m; ++k) {
         const double v = xa[k * ld];
         const bool l = v <= cut;
