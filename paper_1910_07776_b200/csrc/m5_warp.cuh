@@ -162,6 +162,9 @@ __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const
   bt = INFINITY;
   const int m = hi - lo;
   const double* yv = y + lo;
+  double* frac = W.ev;      // |L|/|T| = k/m for k < m (W.ev is free while the tree grows)
+  for (int k = lane; k < m; k += 32) frac[k] = __ddiv_rn((double)k, (double)m);
+  __syncwarp();
   for (int a = lane; a < deff; a += 32) {
     const double* xa = W.Xs + lo * W.ld + a;
     const int ld = W.ld;
@@ -211,7 +214,7 @@ SR_UNROLL(SR_M5_UNROLL)
         qR = l ? qR : t;
       }
       const double sdL = __dsqrt_rn(__ddiv_rn(qL, (double)nL)), sdR = __dsqrt_rn(__ddiv_rn(qR, (double)nR));
-      const double fL = __ddiv_rn((double)nL, (double)m), fR = __ddiv_rn((double)nR, (double)m);
+      const double fL = frac[nL], fR = frac[nR];
       const double sdr = __dsub_rn(__dsub_rn(sdT, __dmul_rn(fL, sdL)), __dmul_rn(fR, sdR));
       if (m5_better(sdr, a, thr, bs, ba, bt)) {
         bs = sdr;
