@@ -155,6 +155,70 @@ __device__ __forceinline__ bool m5_better(double s, int a, double t, double bs, 
 // (squared deviations) only for real candidates -- two O(m) passes per row
 // instead of three, the same IEEE operations in the same order as the
 // oracle's sd_pop over the filtered lists.
+// Second SDR pass and score of one candidate (left sums sL, sR, count nL of
+// the partition x <= cut), as the oracle's sd_pop of the two filtered lists.
+__device__ __forceinline__ double m5_score(const double* xa, int ld, const double* yv, int m, double cut, double sL,
+                                           double sR, int nL, const double* frac, double sdT) {
+  const int nR = m - nL;
+  const double mL = __ddiv_rn(sL, (double)nL), mR = __ddiv_rn(sR, (double)nR);
+  double qL = 0.0, qR = 0.0;
+SR_UNROLL(SR_M5_UNROLL)
+  for (int k = 0; k < m; ++k) {
+    const double v = xa[k * ld];
+    const bool l = v <= cut;
+    const double dv = __dsub_rn(yv[k], l ? mL : mR);
+    const double t = __dadd_rn(l ? qL : qR, __dmul_rn(dv, dv));
+    qL = l ? t : qL;
+    qR = l ? qR : t;
+  }
+  const double sdL = __dsqrt_rn(__ddiv_rn(qL, (double)nL)), sdR = __dsqrt_rn(__ddiv_rn(qR, (double)nR));
+  return __dsub_rn(__dsub_rn(sdT, __dmul_rn(frac[nL], sdL)), __dmul_rn(frac[nR], sdR));
+}
+
+// Candidate at row j (see m5_best_split): false if none; else its SDR and threshold.
+__device__ __forceinline__ bool m5_candidate(const double* xa, int ld, const double* yv, int m, int j,
+                                             const double* frac, double sdT, double& sdr, double& thr) {
+  const double u = xa[j * ld];
+  bool dup = false;
+  double nx = INFINITY, sL = 0.0, sR = 0.0;
+  int nL = 0;
+SR_UNROLL(SR_M5_UNROLL)
+  for (int k = 0; k < m; ++k) {
+    const double v = xa[k * ld], yk = yv[k];
+    dup |= (k < j) & (v == u);
+    nx = (v > u && v < nx) ? v : nx;
+    const bool l = v <= u;
+    const double t = __dadd_rn(l ? sL : sR, yk);
+    sL = l ? t : sL;
+    sR = l ? sR : t;
+    nL += l;
+  }
+  if (dup || nx == INFINITY) return false;
+  thr = __dmul_rn(__dadd_rn(u, nx), 0.5);   // (lo + hi) / 2
+  double cut = u;
+  if (!(thr < nx)) {   // u, nx adjacent doubles and the midpoint rounded up: x <= thr takes nx too
+    cut = thr;
+    sL = sR = 0.0;
+    nL = 0;
+    for (int k = 0; k < m; ++k) {
+      const bool l = xa[k * ld] <= cut;
+      const double t = __dadd_rn(l ? sL : sR, yv[k]);
+      sL = l ? t : sL;
+      sR = l ? sR : t;
+      nL += l;
+    }
+    if (nL == m) return false;   // unreachable for distinct finite values; keeps the sds defined
+  }
+  sdr = m5_score(xa, ld, yv, m, cut, sL, sR, nL, frac, sdT);
+  return true;
+}
+
+// Large nodes (m > kM5WideRows): rows j and j + 1 share one fused first pass
+// (two independent sum chains per row load); the second passes stay per
+// candidate.  A candidate whose midpoint rounds up (adjacent doubles) is
+// rescored by m5_candidate.
+constexpr int kM5WideRows = 32;
+
 __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const double* y, double sdT, int lane,
                                 int& ba, double& bt) {
   double bs = -INFINITY;
@@ -168,58 +232,56 @@ __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const
   for (int a = lane; a < deff; a += 32) {
     const double* xa = W.Xs + lo * W.ld + a;
     const int ld = W.ld;
+    if (m <= kM5WideRows) {
+      #pragma unroll 1
+      for (int j = 0; j < m; ++j) {
+        double sdr, thr;
+        if (m5_candidate(xa, ld, yv, m, j, frac, sdT, sdr, thr) && m5_better(sdr, a, thr, bs, ba, bt)) {
+          bs = sdr;
+          ba = a;
+          bt = thr;
+        }
+      }
+      continue;
+    }
     #pragma unroll 1
-    for (int j = 0; j < m; ++j) {
-      const double u = xa[j * ld];
-      bool dup = false;
-      double nx = INFINITY, sL = 0.0, sR = 0.0;
-      int nL = 0;
+    for (int j = 0; j < m; j += 2) {
+      const bool two = j + 1 < m;
+      const double u0 = xa[j * ld], u1 = two ? xa[(j + 1) * ld] : INFINITY;
+      bool d0 = false, d1 = false;
+      double n0 = INFINITY, n1 = INFINITY, sL0 = 0.0, sR0 = 0.0, sL1 = 0.0, sR1 = 0.0;
+      int nL0 = 0, nL1 = 0;
 SR_UNROLL(SR_M5_UNROLL)
       for (int k = 0; k < m; ++k) {
         const double v = xa[k * ld], yk = yv[k];
-        dup |= (k < j) & (v == u);
-        nx = (v > u && v < nx) ? v : nx;
-        const bool l = v <= u;
-        const double t = __dadd_rn(l ? sL : sR, yk);
-        sL = l ? t : sL;
-        sR = l ? sR : t;
-        nL += l;
+        d0 |= (k < j) & (v == u0);
+        d1 |= (k < j + 1) & (v == u1);
+        n0 = (v > u0 && v < n0) ? v : n0;
+        n1 = (v > u1 && v < n1) ? v : n1;
+        const bool l0 = v <= u0, l1 = v <= u1;
+        const double t0 = __dadd_rn(l0 ? sL0 : sR0, yk), t1 = __dadd_rn(l1 ? sL1 : sR1, yk);
+        sL0 = l0 ? t0 : sL0;
+        sR0 = l0 ? sR0 : t0;
+        sL1 = l1 ? t1 : sL1;
+        sR1 = l1 ? sR1 : t1;
+        nL0 += l0;
+        nL1 += l1;
       }
-      if (dup || nx == INFINITY) continue;
-      const double thr = __dmul_rn(__dadd_rn(u, nx), 0.5);   // (lo + hi) / 2
-      double cut = u;
-      if (!(thr < nx)) {   // u, nx adjacent doubles and the midpoint rounded up: x <= thr takes nx too
-        cut = thr;
-        sL = sR = 0.0;
-        nL = 0;
-        for (int k = 0; k < m; ++k) {
-          const bool l = xa[k * ld] <= cut;
-          const double t = __dadd_rn(l ? sL : sR, yv[k]);
-          sL = l ? t : sL;
-          sR = l ? sR : t;
-          nL += l;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const double u = c ? u1 : u0, nx = c ? n1 : n0;
+        if ((c ? d1 : d0) || nx == INFINITY) continue;
+        double thr = __dmul_rn(__dadd_rn(u, nx), 0.5), sdr;
+        if (thr < nx) {
+          sdr = m5_score(xa, ld, yv, m, u, c ? sL1 : sL0, c ? sR1 : sR0, c ? nL1 : nL0, frac, sdT);
+        } else if (!m5_candidate(xa, ld, yv, m, j + c, frac, sdT, sdr, thr)) {
+          continue;
         }
-        if (nL == m) continue;   // unreachable for distinct finite values; keeps the sds defined
-      }
-      const int nR = m - nL;
-      const double mL = __ddiv_rn(sL, (double)nL), mR = __ddiv_rn(sR, (double)nR);
-      double qL = 0.0, qR = 0.0;
-SR_UNROLL(SR_M5_UNROLL)
-      for (int k = 0; k < m; ++k) {
-        const double v = xa[k * ld];
-        const bool l = v <= cut;
-        const double dv = __dsub_rn(yv[k], l ? mL : mR);
-        const double t = __dadd_rn(l ? qL : qR, __dmul_rn(dv, dv));
-        qL = l ? t : qL;
-        qR = l ? qR : t;
-      }
-      const double sdL = __dsqrt_rn(__ddiv_rn(qL, (double)nL)), sdR = __dsqrt_rn(__ddiv_rn(qR, (double)nR));
-      const double fL = frac[nL], fR = frac[nR];
-      const double sdr = __dsub_rn(__dsub_rn(sdT, __dmul_rn(fL, sdL)), __dmul_rn(fR, sdR));
-      if (m5_better(sdr, a, thr, bs, ba, bt)) {
-        bs = sdr;
-        ba = a;
-        bt = thr;
+        if (m5_better(sdr, a, thr, bs, ba, bt)) {
+          bs = sdr;
+          ba = a;
+          bt = thr;
+        }
       }
     }
   }
