@@ -97,32 +97,60 @@ def test_m5_c5_feature_masks_and_aggregation():
     assert list(agg["top"][:len(top)]) == list(top)
 
 
+def _adjacent_dataset(cfg, seed=3):
+    ds = cfg.dataset
+    N = ds.counters.shape[0]
+    ds.cycles[:] = 1.0
+    rng = np.random.default_rng(seed)
+    ds.counters[:, 1:] = 7.0                                   # inactive (constant)
+    col = np.round(rng.uniform(0.05, 0.95, size=N), 2)         # duplicates at 2 decimals
+    u = np.nextafter(0.5, 1.0)
+    for g0 in range(0, N, 64):                                 # in every group
+        col[g0 + 4], col[g0 + 8] = u, np.nextafter(u, 1.0)
+        col[g0] = 0.0
+        col[g0 + 1] = col[g0 + 2] = 1.0                        # rg = 1: scaled == raw
+    ds.counters[:, 0] = col
+    # labels step at u: slots above u run slower
+    ds.runtime_ms[:] = np.where(col > u, 2.0, 1.0) * (1.0 + 0.3 * rng.uniform(size=N))
+    assert (u + np.nextafter(u, 1.0)) / 2 == np.nextafter(u, 1.0)
+
+
 def test_m5_adjacent_double_thresholds():
     """Degenerate split candidates (M1): one active counter whose scaled values
     include adjacent doubles u < nx with an odd-mantissa u, so the midpoint
     (u + nx)/2 rounds up to nx and x <= threshold takes nx to the left (the
-    kernel's fused scan must then redo the pass with the threshold itself);
-    plus duplicated values.  All 64 C1 folds vs the oracle."""
+    kernel's fused scan must then redo the pass with the threshold itself; a
+    kernel without the redo fails this test); plus duplicated values.  C1, all
+    64 folds (nodes <= 31 rows), and C2 scenarios of 64 and 96 training pairs
+    (nodes > 32 rows: the paired-candidate pass) vs the oracle."""
     cfg = gen.make_config("C1")
-    ds = cfg.dataset
-    ds.cycles[:] = 1.0
-    rng = np.random.default_rng(3)
-    ds.counters[:, 1:] = 7.0                                   # inactive (constant)
-    col = np.round(rng.uniform(0.05, 0.95, size=64), 2)        # duplicates at 2 decimals
-    u = np.nextafter(0.5, 1.0)
-    col[[4, 8]] = [u, np.nextafter(u, 1.0)]
-    col[[0]] = 0.0
-    col[[1, 2]] = 1.0                                          # rg = 1: scaled == raw
-    ds.counters[:, 0] = col
-    # labels step at u: slots above u run slower
-    ds.runtime_ms[:] = np.where(col > u, 2.0, 1.0) * (1.0 + 0.01 * rng.uniform(size=64))
-    assert (u + np.nextafter(u, 1.0)) / 2 == np.nextafter(u, 1.0)
+    _adjacent_dataset(cfg)
     got, ref = _run(cfg, 0, 64)
     # step labels make equal EX across optimizations common (rank-tie guard
     # cases, R21); the unguarded scenarios carry the comparison
     st = compare(got, ref, max_guard_frac=0.5)
     assert st["n"] - st["guarded"] >= 32
-    print("M5P adjacent", st)
+    print("M5P adjacent C1", st)
+    from paper_1910_07776_b200 import Context, default_params
+    cfg = gen.make_config("C2")
+    _adjacent_dataset(cfg, seed=4)
+    ctx = Context(0)
+    ctx.load(cfg.dataset)
+    ctx.define_scenarios(cfg.scenarios)
+    got = ctx.evaluate(0, 240, params=default_params(learner=2), want_ex=True)
+    ctx.close()
+    ntr = got["opt"]["n_train"].max(axis=1)
+    idx = [int(np.argmax(ntr == 64)), int(np.argmax(ntr == 96)), int(len(ntr) - 1 - np.argmax(ntr[::-1] == 96))]
+    refs = [m5.evaluate(cfg.dataset, cfg.scenarios, s, 1) for s in idx]
+    ref = dict(opt=np.concatenate([r["opt"] for r in refs]), scn=np.concatenate([r["scn"] for r in refs]),
+               ex=np.concatenate([r["ex"] for r in refs]))
+    st = compare(_sub(got, idx), ref, max_guard_frac=1.0)
+    # these scenarios all carry rank-tie guard cases; the trees themselves
+    # (every EX) must still agree
+    from tests.parity import rel_err
+    e = rel_err(_sub(got, idx)["ex"], ref["ex"])
+    print("M5P adjacent C2", idx, st, "EX worst", e.max())
+    assert e.max() <= 1e-9
 
 
 def test_m5_bh6_sampled():
