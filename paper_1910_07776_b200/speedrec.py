@@ -128,7 +128,15 @@ def lib() -> ct.CDLL:
     return _lib
 
 
+SR_LINREG, SR_IBK, SR_M5P = 0, 1, 2          # sr_learner (include/speedrec.h)
+LEARNERS = {"linreg": SR_LINREG, "ibk": SR_IBK, "m5": SR_M5P}
+
+
 def default_params(**overrides) -> sr_params:
+    """sr_default_params + overrides; learner may be given by name
+    ("linreg" | "ibk" | "m5") or by its sr_learner value."""
+    if isinstance(overrides.get("learner"), str):
+        overrides["learner"] = LEARNERS[overrides["learner"]]
     p = sr_params()
     lib().sr_default_params(ct.byref(p))
     for k, v in overrides.items():

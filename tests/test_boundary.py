@@ -84,3 +84,18 @@ def test_product_path_does_not_touch_oracle():
     otxt = open(os.path.join(ROOT, "oracle", "oracle.c")).read() + open(os.path.join(ROOT, "oracle", "__init__.py")).read()
     assert "paper_1910_07776_b200" not in otxt.replace("paper_1910_07776_b200/ (the CUDA path)", "").replace(
         "`paper_1910_07776_b200/`", "")
+
+
+def test_learner_names_map_to_the_header_enum():
+    """sr_learner values (include/speedrec.h) and their names in the binding."""
+    import re
+    from paper_1910_07776_b200 import SR_IBK, SR_LINREG, SR_M5P, default_params
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                            "speedrec.h")).read()
+    enum = dict((k, int(v)) for k, v in re.findall(r"(SR_LINREG|SR_IBK|SR_M5P) = (\d+)", hdr))
+    assert enum == {"SR_LINREG": SR_LINREG, "SR_IBK": SR_IBK, "SR_M5P": SR_M5P}
+    assert default_params(learner="m5").learner == SR_M5P
+    assert default_params(learner="ibk").learner == SR_IBK
+    assert default_params().learner == SR_LINREG
+    with pytest.raises(KeyError):
+        default_params(learner="logistic")
