@@ -39,7 +39,8 @@
  *     n_opt_ids <= 16, max_count <= 8.  Up to 64 groups run on the warp path
  *     (all features); more groups on the large-batch path (config C4), which
  *     needs <= 8 scored optimizations and supports neither mask aggregation
- *     nor sr_sweep.  Violations return SR_E_UNSUPPORTED.
+ *     nor sr_sweep.  Learner SR_M5P runs on the warp path only, with <= 64
+ *     counters.  Violations return SR_E_UNSUPPORTED.
  */
 #ifndef SPEEDREC_H_
 #define SPEEDREC_H_
