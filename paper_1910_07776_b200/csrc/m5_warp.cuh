@@ -217,7 +217,10 @@ SR_UNROLL(SR_M5_UNROLL)
 // (two independent sum chains per row load); the second passes stay per
 // candidate.  A candidate whose midpoint rounds up (adjacent doubles) is
 // rescored by m5_candidate.
-constexpr int kM5WideRows = 32;
+#ifndef SR_M5_WIDE_ROWS
+#define SR_M5_WIDE_ROWS 32
+#endif
+constexpr int kM5WideRows = SR_M5_WIDE_ROWS;   // A/B knob
 
 __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const double* y, double sdT, int lane,
                                 int& ba, double& bt) {
