@@ -149,11 +149,14 @@ def make_config(name: str, n_splits: Optional[int] = None, n_masks_k: Optional[i
         sc = table2_scenarios(ds, OPT_NAMES_C2)
         desc = "BH x 6 inputs (Table 1) x 3 runs x 64 variants, 32 counters, Table-2 Exp 1-4 (144)"
     elif name == "C3":
-        ds = generate(n_programs=2, n_inputs=1, n_runs=1, n_counters=64, seed=dseed,
-                      opt_names=GENERIC_OPTS, program_opts=[GENERIC_OPTS, GENERIC_OPTS],
+        # n_programs=1: one group, so a fit's n ~ Bin(32, 1/4) reaches the
+        # degenerate fits n = 0 (R18 untrained), 1, 2, 3 (parity edge cases)
+        P = n_programs or 2
+        ds = generate(n_programs=P, n_inputs=1, n_runs=1, n_counters=64, seed=dseed,
+                      opt_names=GENERIC_OPTS, program_opts=[GENERIC_OPTS] * P,
                       small_opt="O0")
         sc = Scenarios(kind="random", n_splits=n_splits or 1_000_000, group_words=1, seed=sseed)
-        desc = "2 programs x 64 variants, 64 counters, random slot splits"
+        desc = f"{P} programs x 64 variants, 64 counters, random slot splits"
     elif name == "C4":
         P = n_programs or 1024
         ds = generate(n_programs=P, n_inputs=1, n_runs=1, n_counters=128, seed=dseed,

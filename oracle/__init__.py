@@ -49,7 +49,7 @@ class OrScenarios(ct.Structure):
 class OrParams(ct.Structure):
     _fields_ = [("ridge", ct.c_double), ("threshold", ct.c_double), ("clamp_floor", ct.c_double),
                 ("guard_tol", ct.c_double), ("max_count", ct.c_int32), ("learner", ct.c_int32),
-                ("k_nn", ct.c_int32)]
+                ("k_nn", ct.c_int32), ("force_quad", ct.c_int32)]
 
 
 OPT_SCORE_DTYPE = np.dtype([("n_train", "<i4"), ("n_test", "<i4"), ("n_correct", "<i4"),
@@ -73,9 +73,10 @@ def lib():
         _lib.or_scale.restype = ct.c_int32
         _lib.or_scale.argtypes = [ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_int32, ct.c_void_p,
                                   ct.c_void_p, ct.c_void_p, ct.c_void_p]
-        _lib.or_fit_predict.restype = ct.c_int32
-        _lib.or_fit_predict.argtypes = [ct.c_int32, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_void_p,
-                                        ct.c_int32, ct.c_void_p, ct.c_double, ct.c_void_p, ct.c_void_p]
+        for fn in (_lib.or_fit_predict, _lib.or_fit_predict_ld):
+            fn.restype = ct.c_int32
+            fn.argtypes = [ct.c_int32, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_void_p,
+                           ct.c_int32, ct.c_void_p, ct.c_double, ct.c_void_p, ct.c_void_p, ct.c_void_p]
         _lib.or_rank.restype = ct.c_int32
         _lib.or_knn_predict.restype = None
         _lib.or_knn_predict.argtypes = [ct.c_int32, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_void_p,
@@ -87,7 +88,8 @@ def lib():
         _lib.or_evaluate.restype = ct.c_int32
         _lib.or_evaluate.argtypes = [ct.POINTER(OrDataset), ct.POINTER(OrScenarios),
                                      ct.POINTER(OrParams), ct.c_int64, ct.c_int64, ct.c_void_p,
-                                     ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_int32]
+                                     ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p,
+                                     ct.c_int32]
     return _lib
 
 
@@ -124,8 +126,11 @@ def scale(X: np.ndarray, Xt: np.ndarray):
     return Xs[:, :de].copy(), Xts[:, :de].copy(), act[:de].copy()
 
 
-def fit_predict(Xs: np.ndarray, y: np.ndarray, Xts: np.ndarray, ridge: float = 1e-8):
-    """Ridge fit on already-scaled features; returns (EX [t], coef [1+d])."""
+def fit_predict(Xs: np.ndarray, y: np.ndarray, Xts: np.ndarray, ridge: float = 1e-8, precision: str = "quad",
+                want_kappa: bool = False):
+    """Ridge fit on already-scaled features; returns (EX [t], coef [1+d])
+    (+ kappa^ = (max L_ii / min L_ii)^2 with want_kappa).  precision: "quad"
+    (__float128) or "ld" (x87 long double, SURVEY 8(c)'s C4 allowance)."""
     Xs = np.ascontiguousarray(Xs, dtype=np.float64)
     n, d = Xs.shape
     y = np.ascontiguousarray(y, dtype=np.float64)
@@ -134,11 +139,13 @@ def fit_predict(Xs: np.ndarray, y: np.ndarray, Xts: np.ndarray, ridge: float = 1
     t = Xts.shape[0]
     ex = np.zeros(t)
     coef = np.zeros(1 + d)
-    rc = lib().or_fit_predict(n, d, max(d, 1), _p(Xs) if d else _p(np.zeros(max(n, 1))), _p(y), t,
-                              _p(Xts) if d else _p(np.zeros(max(t, 1))), ridge, _p(ex), _p(coef))
+    kap = ct.c_double(1.0)
+    fn = lib().or_fit_predict if precision == "quad" else lib().or_fit_predict_ld
+    rc = fn(n, d, max(d, 1), _p(Xs) if d else _p(np.zeros(max(n, 1))), _p(y), t,
+            _p(Xts) if d else _p(np.zeros(max(t, 1))), ridge, _p(ex), _p(coef), ct.byref(kap))
     if rc != 0:
         raise FloatingPointError("oracle Cholesky failed")
-    return ex, coef
+    return (ex, coef, kap.value) if want_kappa else (ex, coef)
 
 
 def knn_predict(Xs: np.ndarray, y: np.ndarray, Xts: np.ndarray, k: int = 10) -> np.ndarray:
@@ -194,16 +201,20 @@ def aggregate_masks(opt, scn, n_folds: int, first_mask: int = 0, top_k: int = 64
 
 # ---------------------------------------------------------------- batch
 DEFAULT_PARAMS = dict(ridge=1e-8, threshold=1.05, clamp_floor=0.01, guard_tol=1e-9, max_count=3, learner=0,
-                      k_nn=10)
+                      k_nn=10, force_quad=0)
+# learner ids: 0 ridge LS, 1 IBK; test-only scoring stubs: 100 EX := AC, 101 EX := 1
+LEARNER_PERFECT_STUB, LEARNER_CONSTANT_STUB = 100, 101
 
 
 def evaluate(ds, sc, first: int = 0, count: int | None = None, want_ex: bool = False,
-             want_recs: bool = False, n_threads: int | None = None, **params):
+             want_recs: bool = False, n_threads: int | None = None, want_kappa: bool = False, **params):
     """Run the oracle over scenarios [first, first+count) of (ds, sc).
 
     ds: gen.synth.Dataset; sc: gen.configs.Scenarios.
     Returns dict(opt=structured [count][O], scn=structured [count],
-                 ex=[count][O][G*32] or None, recs=[count][N][K] or None).
+                 ex=[count][O][G*32] or None, recs=[count][N][K] or None,
+                 kappa=[count][O] kappa^ per ridge fit (NaN: no fit) or None,
+                 fit_ld=[count][O] 1 where the fit ran in long double, or None).
     """
     prm = dict(DEFAULT_PARAMS)
     prm.update(params)
@@ -233,7 +244,7 @@ def evaluate(ds, sc, first: int = 0, count: int | None = None, want_ex: bool = F
     s = OrScenarios(kind, sc.group_words, sc.n_splits, _p(tg), _p(eg), _p(om), _p(pg),
                     sc.seed, sc.opt_mask, sc.all_subsets_k, sc.n_masks, _p(fm))
     p = OrParams(prm["ridge"], prm["threshold"], prm["clamp_floor"], prm["guard_tol"],
-                 prm["max_count"], prm["learner"], prm["k_nn"])
+                 prm["max_count"], prm["learner"], prm["k_nn"], prm["force_quad"])
     O = ds.n_opt_ids
     G = ds.n_programs * ds.n_inputs * ds.n_runs
     V = 1 << ds.n_opt_bits
@@ -241,9 +252,11 @@ def evaluate(ds, sc, first: int = 0, count: int | None = None, want_ex: bool = F
     scn = np.zeros(count, dtype=SCN_SCORE_DTYPE)
     ex = np.zeros((count, O, G * V // 2)) if want_ex else None
     recs = np.zeros((count, G * V, prm["max_count"]), dtype=np.int8) if want_recs else None
+    kappa = np.full((count, O), np.nan) if want_kappa else None
+    fit_ld = np.zeros((count, O), dtype=np.int32) if want_kappa else None
     if n_threads is None:
         n_threads = os.cpu_count() or 1
     rc = lib().or_evaluate(ct.byref(d), ct.byref(s), ct.byref(p), first, count, _p(opt), _p(scn),
-                           _p(ex), _p(recs), n_threads)
+                           _p(ex), _p(recs), _p(kappa), _p(fit_ld), n_threads)
     assert rc == 0
-    return dict(opt=opt, scn=scn, ex=ex, recs=recs)
+    return dict(opt=opt, scn=scn, ex=ex, recs=recs, kappa=kappa, fit_ld=fit_ld)

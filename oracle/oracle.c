@@ -66,8 +66,11 @@ typedef struct {
   double clamp_floor;              /* 0.01 */
   double guard_tol;                /* 1e-9 (reading R21) */
   int32_t max_count;               /* 3 */
-  int32_t learner;                 /* 0 ridge least squares (reading D1), 1 IBK k-NN */
+  int32_t learner;                 /* 0 ridge least squares (reading D1), 1 IBK k-NN;
+                                      test-only stubs of SPEC's scoring checks: 100 perfect predictor
+                                      EX := AC, 101 constant predictor EX := 1 */
   int32_t k_nn;                    /* IBK k, 10 */
+  int32_t force_quad;              /* 1: every fit in quad (0: the precision policy of or_fit_policy) */
 } or_params;
 
 typedef struct {
@@ -138,81 +141,122 @@ int32_t or_scale(int32_t n, int32_t d, const double* X, int32_t t, const double*
 /*   (b, w) = argmin sum_i (y_i - b - w.x'_i)^2 + lambda |w|^2             */
 /* written out as its normal equations in centred form:                    */
 /*   xbar = mean x'_i, ybar = mean y_i, Xc = X' - 1 xbar^T, yc = y - ybar  */
-/*   (Xc^T Xc + lambda I) w = Xc^T yc   (Cholesky, quad),  b = ybar - w.xbar */
-/* Prediction EX_j = b + w.x'_j (quad), rounded to FP64 (P:60 Tier 2).      */
+/*   (Xc^T Xc + lambda I) w = Xc^T yc   (Cholesky),  b = ybar - w.xbar      */
+/* Prediction EX_j = b + w.x'_j, rounded to FP64 (P:60 Tier 2).             */
 /* Xs is [n][ld], Xts is [t][ld]; only the first d columns are used.        */
 /* coef_out (optional) receives [b, w_0..w_{d-1}] rounded to FP64.          */
+/* kappa_out (optional) receives kappa^ = (max L_ii / min L_ii)^2 of the    */
+/* Cholesky factor (1 when d = 0).                          */
 /* Returns 0, or -1 if the Cholesky pivot is not positive.                 */
+/*                                                                          */
+/* The body is written once and instantiated in two working precisions     */
+/* (SURVEY 8(c) "Oracle precision policy"): __float128 (quad) for every fit */
+/* with n - 1 < 2 d or p = d + 1 <= 65 (all of C1, C2, C3, C5), and x87     */
+/* long double for the large overdetermined C4 fits, accepted only when     */
+/* kappa^ * 2^-64 < 1e-12 (else the fit is redone in quad).                 */
 /* ------------------------------------------------------------------ */
-int32_t or_fit_predict(int32_t n, int32_t d, int32_t ld, const double* Xs, const double* y,
-                       int32_t t, const double* Xts, double lambda, double* ex_out,
-                       double* coef_out) {
-  quad* xbar = (quad*)calloc((size_t)d + 1, sizeof(quad));
-  quad* G = (quad*)calloc((size_t)d * d + 1, sizeof(quad));
-  quad* rhs = (quad*)calloc((size_t)d + 1, sizeof(quad));
-  quad* w = (quad*)calloc((size_t)d + 1, sizeof(quad));
-  quad ybar = 0;
-  int32_t rc = 0;
-  for (int32_t i = 0; i < n; ++i) ybar += (quad)y[i];
-  ybar /= (quad)n;
-  for (int32_t a = 0; a < d; ++a) {
-    quad s = 0;
-    for (int32_t i = 0; i < n; ++i) s += (quad)Xs[(int64_t)i * ld + a];
-    xbar[a] = s / (quad)n;
+#define OR_DEFINE_FIT(NAME, T, SQRT)                                                               \
+  int32_t NAME(int32_t n, int32_t d, int32_t ld, const double* Xs, const double* y, int32_t t,    \
+               const double* Xts, double lambda, double* ex_out, double* coef_out,                \
+               double* kappa_out) {                                                               \
+    T* xbar = (T*)calloc((size_t)d + 1, sizeof(T));                                               \
+    T* G = (T*)calloc((size_t)d * d + 1, sizeof(T));                                              \
+    T* rhs = (T*)calloc((size_t)d + 1, sizeof(T));                                                \
+    T* w = (T*)calloc((size_t)d + 1, sizeof(T));                                                  \
+    T ybar = 0;                                                                                   \
+    int32_t rc = 0;                                                                               \
+    for (int32_t i = 0; i < n; ++i) ybar += (T)y[i];                                              \
+    ybar /= (T)n;                                                                                 \
+    for (int32_t a = 0; a < d; ++a) {                                                             \
+      T s = 0;                                                                                    \
+      for (int32_t i = 0; i < n; ++i) s += (T)Xs[(int64_t)i * ld + a];                            \
+      xbar[a] = s / (T)n;                                                                         \
+    }                                                                                             \
+    /* G = Xc^T Xc + lambda I ; rhs = Xc^T yc */                                                  \
+    for (int32_t a = 0; a < d; ++a) {                                                             \
+      for (int32_t c = 0; c <= a; ++c) {                                                          \
+        T s = 0;                                                                                  \
+        for (int32_t i = 0; i < n; ++i)                                                           \
+          s += ((T)Xs[(int64_t)i * ld + a] - xbar[a]) * ((T)Xs[(int64_t)i * ld + c] - xbar[c]);   \
+        G[a * d + c] = s;                                                                         \
+        G[c * d + a] = s;                                                                         \
+      }                                                                                           \
+      G[a * d + a] += (T)lambda;                                                                  \
+      T r = 0;                                                                                    \
+      for (int32_t i = 0; i < n; ++i) r += ((T)Xs[(int64_t)i * ld + a] - xbar[a]) * ((T)y[i] - ybar); \
+      rhs[a] = r;                                                                                 \
+    }                                                                                             \
+    /* Cholesky G = L L^T (lower triangle stored in G) */                                         \
+    for (int32_t j = 0; j < d && rc == 0; ++j) {                                                  \
+      T s = G[j * d + j];                                                                         \
+      for (int32_t k = 0; k < j; ++k) s -= G[j * d + k] * G[j * d + k];                           \
+      if (!(s > 0)) { rc = -1; break; }                                                           \
+      T ljj = SQRT(s);                                                                            \
+      G[j * d + j] = ljj;                                                                         \
+      for (int32_t i = j + 1; i < d; ++i) {                                                       \
+        T u = G[i * d + j];                                                                       \
+        for (int32_t k = 0; k < j; ++k) u -= G[i * d + k] * G[j * d + k];                         \
+        G[i * d + j] = u / ljj;                                                                   \
+      }                                                                                           \
+    }                                                                                             \
+    if (rc == 0) {                                                                                \
+      if (kappa_out) {                                                                            \
+        T lmax = 1, lmin = 1;                                                                     \
+        for (int32_t j = 0; j < d; ++j) {                                                         \
+          if (j == 0 || G[j * d + j] > lmax) lmax = G[j * d + j];                                 \
+          if (j == 0 || G[j * d + j] < lmin) lmin = G[j * d + j];                                 \
+        }                                                                                         \
+        *kappa_out = (double)((lmax / lmin) * (lmax / lmin));                                     \
+      }                                                                                           \
+      /* L z = rhs ; L^T w = z */                                                                 \
+      for (int32_t i = 0; i < d; ++i) {                                                           \
+        T u = rhs[i];                                                                             \
+        for (int32_t k = 0; k < i; ++k) u -= G[i * d + k] * w[k];                                 \
+        w[i] = u / G[i * d + i];                                                                  \
+      }                                                                                           \
+      for (int32_t i = d - 1; i >= 0; --i) {                                                      \
+        T u = w[i];                                                                               \
+        for (int32_t k = i + 1; k < d; ++k) u -= G[k * d + i] * w[k];                             \
+        w[i] = u / G[i * d + i];                                                                  \
+      }                                                                                           \
+      T b = ybar;                                                                                 \
+      for (int32_t a = 0; a < d; ++a) b -= w[a] * xbar[a];                                        \
+      for (int32_t j = 0; j < t; ++j) {                                                           \
+        T e = b;                                                                                  \
+        for (int32_t a = 0; a < d; ++a) e += w[a] * (T)Xts[(int64_t)j * ld + a];                  \
+        ex_out[j] = (double)e;                                                                    \
+      }                                                                                           \
+      if (coef_out) {                                                                             \
+        coef_out[0] = (double)b;                                                                  \
+        for (int32_t a = 0; a < d; ++a) coef_out[1 + a] = (double)w[a];                           \
+      }                                                                                           \
+    }                                                                                             \
+    free(xbar); free(G); free(rhs); free(w);                                                      \
+    return rc;                                                                                    \
   }
-  /* G = Xc^T Xc + lambda I ; rhs = Xc^T yc */
-  for (int32_t a = 0; a < d; ++a) {
-    for (int32_t c = 0; c <= a; ++c) {
-      quad s = 0;
-      for (int32_t i = 0; i < n; ++i)
-        s += ((quad)Xs[(int64_t)i * ld + a] - xbar[a]) * ((quad)Xs[(int64_t)i * ld + c] - xbar[c]);
-      G[a * d + c] = s;
-      G[c * d + a] = s;
-    }
-    G[a * d + a] += (quad)lambda;
-    quad r = 0;
-    for (int32_t i = 0; i < n; ++i) r += ((quad)Xs[(int64_t)i * ld + a] - xbar[a]) * ((quad)y[i] - ybar);
-    rhs[a] = r;
-  }
-  /* Cholesky G = L L^T (lower triangle stored in G) */
-  for (int32_t j = 0; j < d && rc == 0; ++j) {
-    quad s = G[j * d + j];
-    for (int32_t k = 0; k < j; ++k) s -= G[j * d + k] * G[j * d + k];
-    if (!(s > 0)) { rc = -1; break; }
-    quad ljj = sqrtq(s);
-    G[j * d + j] = ljj;
-    for (int32_t i = j + 1; i < d; ++i) {
-      quad u = G[i * d + j];
-      for (int32_t k = 0; k < j; ++k) u -= G[i * d + k] * G[j * d + k];
-      G[i * d + j] = u / ljj;
+
+OR_DEFINE_FIT(or_fit_predict, quad, sqrtq)
+OR_DEFINE_FIT(or_fit_predict_ld, long double, sqrtl)
+
+/* The precision policy above: quad unless the fit is overdetermined
+ * (n - 1 >= 2 d) with p = d + 1 > 65; then long double, kept only when
+ * kappa^ * 2^-64 < 1e-12, i.e. its relative error bound is far inside the
+ * 1e-9 parity bar (else redone in quad).  force_quad: quad always.
+ * *used_ld reports which precision produced the result. */
+int32_t or_fit_policy(int32_t n, int32_t d, int32_t ld, const double* Xs, const double* y, int32_t t,
+                      const double* Xts, double lambda, double* ex_out, double* coef_out,
+                      double* kappa_out, int32_t force_quad, int32_t* used_ld) {
+  double kap = 1.0;
+  *used_ld = 0;
+  if (!force_quad && n - 1 >= 2 * d && d + 1 > 65) {
+    int32_t rc = or_fit_predict_ld(n, d, ld, Xs, y, t, Xts, lambda, ex_out, coef_out, &kap);
+    if (rc == 0 && kap * 0x1p-64 < 1e-12) {
+      *used_ld = 1;
+      if (kappa_out) *kappa_out = kap;
+      return 0;
     }
   }
-  if (rc == 0) {
-    /* L z = rhs ; L^T w = z */
-    for (int32_t i = 0; i < d; ++i) {
-      quad u = rhs[i];
-      for (int32_t k = 0; k < i; ++k) u -= G[i * d + k] * w[k];
-      w[i] = u / G[i * d + i];
-    }
-    for (int32_t i = d - 1; i >= 0; --i) {
-      quad u = w[i];
-      for (int32_t k = i + 1; k < d; ++k) u -= G[k * d + i] * w[k];
-      w[i] = u / G[i * d + i];
-    }
-    quad b = ybar;
-    for (int32_t a = 0; a < d; ++a) b -= w[a] * xbar[a];
-    for (int32_t j = 0; j < t; ++j) {
-      quad e = b;
-      for (int32_t a = 0; a < d; ++a) e += w[a] * (quad)Xts[(int64_t)j * ld + a];
-      ex_out[j] = (double)e;
-    }
-    if (coef_out) {
-      coef_out[0] = (double)b;
-      for (int32_t a = 0; a < d; ++a) coef_out[1 + a] = (double)w[a];
-    }
-  }
-  free(xbar); free(G); free(rhs); free(w);
-  return rc;
+  return or_fit_predict(n, d, ld, Xs, y, t, Xts, lambda, ex_out, coef_out, kappa_out);
 }
 
 /* ------------------------------------------------------------------ */
@@ -315,6 +359,8 @@ typedef struct {
   or_scn_score* scn_scores;   /* [count] */
   double* ex;                 /* [count][O][G * 2^(m-1)] or NULL */
   int8_t* recs;               /* [count][N][max_count] or NULL */
+  double* kappa;              /* [count][O] kappa^ of each ridge fit (NaN: no fit) or NULL */
+  int32_t* fit_ld;            /* [count][O] 1 if the fit ran in long double, or NULL */
   const double* x;            /* rates [N][C] */
   int32_t rc;
 } or_job;
@@ -322,7 +368,7 @@ typedef struct {
 static int bit_of(const uint64_t* words, int64_t i) { return (int)((words[i >> 6] >> (i & 63)) & 1u); }
 
 static void eval_scenario(const or_job* J, int64_t s, or_opt_score* orow, or_scn_score* srow,
-                          double* ex_tab, int8_t* rec_tab) {
+                          double* ex_tab, int8_t* rec_tab, double* kap_row, int32_t* ld_row) {
   const or_dataset* ds = J->ds;
   const or_scenarios* sc = J->sc;
   const or_params* pr = J->pr;
@@ -387,6 +433,8 @@ static void eval_scenario(const or_job* J, int64_t s, or_opt_score* orow, or_scn
   for (int32_t o = 0; o < O; ++o) {
     or_opt_score* os = &orow[o];
     memset(os, 0, sizeof(*os));
+    if (kap_row) kap_row[o] = NAN;
+    if (ld_row) ld_row[o] = 0;
     if (!((omask >> o) & 1u)) continue;
     /* --- pairs ("pairs of before and after code samples"; P:118 the
      *     32/32 lattice split; label = rt_before / rt_after, reading D2) --- */
@@ -428,9 +476,18 @@ static void eval_scenario(const or_job* J, int64_t s, or_opt_score* orow, or_scn
     int32_t d_eff = d > 0 ? or_scale(n, d, Xr, nt, Xtr, Xs, Xts, NULL) : 0;
     if (pr->learner == 1) {
       or_knn_predict(n, d_eff, d > 0 ? d : 1, Xs, tr_y, nt, Xts, pr->k_nn, te_ex);
-    } else if (or_fit_predict(n, d_eff, d > 0 ? d : 1, Xs, tr_y, nt, Xts, pr->ridge, te_ex, NULL) != 0) {
-      /* unreachable for lambda > 0 (G + lambda I is SPD); poison the row */
-      srow->n_guard = -1000000;
+    } else if (pr->learner == 100 || pr->learner == 101) {
+      /* scoring-check stubs: the predictor is replaced, the
+       * clamp / score / rank steps below run unchanged */
+      for (int32_t j = 0; j < nt; ++j) te_ex[j] = pr->learner == 100 ? te_ac[j] : 1.0;
+    } else {
+      double kap = NAN;
+      int32_t used_ld = 0;
+      if (or_fit_policy(n, d_eff, d > 0 ? d : 1, Xs, tr_y, nt, Xts, pr->ridge, te_ex, NULL, &kap,
+                        pr->force_quad, &used_ld) != 0)
+        srow->n_guard = -1000000;   /* unreachable for lambda > 0 (G + lambda I is SPD); poison the row */
+      if (kap_row) kap_row[o] = kap;
+      if (ld_row) ld_row[o] = used_ld;
     }
     /* --- clamp (reading R7) and score --- */
     quad sum = 0;
@@ -511,7 +568,8 @@ static void* job_run(void* arg) {
     int8_t* rc = J->recs ? J->recs + j * rec_stride : NULL;
     if (ex) memset(ex, 0, sizeof(double) * (size_t)ex_stride);
     if (rc) memset(rc, -1, (size_t)rec_stride);
-    eval_scenario(J, J->first + j, J->opt_scores + j * ds->O, J->scn_scores + j, ex, rc);
+    eval_scenario(J, J->first + j, J->opt_scores + j * ds->O, J->scn_scores + j, ex, rc,
+                  J->kappa ? J->kappa + j * ds->O : NULL, J->fit_ld ? J->fit_ld + j * ds->O : NULL);
   }
   return NULL;
 }
@@ -520,7 +578,8 @@ static void* job_run(void* arg) {
  * (contiguous chunks).  Output layout matches the CUDA path's sr_outputs. */
 int32_t or_evaluate(const or_dataset* ds, const or_scenarios* sc, const or_params* pr,
                     int64_t first, int64_t count, or_opt_score* opt_scores,
-                    or_scn_score* scn_scores, double* ex, int8_t* recs, int32_t n_threads) {
+                    or_scn_score* scn_scores, double* ex, int8_t* recs, double* kappa, int32_t* fit_ld,
+                    int32_t n_threads) {
   const int64_t N = ((int64_t)ds->P * ds->I * ds->R) << ds->m;
   double* x = (double*)malloc(sizeof(double) * (size_t)N * (size_t)ds->C);
   or_rates(ds->counters, ds->cycles, N, ds->C, x);
@@ -540,6 +599,8 @@ int32_t or_evaluate(const or_dataset* ds, const or_scenarios* sc, const or_param
     J->scn_scores = scn_scores + base;
     J->ex = ex ? ex + base * ex_stride : NULL;
     J->recs = recs ? recs + base * rec_stride : NULL;
+    J->kappa = kappa ? kappa + base * ds->O : NULL;
+    J->fit_ld = fit_ld ? fit_ld + base * ds->O : NULL;
     base += c;
     pthread_create(&th[k], NULL, job_run, J);
   }

@@ -471,3 +471,175 @@ def test_knn_pipeline_exact_recall_exp1():
                 v = ((k >> b) << (b + 1)) | (k & ((1 << b) - 1))
                 ac = ds.runtime_ms[g_train * V + v] / ds.runtime_ms[g_train * V + (v | (1 << b))]
                 assert r["ex"][s, o, g_train * 32 + k] == ac
+
+
+# ---------------------------------------------- clamp rule (reading R7)
+def test_pipeline_clamp_rule():
+    # gen.plants.clamp_plant: split 0 holds out version 0, whose feature lies
+    # outside the training range of a planted line AC = 2.1 - x; the ridge
+    # extrapolates to 2.1 - 3 = -0.9 (ridge bias ~1e-8), so S:327 applies:
+    # EX := 0.01, the case is flagged, and the ratio and the sign decision use
+    # the clamped value (AC / 0.01; 0.01 <= 1 while AC = 1.5 > 1: incorrect).
+    from gen.plants import clamp_plant
+    cfg = clamp_plant(x_held=3.0, ac_held=1.5)
+    r = oracle.evaluate(cfg.dataset, cfg.scenarios, 0, 1, want_ex=True, want_recs=True)
+    row = r["opt"][0, 0]
+    assert (row["n_train"], row["n_test"]) == (31, 1)
+    assert row["n_clamped"] == 1 and row["n_correct"] == 0
+    assert r["ex"][0, 0, 0] == 0.01                        # the stored EX is the floor itself
+    assert row["sum_ratio"] == row["min_ratio"] == row["max_ratio"] == 1.5 / 0.01
+    assert r["scn"][0]["n_rec"] == 0                        # 0.01 < 1.05: not recommended
+    # the same fit without the clamp rule: the unclamped prediction is the line
+    Xs, Xts, _ = oracle.scale(oracle.rates(cfg.dataset.counters, cfg.dataset.cycles)[2::2],
+                              oracle.rates(cfg.dataset.counters, cfg.dataset.cycles)[0:1])
+    y = cfg.dataset.runtime_ms[2::2] / cfg.dataset.runtime_ms[3::2]
+    ex, _ = oracle.fit_predict(Xs, y, Xts)
+    assert abs(ex[0] - (2.1 - 3.0)) < 1e-6
+
+
+def test_pipeline_clamp_keeps_positive_predictions():
+    # the other side of the rule: EX ~ 2.1 - 2.05 = 0.05 > 0 is kept as is
+    from gen.plants import clamp_plant
+    cfg = clamp_plant(x_held=2.05, ac_held=0.7)
+    r = oracle.evaluate(cfg.dataset, cfg.scenarios, 0, 1, want_ex=True)
+    row = r["opt"][0, 0]
+    assert row["n_clamped"] == 0
+    assert abs(r["ex"][0, 0, 0] - 0.05) < 1e-6
+    assert abs(row["sum_ratio"] - 0.7 / 0.05) < 1e-3
+    assert row["n_correct"] == 1                            # 0.05 <= 1 and 0.7 <= 1
+
+
+# --------------------------- perfect / constant predictor
+def _brute_test_ac(ds, sc, s, o):
+    """Independent brute force: the AC of every test case of (scenario s, o),
+    for LOO / GROUPS splits (membership written out from the definitions)."""
+    V = 1 << ds.n_opt_bits
+    out = []
+    for g in range(ds.n_groups):
+        p = g // (ds.n_inputs * ds.n_runs)
+        b = int(ds.opt_bit[p, o])
+        if b < 0:
+            continue
+        for v in range(V):
+            if (v >> b) & 1:
+                continue
+            t = g * V + v
+            if sc.kind == "loo":
+                test = t == s
+            else:
+                test = (int(sc.test_groups[s][g // 64]) >> (g % 64)) & 1
+            if test:
+                out.append(ds.runtime_ms[t] / ds.runtime_ms[t | (1 << b)])
+    return out
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_pipeline_perfect_predictor_identity(name):
+    # S:383 / S:407: a predictor with EX = AC scores 100 % and every AC/EX is 1.
+    # (a) the ridge learner itself on gen.plants.pow2_lattice: every pair of an
+    #     optimization has the same (power-of-two) label, a fit on constant
+    #     labels predicts that label exactly (O4(4)), so EX = AC exactly;
+    # (b) the test-only stub learner EX := AC on the unmodified config.
+    from gen.plants import pow2_lattice
+    for cfg, learner in ((pow2_lattice(name), 0), (gen.make_config(name), oracle.LEARNER_PERFECT_STUB)):
+        n = cfg.scenarios.n_scenarios
+        r = oracle.evaluate(cfg.dataset, cfg.scenarios, 0, n, want_ex=True, learner=learner)
+        o, sc = r["opt"], r["scn"]
+        live = o["n_test"] > 0
+        assert live.sum() > 0
+        assert (o["n_correct"] == o["n_test"]).all()
+        assert (o["n_clamped"] == 0).all()
+        assert (o["sum_ratio"][live] == o["n_test"][live]).all()
+        assert (o["min_ratio"][live] == 1.0).all() and (o["max_ratio"][live] == 1.0).all()
+        assert (sc["n_rec_hit"] == sc["n_rec"]).all() and sc["n_rec"].sum() > 0
+
+
+def test_pipeline_constant_predictor_stub():
+    # S:384: with EX := 1 every ratio AC/EX equals AC; EX = 1 is "no gain"
+    # (R11, S:388), so exactly the cases with AC <= 1 are correct; 1 < 1.05:
+    # no recommendation; EX = 1 lies on the sign boundary, so every test case
+    # is a guard case (R21).
+    from fractions import Fraction
+    for name in ("C1", "C2"):
+        cfg = gen.make_config(name)
+        ds, scd = cfg.dataset, cfg.scenarios
+        n = min(scd.n_scenarios, 60)
+        r = oracle.evaluate(ds, scd, 0, n, learner=oracle.LEARNER_CONSTANT_STUB)
+        for s in range(n):
+            om = int(scd.split_opt_masks[s]) if scd.split_opt_masks is not None else 0xFFFFFFFF
+            for o in range(ds.n_opt_ids):
+                row = r["opt"][s, o]
+                if not (om >> o) & 1 or row["n_test"] == 0:
+                    continue
+                ac = _brute_test_ac(ds, scd, s, o)
+                assert len(ac) == row["n_test"]
+                assert row["n_correct"] == sum(a <= 1.0 for a in ac)
+                assert row["min_ratio"] == min(ac) and row["max_ratio"] == max(ac)
+                exact = sum(Fraction(a) for a in ac)
+                assert abs(Fraction(float(row["sum_ratio"])) - exact) <= exact * Fraction(1, 2**52)
+        assert (r["scn"]["n_rec"][:n] == 0).all()
+        assert (r["scn"]["n_guard"][:n] >= r["opt"]["n_test"][:n].sum(1)).all()
+
+
+# ------------------------------------------------------------- kappa^ (O4)
+def test_kappa_closed_form_and_bound():
+    # Orthogonal centred columns: G = diag(|x_a - xbar_a|^2) + lambda I, so the
+    # Cholesky pivots are the diagonal and kappa^ = max/min of it exactly.
+    Xs = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 3.0], [1.0, 3.0]])
+    y = np.array([1.0, 1.2, 0.9, 1.4])
+    lam = 1e-8
+    for prec in ("quad", "ld"):
+        _, _, kap = oracle.fit_predict(Xs, y, Xs, ridge=lam, precision=prec, want_kappa=True)
+        assert abs(kap - (9.0 + lam) / (1.0 + lam)) <= 1e-14 * kap
+    # general case: 1 <= kappa^ <= cond_2(G) (pivots lie inside the spectrum)
+    rng = np.random.default_rng(30)
+    for n, d in ((40, 6), (10, 20), (200, 70)):
+        Xs = rng.uniform(0, 1, (n, d))
+        _, _, kap = oracle.fit_predict(Xs, rng.uniform(0.6, 1.4, n), Xs[:2], want_kappa=True)
+        Xc = Xs - Xs.mean(0)
+        ev = np.linalg.eigvalsh(Xc.T @ Xc + 1e-8 * np.eye(d))
+        assert 1.0 <= kap <= ev[-1] / ev[0] * (1 + 1e-6)
+
+
+# ---------------------------- long-double fits (SURVEY 8(c) precision policy)
+@pytest.mark.parametrize("n,d", [(8, 3), (5, 3), (6, 1)])
+def test_fit_ld_exact_rational_bruteforce(n, d):
+    rng = np.random.default_rng(200 + 10 * n + d)
+    X = rng.uniform(0, 1, size=(n, d))
+    Xs, Xts, _ = oracle.scale(X, rng.uniform(-0.2, 1.2, size=(4, d)))
+    y = rng.uniform(0.6, 1.4, size=n)
+    ex, _ = oracle.fit_predict(Xs, y, Xts, ridge=1e-8, precision="ld")
+    exact = _exact_ridge(Xs, y, Xts, 1e-8)
+    for e, q in zip(ex, exact):
+        assert abs(Fraction(float(e)) - q) <= abs(q) * Fraction(1, 2**50)
+
+
+def test_fit_ld_planted_model_at_c4_width():
+    # p > 65 overdetermined (the only regime the policy sends to long double):
+    # a planted y = c0 + Xs c with lambda = 0 is recovered, and with lambda =
+    # 1e-8 the long-double and quad predictions agree far inside the 1e-9 bar.
+    rng = np.random.default_rng(31)
+    n, d = 1024, 128
+    Xs = rng.uniform(0, 1, size=(n, d))
+    c = rng.normal(0, 0.1, size=d)
+    y = 1.0 + Xs @ c
+    Xts = rng.uniform(0, 1, size=(16, d))
+    ex, coef = oracle.fit_predict(Xs, y, Xts, ridge=0.0, precision="ld")
+    np.testing.assert_allclose(coef, np.r_[1.0, c], rtol=0, atol=1e-11)
+    yn = y + rng.normal(0, 0.01, size=n)
+    exl, _, kl = oracle.fit_predict(Xs, yn, Xts, precision="ld", want_kappa=True)
+    exq, _, kq = oracle.fit_predict(Xs, yn, Xts, precision="quad", want_kappa=True)
+    np.testing.assert_allclose(exl, exq, rtol=1e-14, atol=0)
+    assert abs(kl - kq) <= 1e-10 * kq
+
+
+def test_precision_policy_by_regime():
+    # C3 fits (p <= 65 / underdetermined) stay in quad; C4 fits (n ~ 8192, p =
+    # 129, kappa^ ~ 1e3-1e4) run in long double with kappa^ * 2^-64 < 1e-12.
+    c3 = gen.make_config("C3", n_splits=4)
+    r = oracle.evaluate(c3.dataset, c3.scenarios, 0, 4, want_kappa=True)
+    assert (r["fit_ld"] == 0).all() and np.isfinite(r["kappa"]).all()
+    c4 = gen.make_config("C4", n_splits=1, n_programs=128)
+    r = oracle.evaluate(c4.dataset, c4.scenarios, 0, 1, want_kappa=True)
+    assert (r["fit_ld"] == 1).all()
+    assert (r["kappa"] * 2.0 ** -64 < 1e-12).all() and (r["kappa"] >= 1).all()
