@@ -404,7 +404,9 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     row.fp_test = warp_xor(fpte);
     __syncwarp();
     if (n > 0 && lane == 0) atomicOr(&A.trained[sl], 1u << o);
-    if (n == 0 || nt == 0) {          // untrained (reading R18) or nothing to predict
+    // untrained (reading R18) or nothing to predict; sr_fit (MODE 2) fits every
+    // trained optimization, tested or not (its model is the call's output)
+    if (n == 0 || (nt == 0 && MODE != 2)) {
       if (lane == 0 && A.opt_out) A.opt_out[so * O + o] = row;
       if (A.agg && lane == 0 && nt > 0) atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 1], nt);
       finish(sl, om);
@@ -593,6 +595,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     row.sum_ratio = warp_sum(rsum);
     row.min_ratio = warp_min(rmin);
     row.max_ratio = warp_max(rmax);
+    if (MODE == 2 && nt == 0) row.min_ratio = row.max_ratio = 0.0;   // fitted, nothing tested
     guard = warp_isum(guard);
     tot_corr += row.n_correct;
     tot_test += nt;

@@ -61,6 +61,7 @@ struct BigArgs {
   double* ex_out;
   int8_t* rec_out;
   unsigned long long* totals;
+  int fit_all;        // sr_fit: fit every trained optimization, also those with no test case
 };
 
 __device__ __forceinline__ void member_words(const BigArgs& A, long long split, int g, uint64_t& tr,
@@ -274,14 +275,14 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
     const int nt = cta_scan(cte, G, wsum);
     row.n_train = n;
     row.n_test = nt;
-    if (n == 0 || nt == 0) {
+    if (n == 0 || (nt == 0 && !A.fit_all)) {
       if (t == 0) {
         A.opt_out[sl * O + o] = row;
         A.fitflag[sl * O + o] = n > 0 ? 1 : 0;
         A.c0[sl * O + o] = 0.0;
       }
       for (int c = t; c < C; c += kBigThreads) A.U[(sl * O + o) * C + c] = 0.0;
-      // (t > 0 and n > 0 never happens here; the rank kernel needs no model)
+      // n > 0, nt == 0: the rank kernel needs no model (sr_fit asks for it: fit_all)
       continue;
     }
     #pragma unroll 4

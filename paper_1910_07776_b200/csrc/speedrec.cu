@@ -305,6 +305,10 @@ sr_status sr_load_dataset(sr_ctx* c, const sr_dataset* d) {
   if (d->n_counters > kMaxCounters) return fail(c, SR_E_UNSUPPORTED, "dataset: n_counters=%d > 128", d->n_counters);
   if (d->n_opt_ids > kMaxOpt) return fail(c, SR_E_UNSUPPORTED, "dataset: n_opt_ids=%d > 16", d->n_opt_ids);
   cudaSetDevice(c->device);
+  // the device copies are overwritten below: the old dataset (and the scenario
+  // batch defined on it) stop being valid now, whatever the outcome
+  c->have_ds = false;
+  c->have_sc = false;
   const long long G = (long long)d->n_programs * d->n_inputs * d->n_runs;
   const long long N = G * 64;
   const int C = d->n_counters, O = d->n_opt_ids, P = d->n_programs;
@@ -385,6 +389,10 @@ sr_status sr_define_scenarios(sr_ctx* c, const sr_scenarios* s, int64_t* n_scena
   const uint32_t valid_ids = (c->O >= 32) ? ~0u : ((1u << c->O) - 1u);
   cudaSetDevice(c->device);
   sr_status st;
+  // from here on the previous definition is being overwritten: it stops being
+  // valid now, so a failure below leaves no half-updated batch behind
+  c->have_sc = false;
+  ++c->sc_gen;
   c->sc = *s;
   int np_tr = 0, np_te = 0, n_tg = 0, n_os = 0;
   if (s->kind == SR_SPLIT_GROUPS) {
@@ -613,6 +621,7 @@ sr_status run_mask_path(sr_ctx* c, const sr_params* prm, long long first, long l
   if (const char* e = getenv("SPEEDREC_MASK_PATH"))
     if (atoi(e) == 0) return SR_OK;
   if (c->sweep) return SR_OK;   // sr_sweep ranks on the warp path
+  if (c->coef_req) return SR_OK;   // sr_fit needs the coefficient store of k_fit_warp<.,2>
   if (c->sc.kind != SR_SPLIT_LOO || C > kMaskMaxC || O > kMaskMaxO || prm->learner != SR_LINREG ||
       prm->debug_mcap > 0 || count <= 0 || first % S || count % S || c->sc.n_masks < 2)
     return SR_OK;
@@ -905,6 +914,7 @@ sr_status evaluate_big(sr_ctx* c, const sr_params* prm, long long first, long lo
   B.c0 = (double*)c->big_c0.p;
   B.fitflag = (int32_t*)c->big_flag.p;
   B.totals = tot;
+  B.fit_all = c->coef_req ? 1 : 0;
   const int smem = (kBigMaxD * kBigGLd + kBigChunk * kBigLd + kBigChunk * kBigMaxD + 6 * kBigMaxD + 2 * kBigChunk +
                     16 + 8) * 8 + (2 * kBigMaxD + 2 * G + 20) * 4;
   CU(cudaFuncSetAttribute(k_fit_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -985,7 +995,13 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     return fail(c, SR_E_ARG, "evaluate: k_nn=%d outside [1, %d]", prm->k_nn, kKnnMax);
   if (prm->max_count < 1 || prm->max_count > kMaxRec) return fail(c, SR_E_ARG, "evaluate: max_count=%d", prm->max_count);
   if (prm->refine_steps < 0 || prm->refine_steps > 8) return fail(c, SR_E_ARG, "evaluate: refine_steps=%d", prm->refine_steps);
-  if (!(prm->ridge > 0.0)) return fail(c, SR_E_ARG, "evaluate: ridge must be > 0");
+  if (!(prm->ridge > 0.0) || !std::isfinite(prm->ridge)) return fail(c, SR_E_ARG, "evaluate: ridge must be finite and > 0");
+  // the EX table marks clamped values by sign: the floor must be positive (S:327 uses 0.01)
+  if (!(prm->clamp_floor > 0.0) || !std::isfinite(prm->clamp_floor))
+    return fail(c, SR_E_ARG, "evaluate: clamp_floor must be finite and > 0");
+  if (!std::isfinite(prm->threshold)) return fail(c, SR_E_ARG, "evaluate: threshold must be finite");
+  if (!(prm->guard_tol >= 0.0) || !std::isfinite(prm->guard_tol))
+    return fail(c, SR_E_ARG, "evaluate: guard_tol must be finite and >= 0");
   cudaSetDevice(c->device);
   c->last_launches = 0;
   const int G = c->G, O = c->O, C = c->C;
@@ -1384,6 +1400,7 @@ sr_status sr_predict(const sr_params* prm, const double* coef, int32_t n_opts, i
                      const double* counters, double cycles, double* ex_out) {
   if (!prm || !coef || !counters || !ex_out || n_opts < 1 || n_opts > 16 || n_counters < 1 || n_counters > 128)
     return SR_E_ARG;
+  if (!(prm->clamp_floor > 0.0) || !std::isfinite(prm->clamp_floor)) return SR_E_ARG;
   if (!(cycles > 0.0) || !std::isfinite(cycles)) return SR_E_DATA;
   for (int k = 0; k < n_counters; ++k)
     if (!(counters[k] >= 0.0) || !std::isfinite(counters[k])) return SR_E_DATA;
@@ -1404,7 +1421,7 @@ sr_status sr_predict(const sr_params* prm, const double* coef, int32_t n_opts, i
 sr_status sr_recommend(const sr_params* prm, const double* ex, const uint8_t* candidate, int32_t n_opts,
                        int8_t* rec_out, int32_t* n_rec_out) {
   if (!prm || !ex || !rec_out || !n_rec_out || n_opts < 0 || n_opts > 16 || prm->max_count < 1 ||
-      prm->max_count > 64)
+      prm->max_count > 64 || !std::isfinite(prm->threshold))
     return SR_E_ARG;
   int ids[16], n = 0;
   for (int q = 0; q < n_opts; ++q)

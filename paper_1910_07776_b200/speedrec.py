@@ -166,6 +166,7 @@ class Context:
             raise SpeedrecError(st, f"sr_create(device={device}) failed (needs an sm_100 GPU)")
         self._keep = []
         self.n_scenarios = 0
+        self.n_splits = None
         self.shape = None
 
     def close(self):
@@ -195,6 +196,8 @@ class Context:
             opt_bit = np.ascontiguousarray(opt_bit, dtype=np.int8)
         d = sr_dataset(n_programs, n_inputs, n_runs, n_opt_bits, n_counters, n_opt_ids,
                        _ptr(counters), _ptr(cycles), _ptr(runtime_ms), _ptr(opt_bit), int(dev))
+        self.shape = None             # the library drops the previous dataset on any failure
+        self.n_scenarios = 0
         self._check(lib().sr_load_dataset(self._h, ct.byref(d)))
         self.shape = dict(P=n_programs, I=n_inputs, R=n_runs, C=n_counters, O=n_opt_ids,
                           G=n_programs * n_inputs * n_runs)
@@ -218,9 +221,12 @@ class Context:
         s = sr_scenarios(SPLIT_KIND[sc.kind], sc.group_words, sc.n_splits, _ptr(tg), _ptr(eg), _ptr(om),
                          _ptr(pg), sc.seed, sc.opt_mask, sc.all_subsets_k, sc.n_masks, _ptr(fm))
         n = ct.c_int64()
+        self.n_scenarios = 0          # the library drops the previous definition on any failure
+        self.n_splits = None
         self._check(lib().sr_define_scenarios(self._h, ct.byref(s), ct.byref(n)))
         self._keep = []
         self.n_scenarios = n.value
+        self.n_splits = int(sc.n_splits)
         return n.value
 
     # ------------------------------------------------------------ compute
@@ -249,7 +255,10 @@ class Context:
             tot = np.zeros(4, dtype=np.int64)
             masks = top = None
             if want_masks:
-                masks = np.zeros(count // n_folds, dtype=MASK_SCORE_DTYPE)
+                folds = n_folds if n_folds is not None else getattr(self, "n_splits", None)
+                if not folds:
+                    raise ValueError("evaluate(want_masks=True): define_scenarios first (mask rows sum its n_splits folds)")
+                masks = np.zeros(count // folds, dtype=MASK_SCORE_DTYPE)
                 top = np.zeros(p.top_k, dtype=np.int64)
             o = sr_outputs(_ptr(opt), _ptr(scn), _ptr(ex), _ptr(recs), _ptr(tot), _ptr(masks), _ptr(top), 0)
             self._check(lib().sr_evaluate(self._h, ct.byref(p), first, count, ct.byref(o)))
