@@ -9,8 +9,11 @@ One step = one sr_evaluate call over the rank's batch of scenarios: A0 rates,
 A1 labels + pairs, A2-A7 fused (three kernel launches).  Default workload =
 config C3 (2 programs x 64 variants x 64 counters, 1e6 random train/test
 splits per GPU; weak scaling: rank r evaluates splits [r*S, (r+1)*S)).
-Under torchrun each rank drives one GPU; the only collective is the NCCL
-all-reduce of the pooled integer totals (A7 "per config") and of the timing.
+Under torchrun each rank drives one GPU and evaluates its own scenario
+shard with no collective on the data path; each step then gathers the
+per-scenario score tables to rank 0 with one NCCL all_gather_into_tensor per
+table (inside the timed step, also reported on its own as
+`gather`), and the pooled integer totals and the timing are all-reduced.
 """
 from __future__ import annotations
 
@@ -266,6 +269,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg (tuning runs)")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the secondary per-config lines (C1, C2, C4, C5) of the default run")
+    ap.add_argument("--dump-tables", default=None,
+                    help="rank 0 writes the gathered score tables (npz) here (tests/test_gpu_dist.py)")
     ap.add_argument("--sweep", type=int, default=0,
                     help="NEXT-3: time sr_sweep with this many thresholds x 4 list lengths instead of sr_evaluate")
     args = ap.parse_args()
@@ -337,6 +342,17 @@ def main():
     from paper_1910_07776_b200.speedrec import default_params
     prm = default_params(learner=LEARNERS[args.learner], top_k=64)
 
+    # score-table gather: fixed-size rows, rank order = scenario order
+    if c5:
+        all_masks = [D.stratified_masks(args.masks_k, r, world) for r in range(world)]
+        mpad = torch.zeros(max(len(m) for m in all_masks) * 16, dtype=torch.uint8, device=dev)
+
+    def gather_tables():
+        if c5:
+            mpad[:out["masks"].numel()].copy_(out["masks"])
+            return {"masks": D.gather_rows(mpad.to(xdev), dist)}
+        return {"opt": D.gather_rows(out["opt"].to(xdev), dist), "scn": D.gather_rows(out["scn"].to(xdev), dist)}
+
     for _ in range(args.warmup):
         ctx.evaluate(first, count, params=prm, out=out)
     torch.cuda.synchronize()
@@ -345,6 +361,8 @@ def main():
     ctx.set_timing(True)
     ctx.reset_kernel_stats()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    gevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    tables = None
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -353,18 +371,26 @@ def main():
             flush.fill_(float(k))
             evs[k][0].record(stream)
             ctx.evaluate(first, count, params=prm, out=out)
+            gevs[k][0].record(stream)
+            if world > 1:
+                tables = gather_tables()
+            gevs[k][1].record(stream)
             evs[k][1].record(stream)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
+    if tables is None:
+        tables = gather_tables()
     step_ms = [a.elapsed_time(b) for a, b in evs]
+    gather_ms = D.max_over_ranks(float(np.mean([a.elapsed_time(b) for a, b in gevs])), dist, device=xdev)
     stats = ctx.kernel_stats()
     ctx.set_timing(False)
     launches = sum(v[0] for v in stats.values())
     my_ms = float(np.mean(step_ms))
     ms = D.max_over_ranks(my_ms, dist, device=xdev)           # max over ranks (device-timed)
     tot = D.reduce_totals(out["totals"].to(xdev), dist)       # pooled A7 totals (exact)
-    value = world * count / (ms / 1e3)
+    # whole-job throughput: every scenario all ranks evaluated (C5: all 2^k masks x folds)
+    value = ((1 << args.masks_k) * folds if c5 else world * count) / (ms / 1e3)
 
     # ---------------- roofline of the dominant kernel (FP64 ALU/DMMA bound)
     big = ds.n_groups > 64          # CTA-per-fit path (C4): prediction runs in k_rank_big
@@ -475,6 +501,14 @@ def main():
                "kind": "oracle",
                "sample": f"first {args.cpu_sample} scenarios of {args.config} (same splits the GPU evaluates)"}
 
+    # rank 0: the gathered tables in global scenario (C5: mask) order
+    gathered, pooled = None, None
+    if rank == 0:
+        if c5:
+            gathered = {"masks": D.scatter_mask_rows(tables["masks"].cpu().numpy(), all_masks, 1 << args.masks_k)}
+        else:
+            gathered = {k: v.cpu().numpy() for k, v in tables.items()}
+            pooled = D.pooled_ratio(gathered["opt"])
     top_global = None
     if c5:   # C5 A7: local top-64 (library) -> global mask ids -> exact merge over ranks
         from paper_1910_07776_b200.speedrec import MASK_SCORE_DTYPE
@@ -503,6 +537,11 @@ def main():
                                         "per fit (DESIGN 6)" if args.learner == "m5"
                                         else "algorithmic flops of the fits (DESIGN 6)")},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "gather": {"collective": "all_gather_into_tensor" if world > 1 else "none (1 GPU)",
+                       "backend": backend if world > 1 else None, "ms_per_step": gather_ms,
+                       "bytes_per_rank": int(sum(v.numel() for v in tables.values()) // world) if world > 1 else 0,
+                       "in_step": True},
+            "pooled_ratio": pooled,
             "clocks": clk_sum,
             "accuracy": {"pooled_sign_accuracy_pct": 100.0 * tt[0] / max(tt[1], 1), "cases": int(tt[1]),
                          "recommendations": int(tt[2]), "rec_hits": int(tt[3])},
@@ -512,6 +551,9 @@ def main():
             line["config"].update(masks_k=args.masks_k, masks_per_gpu=int(len(masks)), folds=int(folds),
                                   partition="popcount-stratified round-robin (SURVEY 8(e))")
             line["top_masks_head"] = [int(m) for m in top_global[:8]]
+        if args.dump_tables:
+            extra = {"top": np.asarray(top_global)} if c5 else {}
+            np.savez(args.dump_tables, totals=tot.cpu().numpy(), **gathered, **extra)
         if world == 1 and args.config == "C3" and not args.no_extra:
             ctx.synchronize()
             line["other_configs"] = run_other_configs(args)

@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
 
     // ---- A5: predict + clamp; A7 per-(s,o) scores ----
     double* ext = A.extab + sl * A.ex_stride + q * A.tg_stride;
-    int ncorr = 0, ncl = 0, guard = ok ? 0 : 1000000;
+    int ncorr = 0, ncl = 0, guard = (ok || lane != 0) ? 0 : 1000000;   // per lane, summed below
     double rsum = 0.0, rmin = INFINITY, rmax = -INFINITY;
     auto score = [&](const int j, double e) {
       if (near_tol(e, 0.0, A.guard_tol) || near_tol(e, 1.0, A.guard_tol)) ++guard;
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
       int tg = 0;
       bool tok = true;
       m5_build(W, n, deff, yc, A.lambda, A.refine, A.guard_tol, lane, &tg, &tok);
-      guard += tg + (tok ? 0 : 1000000);
+      if (lane == 0) guard += tg + (tok ? 0 : 1000000);   // warp-uniform counts: once, not per lane
       for (int j = lane; j < nt; j += 32) score(j, m5_predict(W, X + (long long)tes[j] * ldx, col, uv, wv));
     } else if (ibk) {   // NEXT-1: IBk prediction, all lanes sweep together (knn_ex)
       const int kk = min(A.k_nn, n);

@@ -1155,6 +1155,11 @@ static __global__ void __launch_bounds__(kBigThreads, 1) k_rank_big4(const BigAr
         }
       }
     }
+    // the next iteration's cp.async stage(g + 2) overwrites this group's label
+    // buffer ys[g & 1]: every thread must be done scoring group g first (a
+    // thread with no scenario of its own otherwise races ahead; found by the
+    // single-scenario C4 parity test, tests/test_gpu_samples.py)
+    __syncthreads();
   }
   // ---- deterministic reduction per scenario: lanes (butterfly), its 2 warps in order ----
 #pragma unroll

@@ -1,11 +1,18 @@
-"""Multi-GPU plumbing of the scenario-sharded path (DESIGN.md §7).
+"""Multi-GPU plumbing of the scenario-sharded path (DESIGN.md §7; SURVEY §8(e)).
 
-One process per GPU (torchrun).  Scenarios are independent, so the only
-exchange steps are (a) the pooled integer totals of A7 ("per config" sign
-accuracy, recommendation hits) and (b) for C5 the global top-K mask ranking,
-both exact because they are integer reductions / integer-key selections.
-Timing is the max over ranks.  Works with the "nccl" backend on GPUs and the
-"gloo" backend on CPU (tests/test_dist.py).
+One process per GPU (torchrun).  Scenarios are independent, so there is no
+collective on the data path; the exchange steps come after it:
+  (a) the per-scenario score tables (fixed-size sr_opt_score / sr_scn_score
+      rows, or C5's sr_mask_score rows) gathered to rank 0 with ONE
+      all_gather_into_tensor each (NCCL over NVLink on GPUs), in rank order =
+      scenario order, so the N-GPU table is byte-identical to the 1-GPU one;
+  (b) the pooled integer totals of A7 ("per config" sign accuracy,
+      recommendation hits), an exact integer all-reduce;
+  (c) for C5 the global top-K mask ranking, an exact integer-key merge.
+FP statistics over scenarios are computed on rank 0 from the gathered table
+(`pooled_ratio`), so they do not depend on the GPU count either.  Timing is
+the max over ranks.  Works with "nccl" on GPUs and "gloo" on CPU
+(tests/test_dist.py, tests/test_gpu_dist.py).
 """
 from __future__ import annotations
 
@@ -89,3 +96,39 @@ def merge_top_masks(local_ids, local_correct, k: int, dist, device="cpu") -> np.
     allk = np.sort(allk[allk != 0])[::-1][:k]
     ids = (0xFFFFFFFF - (allk & np.uint64(0xFFFFFFFF))).astype(np.int64)
     return np.concatenate([ids, -np.ones(k - len(ids), dtype=np.int64)])
+
+
+def gather_rows(rows, dist):
+    """All-gather one rank's fixed-size score rows (a 1-D uint8 tensor of
+    equal length on every rank: weak scaling gives each rank the same number
+    of scenarios) into [world * len] in rank order, with ONE
+    all_gather_into_tensor.  World 1: the rows themselves."""
+    import torch
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return rows
+    out = torch.empty(rows.numel() * dist.get_world_size(), dtype=rows.dtype, device=rows.device)
+    dist.all_gather_into_tensor(out, rows.contiguous())
+    return out
+
+
+def scatter_mask_rows(gathered, masks_of_rank, n_masks: int, row_bytes: int = 16):
+    """C5: the gathered mask rows of every rank (rank r's rows for its
+    stratified masks, padded to the longest list) -> one [n_masks] table in
+    global mask order (numpy uint8 [n_masks * row_bytes])."""
+    g = np.asarray(gathered).reshape(len(masks_of_rank), -1)
+    out = np.zeros((n_masks, row_bytes), dtype=np.uint8)
+    for r, m in enumerate(masks_of_rank):
+        out[m] = g[r, :len(m) * row_bytes].reshape(len(m), row_bytes)
+    return out.reshape(-1)
+
+
+def pooled_ratio(opt_rows) -> dict:
+    """Per-config FP statistics from a full (gathered) sr_opt_score table, in
+    scenario order: sum of AC/EX over all test cases (math.fsum: correctly
+    rounded, so the value is one function of the table) and its mean."""
+    import math
+    from .speedrec import OPT_SCORE_DTYPE
+    o = np.asarray(opt_rows).view(OPT_SCORE_DTYPE).ravel()
+    n = int(o["n_test"].astype(np.int64).sum())
+    s = math.fsum(o["sum_ratio"][o["n_test"] > 0].tolist())
+    return {"sum_ratio": s, "cases": n, "mean_ratio": s / n if n else None}

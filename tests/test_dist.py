@@ -137,3 +137,54 @@ def test_topk_key_order_matches_rule():
     keys = [D.topk_key(c, m) for c, m in ((5, 3), (9, 7), (9, 2), (0, 0))]
     order = np.argsort(keys)[::-1]
     assert list(order) == [2, 1, 0, 3]
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1910_07776_b200.speedrec import OPT_SCORE_DTYPE
+        # weak scaling: rank r holds rows of scenarios [r*S, (r+1)*S) of one table
+        full = _table(2 * 50)
+        mine = full[rank * 50 * 6:(rank + 1) * 50 * 6]
+        t = torch.from_numpy(mine.view(np.uint8).copy())
+        g = D.gather_rows(t, dist).numpy()
+        # C5: stratified mask lists of unequal length, padded, scattered back
+        allm = [D.stratified_masks(5, r, world) for r in range(world)]
+        rows = np.arange(32 * 16, dtype=np.int64).astype(np.uint8).reshape(32, 16)
+        pad = np.zeros((max(len(m) for m in allm), 16), np.uint8)
+        pad[:len(allm[rank])] = rows[allm[rank]]
+        gm = D.gather_rows(torch.from_numpy(pad.reshape(-1)), dist).numpy()
+        q.put((rank, g.tobytes() == full.view(np.uint8).tobytes(),
+               D.scatter_mask_rows(gm, allm, 32).tobytes() == rows.tobytes(),
+               D.pooled_ratio(g) == D.pooled_ratio(full.view(np.uint8))))
+    finally:
+        dist.destroy_process_group()
+
+
+def _table(n_scn, O=6):
+    from paper_1910_07776_b200.speedrec import OPT_SCORE_DTYPE
+    rng = np.random.default_rng(4)
+    o = np.zeros(n_scn * O, dtype=OPT_SCORE_DTYPE)
+    o["n_test"] = rng.integers(0, 40, size=o.size)
+    o["sum_ratio"] = o["n_test"] * rng.uniform(0.5, 1.5, size=o.size)
+    o["fp_train"] = rng.integers(0, 2**63, size=o.size)
+    return o
+
+
+def test_gloo_world2_score_table_gather_is_byte_identical():
+    # one all_gather_into_tensor of fixed-size rows per table; the
+    # gathered table (rank order = scenario order) equals the 1-process table
+    # byte for byte, and the FP pooled statistic computed from it is the same.
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, same, same_masks, same_pool in res:
+        assert same and same_masks and same_pool, (rank, same, same_masks, same_pool)
