@@ -269,7 +269,10 @@ __device__ __forceinline__ void rank_scenario(const EvalArgs& A, long long sl, i
 
 // ---------------------------------------------------------------- fit kernel
 // MODE 0: ridge LS (the paper's model); 1: IBK (NEXT-1); 2: ridge LS + the
-// sr_fit coefficient store; 3: M5P model tree (NEXT-2, m5_warp.cuh).  Separate instantiations keep the hot code lean.
+// sr_fit coefficient store; 3: M5P model tree (NEXT-2, m5_warp.cuh); 4: ridge
+// LS writing each fit's model (u, c0) and counts to the model table, with A5-A7
+// in k_pred_rank (pred_rank.cuh).  Separate instantiations
+// keep the hot code lean.
 // STAGED: x staged in shared memory (compile-time, so every x access is an
 // LDS rather than a generic load).
 template <int WMAX, int MODE, bool STAGED>
@@ -351,6 +354,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
       continue;
     }
     const int q = __popc(om & ((1u << o) - 1u));  // scored-optimization slot in the EX table
+    double* urow = MODE == 4 ? A.utab + (sl * (long long)A.n_os + q) * A.ldu : nullptr;
 
     // ---- A1: split membership (Table 2; R17), features, pairs ----
     for (int g = lane; g < G; g += 32) {
@@ -389,9 +393,11 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
           fptr ^= h;
         }
         if (iste) {
-          const int p = nt + __popc(mte & lt);
-          tes[p] = g * 64 + v;
-          tek[p] = g * 32 + lane;
+          if (MODE != 4) {              // MODE 4 predicts in k_pred_rank: counts only
+            const int p = nt + __popc(mte & lt);
+            tes[p] = g * 64 + v;
+            tek[p] = g * 32 + lane;
+          }
           fpte ^= h;
         }
       }
@@ -403,10 +409,24 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     row.fp_train = warp_xor(fptr);
     row.fp_test = warp_xor(fpte);
     __syncwarp();
-    if (n > 0 && lane == 0) atomicOr(&A.trained[sl], 1u << o);
+    if (n > 0 && lane == 0 && MODE != 4) atomicOr(&A.trained[sl], 1u << o);
+    auto put_counts = [&](double flag) {   // MODE 4: the model-table row's fields after u, c0
+      if (lane == 0) {
+        double* e = urow + A.C;
+        e[kUflag] = flag;
+        e[kUntr] = (double)n;
+        e[kUnte] = (double)nt;
+        e[kUfptr] = __longlong_as_double((long long)row.fp_train);
+        e[kUfpte] = __longlong_as_double((long long)row.fp_test);
+      }
+    };
     // untrained (reading R18) or nothing to predict; sr_fit (MODE 2) fits every
     // trained optimization, tested or not (its model is the call's output)
     if (n == 0 || (nt == 0 && MODE != 2)) {
+      if (MODE == 4) {
+        put_counts(n > 0 ? 1.0 : 0.0);
+        continue;
+      }
       if (lane == 0 && A.opt_out) A.opt_out[so * O + o] = row;
       if (A.agg && lane == 0 && nt > 0) atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 1], nt);
       finish(sl, om);
@@ -524,6 +544,12 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
         double* cf = A.coef_out + (sl * O + o) * (long long)(C + 1);
         for (int c = lane; c < C; c += 32) cf[1 + c] = ufull[c];
         if (lane == 0) cf[0] = c0;
+      }
+      if (MODE == 4) {   // the model for k_pred_rank (A5-A7 there)
+        for (int c = lane; c < C; c += 32) urow[c] = ufull[c];
+        if (lane == 0) urow[C + kUc0] = c0;
+        put_counts(ok ? 1.0 : 2.0);
+        continue;
       }
     }
 

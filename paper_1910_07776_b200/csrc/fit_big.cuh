@@ -162,14 +162,6 @@ __device__ __forceinline__ void big_load_rows(const double* X, int C, int slot, 
   }
 }
 
-// 8-byte asynchronous global -> shared copy (LDGSTS); zero-fills when !valid.
-__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gsrc), "r"(valid ? 8 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Training slot of this thread's row in chunk ch (-1 past n).
 __device__ __forceinline__ int big_slot(const int32_t* trs, int n, int ch) {

@@ -127,7 +127,15 @@ struct EvalArgs {
   int off_warps;         // byte offset of the first warp slab
   double* gscratch;      // per global warp: mscratch doubles (large systems: factor + 2 vectors)
   long long mscratch;
+  // model table of the split LS path (k_fit_warp MODE 4 -> k_pred_rank):
+  // [count][n_os][ldu]: u[0..C) raw-counter weights, then c0, flag, n_train,
+  // n_test, fp_train bits, fp_test bits (flag 0 untrained, 1 fitted, 2 non-positive pivot)
+  double* utab;
+  int ldu;
+  int n_os;              // scored-optimization slots per scenario (table rows)
 };
+// model-table row fields after the C weights (k_fit_warp MODE 4 / k_pred_rank)
+constexpr int kUc0 = 0, kUflag = 1, kUntr = 2, kUnte = 3, kUfptr = 4, kUfpte = 5, kUextra = 6;
 
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -251,6 +259,20 @@ __device__ __forceinline__ bool near_tol(double a, double b, double tol) {
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// 8-byte asynchronous global -> shared copy (LDGSTS); zero-fills when !valid.
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gsrc), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+// 16-byte asynchronous global -> shared copy (LDGSTS, bypassing L1).
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
 }
 
 // ---------------------------------------------------------------- A0 / A1

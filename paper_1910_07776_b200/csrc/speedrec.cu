@@ -22,6 +22,7 @@
 #include "fit_big.cuh"
 #include "ibk_big.cuh"
 #include "kernels.cuh"
+#include "pred_rank.cuh"
 
 using namespace speedrec;
 
@@ -88,6 +89,7 @@ struct sr_ctx {
   const SweepArgs* sweep = nullptr;   // set by sr_sweep for the duration of its evaluate
   DevBuf sw_buf;
   DevBuf extab, trained, guard_acc, mask_acc, done;   // fit -> rank exchange (warp path)
+  DevBuf utab;                                        // fit -> k_pred_rank model table (split LS path)
   // accounting
   bool timing = false;
   std::vector<KStat> kstats;
@@ -265,7 +267,8 @@ void sr_destroy(sr_ctx* c) {
                     &c->out_top, &c->keys_a, &c->keys_b, &c->big_lists, &c->big_y, &c->big_U, &c->big_c0,
                     &c->big_flag, &c->extab, &c->trained, &c->guard_acc, &c->mask_acc, &c->done, &c->fit_coef,
                     &c->mp_G, &c->mp_r, &c->mp_z, &c->mp_meta, &c->mp_perm, &c->mp_rec, &c->mp_order,
-                    &c->mp_units, &c->mp_pfx, &c->mp_glist, &c->sw_buf, &c->ibk_lists, &c->ibk_xs, &c->ibk_meta})
+                    &c->mp_units, &c->mp_pfx, &c->mp_glist, &c->sw_buf, &c->ibk_lists, &c->ibk_xs, &c->ibk_meta,
+                    &c->utab})
     release(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->cp_events) cudaEventDestroy(e);
@@ -1044,13 +1047,19 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   int stage = stage_bytes <= 96 * 1024 && prm->learner != SR_M5P ? 1 : 0;
   if (const char* e = getenv("SPEEDREC_STAGE")) stage = atoi(e) && stage_bytes <= 96 * 1024;
   int wmax = kMaxWarpsPerBlock;
-  if (const char* e = getenv("SPEEDREC_WMAX")) wmax = atoi(e) >= 16 ? 16 : 12;
+  if (const char* e = getenv("SPEEDREC_WMAX")) {
+    const int w = atoi(e);
+    wmax = w >= 16 ? 16 : 12;   // 20/24 warps with a smaller factor cap: slower (profiles/r2e_ab_occupancy.txt)
+  }
   if (prm->learner != SR_LINREG || c->coef_req) wmax = 16;   // the one IBK / M5P / sr_fit instantiation
   if (prm->learner == SR_M5P) wmax = SR_M5_WMAX;
   int budget_cap = budget;
   if (const char* e = getenv("SPEEDREC_SMEM_KB")) budget_cap = std::min(budget, std::max(16, atoi(e)) * 1024);
   int mcap = std::min(mmax, 32);
   if (prm->debug_mcap > 0) mcap = std::min(mcap, prm->debug_mcap);
+  // A/B knob: a smaller shared-memory factor (rare larger systems go to the
+  // global-scratch path) frees shared memory for more warps per SM
+  if (const char* e = getenv("SPEEDREC_MCAP")) mcap = std::min(mcap, std::max(8, atoi(e)));
   WarpLayout L = plan_layout(c, mcap, prm->learner == SR_IBK);
   int avail = budget_cap - head - (stage ? align16((int)stage_bytes) : 0);
   int wpb = std::min(wmax, avail / std::max(L.bytes, 1));
@@ -1090,7 +1099,36 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.off_stage = head;
   A.off_warps = head + (stage ? align16((int)stage_bytes) : 0);
   const int smem = A.off_warps + wpb * L.bytes;
-  auto kfit = prm->learner == SR_IBK ? (stage ? k_fit_warp<16, 1, true> : k_fit_warp<16, 1, false>)
+  // split LS path: k_fit_warp<16, 4, true> leaves each fit's
+  // model in a table, k_pred_rank predicts (DMMA), scores and ranks per
+  // scenario -- no EX table, no k_rank_warp.  SPEEDREC_SPLIT_LS=0 (or the
+  // opt-in fused ranking) keeps the EX-table path.
+  bool split_ls = prm->learner == SR_LINREG && !c->coef_req && !c->sweep && !agg && stage && C <= kPrMaxC &&
+                  c->n_os <= 8 && wmax == 16;
+  if (const char* e = getenv("SPEEDREC_SPLIT_LS")) split_ls = split_ls && atoi(e) != 0;
+  if (const char* e = getenv("SPEEDREC_FUSE_RANK")) split_ls = split_ls && atoi(e) == 0;
+  // k_pred_rank's shared-memory plan: rates staged with a row stride = 4 mod 16
+  // doubles (conflict-free DMMA fragment loads), labels, per-warp EX tiles
+  PredLayout PL{};
+  if (split_ls) {
+    int ld = ((C + 3) / 4) * 4;
+    while (ld % 16 != 4) ld += 4;
+    const int cm = c->n_os <= 6 ? 6 : 8;
+    const int ldu_ = ((C + kUextra + 1) / 2) * 2;
+    int ldut = ldu_;
+    while (ldut % 16 != 4) ldut += 2;
+    PL.ldxp = ld;
+    PL.ldut = ldut;
+    PL.off_x = align16(c->P * O);
+    PL.off_y = PL.off_x + align16((int)(N * ld * 8));
+    PL.off_w = PL.off_y + align16((G * O * 32 + ldut) * 8);
+    PL.wbytes = align16(2 * cm * ldut * 8 + kPrChunk * (cm + 1) * 8 + 8 * 4 + (int)N * 2);
+    PL.warps = std::min(kPrWarps, (budget - PL.off_w) / PL.wbytes);
+    PL.bytes = PL.off_w + PL.warps * PL.wbytes;
+    if (PL.warps < 4) split_ls = false;
+  }
+  auto kfit = split_ls ? k_fit_warp<16, 4, true>
+              : prm->learner == SR_IBK ? (stage ? k_fit_warp<16, 1, true> : k_fit_warp<16, 1, false>)
               : prm->learner == SR_M5P ? (stage ? k_fit_warp<SR_M5_WMAX, 3, true> : k_fit_warp<SR_M5_WMAX, 3, false>)
               : c->coef_req      ? (stage ? k_fit_warp<16, 2, true> : k_fit_warp<16, 2, false>)
               : wmax == 16       ? (stage ? k_fit_warp<16, 0, true> : k_fit_warp<16, 0, false>)
@@ -1105,10 +1143,18 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   const int ex_stride = c->n_os * tg_stride;
   long long chunk_bytes = 1024LL << 20;                 // EX table per launch (SPEEDREC_CHUNK_MB overrides; tools/sweep_c3.sh)
   if (const char* e = getenv("SPEEDREC_CHUNK_MB")) chunk_bytes = std::max(1LL, atoll(e)) << 20;
-  const long long chunk = std::max(1LL, std::min<long long>(count, chunk_bytes / (8LL * ex_stride)));
-  if ((st = ensure(c, c->extab, (size_t)chunk * ex_stride * 8)) || (st = ensure(c, c->trained, (size_t)chunk * 4)) ||
-      (st = ensure(c, c->guard_acc, (size_t)chunk * 4)) || (st = ensure(c, c->done, (size_t)chunk * 4)))
+  const int ldu = ((C + kUextra + 1) / 2) * 2;        // model-table row (split LS path)
+  const long long row_bytes = split_ls ? 8LL * c->n_os * ldu : 8LL * ex_stride;
+  const long long chunk = std::max(1LL, std::min<long long>(count, chunk_bytes / row_bytes));
+  if (split_ls) {
+    if ((st = ensure(c, c->utab, (size_t)(chunk * row_bytes)))) return st;
+  } else if ((st = ensure(c, c->extab, (size_t)chunk * ex_stride * 8)) || (st = ensure(c, c->trained, (size_t)chunk * 4)) ||
+             (st = ensure(c, c->guard_acc, (size_t)chunk * 4)) || (st = ensure(c, c->done, (size_t)chunk * 4))) {
     return st;
+  }
+  A.utab = (double*)c->utab.p;
+  A.ldu = ldu;
+  A.n_os = c->n_os;
   A.extab = (double*)c->extab.p;
   A.ex_stride = ex_stride;
   A.tg_stride = tg_stride;
@@ -1190,8 +1236,10 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     A.first = first + c0;
     A.count = cc;
     A.out0 = c0;
-    CU(cudaMemsetAsync(A.trained, 0, (size_t)cc * 4, c->stream));
-    CU(cudaMemsetAsync(A.guard_acc, 0, (size_t)cc * 4, c->stream));
+    if (!split_ls) {
+      CU(cudaMemsetAsync(A.trained, 0, (size_t)cc * 4, c->stream));
+      CU(cudaMemsetAsync(A.guard_acc, 0, (size_t)cc * 4, c->stream));
+    }
     // fused ranking in the LS fit kernel: opt-in (SPEEDREC_FUSE_RANK=1).  Its
     // per-fit __threadfence + cross-SM counter made the C3 step 2x slower
     // (108 vs 56 ms), so k_rank_warp stays the default.
@@ -1201,6 +1249,13 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     if (A.fuse_rank) CU(cudaMemsetAsync(A.done, 0, (size_t)cc * 4, c->stream));
     const long long fblocks = std::max(1LL, std::min(max_fit_blocks, (cc * O + wpb - 1) / wpb));
     if ((st = launch(c, "k_fit_warp", [&] { kfit<<<(unsigned)fblocks, wpb * 32, smem, c->stream>>>(A); }))) return st;
+    if (split_ls) {
+      auto kpr = c->n_os <= 6 ? k_pred_rank<6> : k_pred_rank<8>;
+      CU(cudaFuncSetAttribute(kpr, cudaFuncAttributeMaxDynamicSharedMemorySize, PL.bytes));
+      const long long pblocks = std::max(1LL, std::min<long long>(c->sm_count, (cc + PL.warps - 1) / PL.warps));
+      if ((st = launch(c, "k_pred_rank", [&] { kpr<<<(unsigned)pblocks, PL.warps * 32, PL.bytes, c->stream>>>(A, PL); })))
+        return st;
+    }
     const long long rblocks = std::max(1LL, std::min<long long>((long long)c->sm_count * 8, (cc + 7) / 8));
     if (c->sweep) {   // NEXT-3 rule sweep instead of the single-rule ranking
       const SweepArgs W = *c->sweep;
@@ -1210,7 +1265,9 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
       continue;
     }
     if (A.fuse_rank) continue;
-    if (c->n_os <= 6) {   // the paper's six optimizations: no empty candidate slots
+    if (split_ls) {
+      // (ranking done by k_pred_rank)
+    } else if (c->n_os <= 6) {   // the paper's six optimizations: no empty candidate slots
       if ((st = launch(c, "k_rank_warp", [&] { k_rank_warp<6><<<(unsigned)rblocks, 256, 0, c->stream>>>(A); })))
         return st;
     } else if (cmax == 8) {
