@@ -436,47 +436,53 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     // ---- A2: per-fit min-max statistics over the training befores (D3) ----
     constexpr bool ibk = MODE == 1, m5 = MODE == 3;
     int deff = 0;
+    // rates are finite and >= 0 (sr_load_dataset validates them), so min/max
+    // need no NaN handling: one compare + select each (dmin/dmax)
+    const unsigned xs32 = STAGED ? (unsigned)__cvta_generic_to_shared(X) : 0u;
+    const int ldx8 = ldx * 8;
     for (int a0 = 0; a0 < d; a0 += 64) {       // two features per lane per row pass
       const int a1 = a0 + lane, a2 = a0 + 32 + lane;
       const int c1 = a1 < d ? F[a1] : 0, c2 = a2 < d ? F[a2] : 0;
-      const double* x0 = X + trs[0] * ldx;
-      double mn1 = x0[c1], mx1 = mn1, sm1 = mn1, mn2 = x0[c2], mx2 = mn2, sm2 = mn2;
+      const int o1 = c1 * 8, o2 = c2 * 8;
+      const int r0 = trs[0] * ldx8;
+      double mn1 = xload<STAGED>(X, xs32, r0 + o1), mx1 = mn1, sm1 = mn1;
+      double mn2 = xload<STAGED>(X, xs32, r0 + o2), mx2 = mn2, sm2 = mn2;
       // two rows per pass into separate accumulators (independent min/max chains)
       double nb1 = mn1, xb1 = mx1, tb1 = 0.0, nb2 = mn2, xb2 = mx2, tb2 = 0.0;
       int i = 1;
       SR_UNROLL(SR_UNROLL_STATS)
       for (; i + 1 < n; i += 2) {
-        const double* xr = X + trs[i] * ldx;
-        const double* xq = X + trs[i + 1] * ldx;
-        const double v1 = xr[c1], v2 = xr[c2], w1 = xq[c1], w2 = xq[c2];
-        mn1 = fmin(mn1, v1);
-        nb1 = fmin(nb1, w1);
-        mx1 = fmax(mx1, v1);
-        xb1 = fmax(xb1, w1);
+        const int ri = trs[i] * ldx8, rq = trs[i + 1] * ldx8;
+        const double v1 = xload<STAGED>(X, xs32, ri + o1), v2 = xload<STAGED>(X, xs32, ri + o2);
+        const double w1 = xload<STAGED>(X, xs32, rq + o1), w2 = xload<STAGED>(X, xs32, rq + o2);
+        mn1 = dmin(mn1, v1);
+        nb1 = dmin(nb1, w1);
+        mx1 = dmax(mx1, v1);
+        xb1 = dmax(xb1, w1);
         sm1 += v1;
         tb1 += w1;
-        mn2 = fmin(mn2, v2);
-        nb2 = fmin(nb2, w2);
-        mx2 = fmax(mx2, v2);
-        xb2 = fmax(xb2, w2);
+        mn2 = dmin(mn2, v2);
+        nb2 = dmin(nb2, w2);
+        mx2 = dmax(mx2, v2);
+        xb2 = dmax(xb2, w2);
         sm2 += v2;
         tb2 += w2;
       }
       if (i < n) {
-        const double* xr = X + trs[i] * ldx;
-        const double v1 = xr[c1], v2 = xr[c2];
-        mn1 = fmin(mn1, v1);
-        mx1 = fmax(mx1, v1);
+        const int ri = trs[i] * ldx8;
+        const double v1 = xload<STAGED>(X, xs32, ri + o1), v2 = xload<STAGED>(X, xs32, ri + o2);
+        mn1 = dmin(mn1, v1);
+        mx1 = dmax(mx1, v1);
         sm1 += v1;
-        mn2 = fmin(mn2, v2);
-        mx2 = fmax(mx2, v2);
+        mn2 = dmin(mn2, v2);
+        mx2 = dmax(mx2, v2);
         sm2 += v2;
       }
-      mn1 = fmin(mn1, nb1);
-      mx1 = fmax(mx1, xb1);
+      mn1 = dmin(mn1, nb1);
+      mx1 = dmax(mx1, xb1);
       sm1 += tb1;
-      mn2 = fmin(mn2, nb2);
-      mx2 = fmax(mx2, xb2);
+      mn2 = dmin(mn2, nb2);
+      mx2 = dmax(mx2, xb2);
       sm2 += tb2;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -521,9 +527,9 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
       // refine where conditioning or the O(n eps) Gram accumulation error needs it
       const int nref = (dual ? 2 * (n - 1) >= deff : ((n - 1) < 2 * deff || n > 64)) ? A.refine : 0;
       if (m > 0 && m <= (L.mcap < 32 ? L.mcap : 32)) {
-        const FastView fv{X, ldx, trs, n, col, xb, sv, deff};
-        ok = dual ? fit_fast<true>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane, L.mcap)
-                  : fit_fast<false>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane, L.mcap);
+        const FastView fv{X, ldx, trs, n, col, xb, sv, deff, xs32};
+        ok = dual ? fit_fast<true, STAGED>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane, L.mcap)
+                  : fit_fast<false, STAGED>(fv, yc, A.lambda, nref, Msm, v2, uv, wv, lane, L.mcap);
       } else if (m > 0) {
         const FitView fv{X, ldx, trs, n, col, xb, sv, deff};
         ok = fit_generic(fv, yc, A.lambda, nref, dual, scr, L.vmax, uv, v2, wv, lane);

@@ -35,81 +35,84 @@ struct FastView {
   const double* xb;
   const double* s;
   int deff;
+  unsigned xs32;     // staged rates: 32-bit shared-window address of X (SX instantiations)
 };
 
+// Rate at byte offset `off` of X: a 32-bit ld.shared when the rates are staged
+// (SX), else a generic load.  The staged rates are read-only after the
+// kernel's staging barrier, so the asm needs no memory clobber.
+template <bool SX>
+__device__ __forceinline__ double xload(const double* X, unsigned xs32, int off) {
+  if (SX) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(xs32 + (unsigned)off));
+    return v;
+  }
+  return *reinterpret_cast<const double*>(reinterpret_cast<const char*>(X) + off);
+}
+template <bool SX>
+__device__ __forceinline__ double xat(const FastView& f, int off) { return xload<SX>(f.X, f.xs32, off); }
+
 // Lower triangle (rb2 row layout) of Z Z^T + lambda I; Z = Xtilde (dual) or
-// Xtilde^T (primal).  One code copy for every m <= 32: up to 4 block-rows,
-// tiles beyond nb = ceil(m/8) skipped by warp-uniform branches (code size
-// matters more than the template specialisation: instruction cache).
-template <bool DUAL>
+// Xtilde^T (primal), NB = ceil(m/8) row-blocks (one compact k-loop per NB,
+// chosen outside the loop: no warp-uniform branches or address rebuilds inside).
+// Fragments: lane (rl, kl) forms Z[I*8 + rl][k0 + kl] = (x - xbar) * s.
+template <bool DUAL, bool SX, int NB>
+__device__ __forceinline__ void gram_acc(const FastView& f, double (&acc)[10][2], int lane) {
+  const int rl = lane >> 2, kl = lane & 3;
+  const int ldx8 = f.ldx * 8;
+  int ro[NB];                        // DUAL: byte offset of row I*8+rl
+  int co[NB];                        // primal: byte offset of column (feature) I*8+rl
+  double xba[NB], sa[NB];
+#pragma unroll
+  for (int I = 0; I < NB; ++I) {
+    const int r = I * 8 + rl;
+    if (DUAL) {
+      // rows >= n only reach Gram rows/columns >= m, never stored or read
+      ro[I] = f.trs[r < f.n ? r : 0] * ldx8;
+    } else {
+      co[I] = f.col[r] * 8;
+      xba[I] = f.xb[r];
+      sa[I] = f.s[r];
+    }
+  }
+  const int kend = DUAL ? f.deff : f.n;
+  #pragma unroll 1
+  for (int k0 = 0; k0 < kend; k0 += 4) {
+    double fr[NB];
+    if (DUAL) {
+      const int ka = k0 + kl;
+      const int c8 = f.col[ka] * 8;
+      const double xbv = f.xb[ka], sv = f.s[ka];
+#pragma unroll
+      for (int I = 0; I < NB; ++I) fr[I] = (xat<SX>(f, ro[I] + c8) - xbv) * sv;
+    } else {
+      const int ri = k0 + kl;
+      const bool live = ri < f.n;
+      const int sr = f.trs[live ? ri : 0] * ldx8;
+#pragma unroll
+      for (int I = 0; I < NB; ++I) fr[I] = live ? (xat<SX>(f, sr + co[I]) - xba[I]) * sa[I] : 0.0;
+    }
+    int t = 0;
+#pragma unroll
+    for (int I = 0; I < NB; ++I)
+#pragma unroll
+      for (int J = 0; J <= I; ++J, ++t) dmma(acc[t][0], acc[t][1], fr[I], fr[J]);
+  }
+}
+
+template <bool DUAL, bool SX>
 __device__ SR_FAST_FN void gram_fast(const FastView& f, int m, double lambda, double* Mpk, int lane) {
   constexpr int NB = 4, NT = 10;
   const int nb = (m + 7) >> 3;
   double acc[NT][2];
 #pragma unroll
   for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  if (nb == 1) gram_acc<DUAL, SX, 1>(f, acc, lane);
+  else if (nb == 2) gram_acc<DUAL, SX, 2>(f, acc, lane);
+  else if (nb == 3) gram_acc<DUAL, SX, 3>(f, acc, lane);
+  else gram_acc<DUAL, SX, 4>(f, acc, lane);
   const int rl = lane >> 2, kl = lane & 3;
-  int so[NB];
-  int ca[NB];
-  double xba[NB], sa[NB];
-  if (DUAL) {
-    // rows >= n only reach Gram rows/columns >= m, which are never stored or
-    // read: point them at row 0 instead of masking every fragment element
-#pragma unroll
-    for (int I = 0; I < NB; ++I) {
-      const int r = I * 8 + rl;
-      so[I] = f.trs[r < f.n ? r : 0] * f.ldx;
-    }
-  } else {
-#pragma unroll
-    for (int I = 0; I < NB; ++I) {
-      const int a = I * 8 + rl;
-      ca[I] = f.col[a];
-      xba[I] = f.xb[a];
-      sa[I] = f.s[a];
-    }
-  }
-  const int kend = DUAL ? f.deff : f.n;
-  SR_UNROLL(SR_UNROLL_GRAM)
-  for (int k0 = 0; k0 < kend; k0 += 4) {
-    // fragments of block-rows >= nb are never formed (warp-uniform branches)
-    double fr[NB];
-    int c = 0, sr = -1;
-    double xbv = 0.0, sv = 0.0;
-    if (DUAL) {
-      const int ka = k0 + kl;
-      c = f.col[ka];
-      xbv = f.xb[ka];
-      sv = f.s[ka];
-    } else {
-      const int ri = k0 + kl;
-      sr = ri < f.n ? f.trs[ri] * f.ldx : -1;
-    }
-    auto frag = [&](int I) -> double {
-      if (DUAL) return (f.X[so[I] + c] - xbv) * sv;
-      return sr >= 0 ? (f.X[sr + ca[I]] - xba[I]) * sa[I] : 0.0;
-    };
-    fr[0] = frag(0);
-    dmma(acc[0][0], acc[0][1], fr[0], fr[0]);
-    if (nb > 1) {
-      fr[1] = frag(1);
-      dmma(acc[1][0], acc[1][1], fr[1], fr[0]);
-      dmma(acc[2][0], acc[2][1], fr[1], fr[1]);
-      if (nb > 2) {
-        fr[2] = frag(2);
-        dmma(acc[3][0], acc[3][1], fr[2], fr[0]);
-        dmma(acc[4][0], acc[4][1], fr[2], fr[1]);
-        dmma(acc[5][0], acc[5][1], fr[2], fr[2]);
-        if (nb > 3) {
-          fr[3] = frag(3);
-          dmma(acc[6][0], acc[6][1], fr[3], fr[0]);
-          dmma(acc[7][0], acc[7][1], fr[3], fr[1]);
-          dmma(acc[8][0], acc[8][1], fr[3], fr[2]);
-          dmma(acc[9][0], acc[9][1], fr[3], fr[3]);
-        }
-      }
-    }
-  }
   int t = 0;
 #pragma unroll
   for (int I = 0; I < NB; ++I) {
@@ -249,21 +252,23 @@ __device__ SR_FAST_FN double solve_ll(const double* M, int m, int lane, double m
 
 // w'_a = s_a * sum_i (x_ia - xb_a) * alpha_i, alpha lane-owned (n <= 32);
 // lanes over features, written to wout[0..deff).
+template <bool SX>
 __device__ SR_FAST_FN void xt_alpha_lanes(const FastView& f, double alpha, double* wout, int lane,
                                            double* abuf) {
   if (lane < f.n) abuf[lane] = alpha;   // broadcast through shared memory (1 LDS per row, no shuffles)
   __syncwarp();
+  const int ldx8 = f.ldx * 8;
   for (int a0 = 0; a0 < f.deff; a0 += 64) {
     const int a1 = a0 + lane, a2 = a0 + 32 + lane;
-    const int c1 = f.col[a1 < f.deff ? a1 : 0], c2 = f.col[a2 < f.deff ? a2 : 0];
+    const int o1 = f.col[a1 < f.deff ? a1 : 0] * 8, o2 = f.col[a2 < f.deff ? a2 : 0] * 8;
     const double x1 = f.xb[a1 < f.deff ? a1 : 0], x2 = f.xb[a2 < f.deff ? a2 : 0];
     double acc1 = 0.0, acc2 = 0.0;
     SR_UNROLL(SR_UNROLL_XTA)
     for (int i = 0; i < f.n; ++i) {
       const double ai = abuf[i];
-      const double* xr = f.X + f.trs[i] * f.ldx;
-      acc1 = fma(xr[c1] - x1, ai, acc1);
-      acc2 = fma(xr[c2] - x2, ai, acc2);
+      const int ro = f.trs[i] * ldx8;
+      acc1 = fma(xat<SX>(f, ro + o1) - x1, ai, acc1);
+      acc2 = fma(xat<SX>(f, ro + o2) - x2, ai, acc2);
     }
     if (a1 < f.deff) wout[a1] = acc1 * f.s[a1];
     if (a2 < f.deff) wout[a2] = acc2 * f.s[a2];
@@ -282,11 +287,11 @@ __device__ __forceinline__ double xrow_dot(const FastView& f, const double* xr, 
 // Output: w' (weights on the scaled features) in wout[0..deff).
 // scratch: [n] doubles for the primal residual; uwork: [deff].
 // mcap: rows the factor buffer holds (the dual fuses the forward solve as row m when m < mcap).
-template <bool DUAL>
+template <bool DUAL, bool SX>
 __device__ SR_FAST_FN bool fit_fast(const FastView& f, const double* yc, double lambda, int refine, double* Mpk,
                          double* scratch, double* uwork, double* wout, int lane, int mcap) {
   const int m = DUAL ? f.n : f.deff;
-  gram_fast<DUAL>(f, m, lambda, Mpk, lane);
+  gram_fast<DUAL, SX>(f, m, lambda, Mpk, lane);
   double myinv;
 #if SPEEDREC_CHOL_RL
   const bool aug = false;
@@ -302,7 +307,7 @@ __device__ SR_FAST_FN bool fit_fast(const FastView& f, const double* yc, double 
     double alpha = lane < f.n ? (aug ? Mpk[rb2(m) + lane] : yc[lane]) : 0.0;
     alpha = aug ? solve_bwd(Mpk, m, lane, myinv, alpha) : solve_ll(Mpk, m, lane, myinv, alpha);
     for (int it = 0; it < refine; ++it) {
-      xt_alpha_lanes(f, alpha, wout, lane, scratch);
+      xt_alpha_lanes<SX>(f, alpha, wout, lane, scratch);
       for (int a = lane; a < f.deff; a += 32) uwork[a] = wout[a] * f.s[a];
       __syncwarp();
       double e = 0.0;
@@ -310,7 +315,7 @@ __device__ SR_FAST_FN bool fit_fast(const FastView& f, const double* yc, double 
       alpha += solve_ll(Mpk, m, lane, myinv, e);
       __syncwarp();
     }
-    xt_alpha_lanes(f, alpha, wout, lane, scratch);
+    xt_alpha_lanes<SX>(f, alpha, wout, lane, scratch);
   } else {
     // rhs_a = s_a * sum_i (x_ia - xb_a) * yc_i, lane a < deff <= 32
     double w = 0.0;

@@ -250,6 +250,10 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 #define SR_UNROLL_XTA 2
 #endif
 
+// min / max of non-NaN doubles: one compare + select (fmin/fmax add NaN handling)
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
+
 __device__ __forceinline__ bool near_tol(double a, double b, double tol) {
   double s = fabs(a) > 1.0 ? fabs(a) : 1.0;
   return fabs(a - b) <= tol * s;
