@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     if (n > 0 && lane == 0 && MODE != 4) atomicOr(&A.trained[sl], 1u << o);
     auto put_counts = [&](double flag) {   // MODE 4: the model-table row's fields after u, c0
       if (lane == 0) {
-        double* e = urow + A.C;
+        double* e = urow + ((A.C + 3) & ~3);   // fields after the k-step-padded weights
         e[kUflag] = flag;
         e[kUntr] = (double)n;
         e[kUnte] = (double)nt;
@@ -552,8 +552,9 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
         if (lane == 0) cf[0] = c0;
       }
       if (MODE == 4) {   // the model for k_pred_rank (A5-A7 there)
-        for (int c = lane; c < C; c += 32) urow[c] = ufull[c];
-        if (lane == 0) urow[C + kUc0] = c0;
+        const int Cp = (C + 3) & ~3;       // weights padded with zeros to whole DMMA k-steps
+        for (int c = lane; c < Cp; c += 32) urow[c] = c < C ? ufull[c] : 0.0;
+        if (lane == 0) urow[Cp + kUc0] = c0;
         put_counts(ok ? 1.0 : 2.0);
         continue;
       }

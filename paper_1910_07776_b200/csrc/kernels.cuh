@@ -128,8 +128,9 @@ struct EvalArgs {
   double* gscratch;      // per global warp: mscratch doubles (large systems: factor + 2 vectors)
   long long mscratch;
   // model table of the split LS path (k_fit_warp MODE 4 -> k_pred_rank):
-  // [count][n_os][ldu]: u[0..C) raw-counter weights, then c0, flag, n_train,
-  // n_test, fp_train bits, fp_test bits (flag 0 untrained, 1 fitted, 2 non-positive pivot)
+  // [count][n_os][ldu]: u[0..Cp) raw-counter weights (Cp = C rounded up to 4,
+  // zero padded), then c0, flag, n_train, n_test, fp_train bits, fp_test bits
+  // (flag 0 untrained, 1 fitted, 2 non-positive pivot)
   double* utab;
   int ldu;
   int n_os;              // scored-optimization slots per scenario (table rows)
@@ -277,6 +278,40 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+
+// 1-D bulk copy global -> shared (TMA engine) completing on an mbarrier, and
+// the mbarrier operations it needs (CTA scope; no cluster launch).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes, uint64_t* bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}" ::"r"(b), "r"(phase)
+      : "memory");
+}
+// 1/x for x > 0 finite: MUFU.RCP64H estimate + two Newton steps (<= 2 ulp).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
 }
 
 // ---------------------------------------------------------------- A0 / A1

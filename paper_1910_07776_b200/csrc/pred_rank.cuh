@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = A.G, O = A.O, C = A.C, N = G * 64;
   const int ldx = PL.ldxp, ldut = PL.ldut, wpb = PL.warps;
+  const int Cp = (C + 3) & ~3, ks = Cp >> 2;       // k-steps; model fields start at Cp
   int8_t* obit = reinterpret_cast<int8_t*>(smem);
   double* xs = reinterpret_cast<double*>(smem + PL.off_x);
   double* ys = reinterpret_cast<double*>(smem + PL.off_y);
@@ -80,27 +81,32 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
   unsigned char* slab = smem + PL.off_w + warp * PL.wbytes;
   double* ubuf = reinterpret_cast<double*>(slab);                                    // [2][CMAX][ldut] model rows
   double* ext = ubuf + 2 * CMAX * ldut;                                              // [kPrChunk][CMAX + 1]
-  int* ols = reinterpret_cast<int*>(ext + kPrChunk * (CMAX + 1));                   // [8] scored ids (-1 pad)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ext + kPrChunk * (CMAX + 1));        // [2] bulk-copy barriers
+  int* ols = reinterpret_cast<int*>(bars + 2);                                       // [8] scored ids (-1 pad)
   int16_t* slots = reinterpret_cast<int16_t*>(ols + 8);                              // [N]
   const int rl = lane >> 2, kl = lane & 3;
-  const int ks = (C + 3) >> 2;                       // k-steps (C <= kPrMaxC)
   const long long gwarp = (long long)blockIdx.x * wpb + warp;
   const long long nwarps = (long long)gridDim.x * wpb;
   unsigned long long tot_corr = 0, tot_test = 0, tot_rec = 0, tot_hit = 0;
   const unsigned lt = (1u << lane) - 1u;
-  // model rows of scenario sl -> buffer b: cp.async, 16 B per copy (ldu is even)
-  const int n_tab = A.n_os < CMAX ? A.n_os : CMAX;
+  // model rows of scenario sl -> buffer b: ONE bulk copy (TMA engine) of the
+  // scenario's n_os contiguous rows (table stride ldu == ldut), completing on
+  // the buffer's mbarrier
+  const unsigned row_bytes = (unsigned)(A.n_os * A.ldu * 8);
   auto prefetch = [&](long long sl, int b) {
-    if (sl < A.count) {
-      const double* src = A.utab + sl * (long long)A.n_os * A.ldu;
-      double* dst = ubuf + b * CMAX * ldut;
-      for (int q = 0; q < n_tab; ++q)
-        for (int c2 = 2 * lane; c2 < A.ldu; c2 += 64) cp_async16(dst + q * ldut + c2, src + q * A.ldu + c2);
+    if (lane == 0 && sl < A.count) {
+      fence_proxy_async();               // this warp's earlier reads of the buffer precede the async write
+      bulk_g2s(ubuf + b * CMAX * ldut, A.utab + sl * (long long)A.n_os * A.ldu, row_bytes, bars + b);
     }
-    cp_commit();
   };
+  if (lane == 0) {
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+    fence_mbar_init();
+  }
   __syncthreads();
   int buf = 0;
+  unsigned phase = 0u;                   // bit b: parity of buffer b's next completion
   prefetch(gwarp, 0);
 
   for (long long sl = gwarp; sl < A.count; sl += nwarps, buf ^= 1) {
@@ -118,7 +124,8 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
       }
       ols[lane] = o;
     }
-    cp_wait<1>();                                    // this scenario's rows (all but the newest group)
+    mbar_wait(bars + buf, (phase >> buf) & 1u);      // this scenario's rows have landed
+    phase ^= 1u << buf;
     __syncwarp();
     const double* ut = ubuf + buf * CMAX * ldut;     // row q: u[0..C), then c0, flag, counts (kU*)
     // the scenario's test versions (slot ids), in slot order
@@ -156,9 +163,8 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
         const double* xr = xs + (row < ns ? slots[row] : 0) * ldx + kl;
         const double* br = (rl < n_os ? ut + rl * ldut : zrow) + kl;
         double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-        for (int k = 0; k < kPrMaxC / 4; ++k)
-          if (k < ks) dmma(d0, d1, xr[4 * k], br[4 * k]);
+#pragma unroll 4
+        for (int k = 0; k < ks; ++k) dmma(d0, d1, xr[4 * k], br[4 * k]);
         double* er = ext + (rb * 8 + rl) * (CMAX + 1) + 2 * kl;
         if (2 * kl < CMAX) er[0] = d0;
         if (2 * kl + 1 < CMAX) er[1] = d1;
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
           const int o = ols[q];
           const int b = o >= 0 ? obit[p * O + o] : -1;
           bool cand = o >= 0 && b >= 0 && !((v >> b) & 1);
-          if (cand && ut[q * ldut + C + kUflag] == 0.0) {   // untrained (R18): counted, never a candidate
+          if (cand && ut[q * ldut + Cp + kUflag] == 0.0) {   // untrained (R18): counted, never a candidate
             ++untrained;
             cand = false;
           }
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
           if (cand) {
             cvm |= 1u << q;
             const int k = rmv(v, b);
-            double e = ut[q * ldut + C + kUc0] + er[q];
+            double e = ut[q * ldut + Cp + kUc0] + er[q];
             if (near_tol(e, 0.0, A.guard_tol) || near_tol(e, 1.0, A.guard_tol)) ++guard;
             if (e <= 0.0) {
               e = A.clamp_floor;
@@ -193,7 +199,7 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
             }
             const double ac = ys[(g * O + o) * 32 + k];
             pc[q] += ((e > 1.0 && ac > 1.0) || (e <= 1.0 && ac <= 1.0)) ? 1 : 0;
-            const double ratio = ac / e;
+            const double ratio = ac * rcp_nr(e);   // AC/EX within 2 ulp (bar: 1e-9)
             ps[q] += ratio;
             pmn[q] = fmin(pmn[q], ratio);
             pmx[q] = fmax(pmx[q], ratio);
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
     {
       const int q = (lane >> 2) & 7;
       if ((lane & 3) == 0 && q < n_os) {
-        const double* e = ut + q * ldut + C;
+        const double* e = ut + q * ldut + Cp;
         OptScore row;
         row.n_train = (int)e[kUntr];
         row.n_test = (int)e[kUnte];
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
         }
       }
       // a non-positive pivot poisons the scenario (guard count, as the EX-table path)
-      gsum += 1000000 * __popc(__ballot_sync(FULL, (lane & 3) == 0 && q < n_os && ut[q * ldut + C + kUflag] == 2.0));
+      gsum += 1000000 * __popc(__ballot_sync(FULL, (lane & 3) == 0 && q < n_os && ut[q * ldut + Cp + kUflag] == 2.0));
     }
     if (lane == 0) {
       if (A.opt_out) {
@@ -299,7 +305,6 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
     tot_hit += nh;
     __syncwarp();            // every lane is done with buffer `buf` before the next prefetch reuses it
   }
-  cp_wait<0>();
   tot_corr = warp_usum(tot_corr);      // accumulated by the row-writing lanes
   tot_test = warp_usum(tot_test);
   if (A.totals && lane == 0 && (tot_test | tot_rec | tot_hit)) {

@@ -1114,15 +1114,14 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     int ld = ((C + 3) / 4) * 4;
     while (ld % 16 != 4) ld += 4;
     const int cm = c->n_os <= 6 ? 6 : 8;
-    const int ldu_ = ((C + kUextra + 1) / 2) * 2;
-    int ldut = ldu_;
+    int ldut = ((C + 3) & ~3) + kUextra;             // weights padded to whole k-steps, then the fields
     while (ldut % 16 != 4) ldut += 2;
     PL.ldxp = ld;
     PL.ldut = ldut;
     PL.off_x = align16(c->P * O);
     PL.off_y = PL.off_x + align16((int)(N * ld * 8));
     PL.off_w = PL.off_y + align16((G * O * 32 + ldut) * 8);
-    PL.wbytes = align16(2 * cm * ldut * 8 + kPrChunk * (cm + 1) * 8 + 8 * 4 + (int)N * 2);
+    PL.wbytes = align16(2 * cm * ldut * 8 + kPrChunk * (cm + 1) * 8 + 16 + 8 * 4 + (int)N * 2);
     PL.warps = std::min(kPrWarps, (budget - PL.off_w) / PL.wbytes);
     PL.bytes = PL.off_w + PL.warps * PL.wbytes;
     if (PL.warps < 4) split_ls = false;
@@ -1143,7 +1142,9 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   const int ex_stride = c->n_os * tg_stride;
   long long chunk_bytes = 1024LL << 20;                 // EX table per launch (SPEEDREC_CHUNK_MB overrides; tools/sweep_c3.sh)
   if (const char* e = getenv("SPEEDREC_CHUNK_MB")) chunk_bytes = std::max(1LL, atoll(e)) << 20;
-  const int ldu = ((C + kUextra + 1) / 2) * 2;        // model-table row (split LS path)
+  // model-table row (split LS path): k_pred_rank's shared-memory row stride,
+  // so one bulk copy moves a scenario's rows
+  const int ldu = split_ls ? PL.ldut : ((C + kUextra + 1) / 2) * 2;
   const long long row_bytes = split_ls ? 8LL * c->n_os * ldu : 8LL * ex_stride;
   const long long chunk = std::max(1LL, std::min<long long>(count, chunk_bytes / row_bytes));
   if (split_ls) {
