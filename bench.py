@@ -108,15 +108,64 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def oracle_rate(cfg, first: int, count: int, threads: int, learner: int = 0):
+def oracle_rate(cfg, first: int, count: int, threads: int, learner: int = 0, stats: dict | None = None):
+    """Scenarios/s of the oracle as it stands on `threads` host threads over
+    scenarios [first, first+count).  stats (LS learner): filled with the
+    sample's kappa^ statistics and the long-double share."""
     import oracle
     t0 = time.perf_counter()
     if learner == 2:    # M5P: the exact-rational Python oracle (oracle/m5.py), one core
         from oracle import m5
         m5.evaluate(cfg.dataset, cfg.scenarios, first, count)
     else:
-        oracle.evaluate(cfg.dataset, cfg.scenarios, first, count, n_threads=threads, learner=learner)
+        r = oracle.evaluate(cfg.dataset, cfg.scenarios, first, count, n_threads=threads, learner=learner,
+                            want_kappa=stats is not None and learner == 0)
+        if stats is not None and r["kappa"] is not None:
+            k = r["kappa"][np.isfinite(r["kappa"])]
+            if k.size:
+                stats.update(kappa_min=float(k.min()), kappa_median=float(np.median(k)), kappa_max=float(k.max()),
+                             fits=int(k.size), long_double_fits=int(r["fit_ld"].sum()),
+                             guard_cases=int(r["scn"]["n_guard"].sum()))
     return count / (time.perf_counter() - t0)
+
+
+def ibk_fit_rate(cfg, threads: int) -> float:
+    """C4 under IBK: one scenario is 6 fits of n*t*d ~ 1.7e10 distance terms
+    each (minutes of oracle time), so the bounded sample is ONE fit (split 0,
+    optimization O0) on one core; scenarios/s = 1 / (6 x its time)."""
+    import copy
+    import oracle
+    sc = copy.copy(cfg.scenarios)
+    sc.opt_mask = 1
+    t0 = time.perf_counter()
+    oracle.evaluate(cfg.dataset, sc, 0, 1, n_threads=1, learner=1)
+    return 1.0 / (6.0 * (time.perf_counter() - t0))
+
+
+# Context (P:216-224, Table 3): the paper's sign accuracies, measured on a
+# Tesla K20c (0.7 GHz Kepler, 13 SMX) with nvprof 6.5 profiles of BH/NB and
+# Weka's IBK / M5P.  Different data and hardware: context, not a target.
+PAPER_TABLE3 = {
+    "source": "PAPER.md Table 3 (P:216-224)",
+    "profiled_on": "Tesla K20c (Kepler, 0.7 GHz, 13 SMX), nvcc 6.0.1 -O3 -arch=sm_35, nvprof 6.5, Weka",
+    "ibk_pct": {"1": 97.3, "2": 96.0, "3": 96.3, "4": 92.0, "5": 83.6, "6": 55.7},
+    "m5p_pct": {"1": 86.4, "2": 86.4, "3": 33.3, "4": 81.6, "5": 33.3, "6": 60.1},
+    "note": "context only: the paper's K20c data; this run is synthetic data (DESIGN.md 8)",
+}
+
+
+def per_experiment_accuracy(cfg, opt_rows) -> dict | None:
+    """Pooled sign accuracy per Table-2 experiment of this run (C2 / BH6)."""
+    exp = getattr(cfg.scenarios, "experiment", None)
+    if exp is None:
+        return None
+    out = {}
+    for e in sorted(set(int(x) for x in exp)):
+        sel = exp[:len(opt_rows)] == e
+        t = int(opt_rows["n_test"][sel].astype(np.int64).sum())
+        c = int(opt_rows["n_correct"][sel].astype(np.int64).sum())
+        out[str(e)] = round(100.0 * c / t, 2) if t else None
+    return out
 
 
 def oracle_cores(threads: int, learner: int) -> int:
@@ -209,9 +258,11 @@ def m5_flops(n: np.ndarray, t: np.ndarray, d: int) -> float:
 
 
 OTHER_CONFIGS = [("C1", "C1", ["--cpu-sample", "64"]), ("C2", "C2", ["--cpu-sample", "240"]),
-                 ("C4", "C4", ["--splits", "592", "--no-cpu-baseline"]),
+                 ("C2-ibk", "C2", ["--learner", "ibk", "--cpu-sample", "240"]),
+                 ("C2-m5", "C2", ["--learner", "m5", "--cpu-sample", "24"]),
+                 ("C4", "C4", ["--splits", "592", "--cpu-sample", "32"]),
                  ("C5", "C5", ["--masks-k", "20", "--cpu-sample", "2048"]),
-                 ("C4-ibk", "C4", ["--splits", "16", "--learner", "ibk", "--no-cpu-baseline"]),
+                 ("C4-ibk", "C4", ["--splits", "16", "--learner", "ibk"]),
                  ("C3-m5", "C3", ["--splits", "65536", "--learner", "m5", "--cpu-sample", "32"])]
 
 
@@ -231,6 +282,7 @@ def run_other_configs(args):
                          "workload": d["config"]["workload"], "scenarios_per_step": d["config"]["splits_per_gpu"],
                          "scaling": d["scaling"], "roofline": {k: r[k] for k in ("kernel", "achieved", "frac")},
                          "cpu_baseline": d.get("cpu_baseline"), "accuracy": d.get("accuracy"),
+                         "guard_cases": d.get("guard_cases"),
                          "top_masks_head": d.get("top_masks_head")}
         except Exception as e:   # reported, never fatal for the headline line
             res[name] = {"error": f"{type(e).__name__}: {e}"[:200]}
@@ -394,6 +446,7 @@ def main():
 
     # ---------------- roofline of the dominant kernel (FP64 ALU/DMMA bound)
     big = ds.n_groups > 64          # CTA-per-fit path (C4): prediction runs in k_rank_big
+    flops_pd = None
     name_dom = ("k_ibk_dist" if args.learner == "ibk" else "k_fit_big") if big else "k_fit_warp"
     if c5:
         # n, t per (fold, opt) do not depend on the mask: take them from one
@@ -408,7 +461,9 @@ def main():
             # arithmetic than this yardstick, so its fraction is an effective one
             name_dom = "k_mask_sfit" if stats.get("k_mask_sfit", (0, 0.0))[0] > 0 else "k_mask_fit"
             n_fit = float(np.sum((n_tr > 0) & (n_te > 0)))
-            ff = lambda d: n_fit * 2.0 * (d ** 3 / 6 + d ** 2 + d)
+            # SURVEY 8(d)'s yardstick: p = |S| + 1 (mask features + intercept)
+            ff = lambda d: n_fit * 2.0 * ((d + 1) ** 3 / 6 + (d + 1) ** 2 + (d + 1))
+            ff_pd = lambda d: n_fit * 2.0 * (d ** 3 / 6 + d ** 2 + d)   # round-1's conservative p = |S|
         elif args.learner == "ibk":
             ff = lambda d: knn_flops(n_tr, n_te, d)
         elif args.learner == "m5":
@@ -416,6 +471,8 @@ def main():
         else:
             ff = lambda d: fit_flops(n_tr, n_te, d, refine=2)
         flops_launch = sum(float(np.sum(pcs == d)) * ff(int(d)) for d in np.unique(pcs))
+        if name_dom in ("k_mask_sfit", "k_mask_fit"):
+            flops_pd = sum(float(np.sum(pcs == d)) * ff_pd(int(d)) for d in np.unique(pcs))
     else:
         opt = out["opt"].cpu().numpy().view(OPT_SCORE_DTYPE).reshape(count, O)
         n_tr, n_te = opt["n_train"].ravel(), opt["n_test"].ravel()
@@ -496,19 +553,36 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        v = oracle_rate(cfg, 0, args.cpu_sample, threads, LEARNERS[args.learner])
-        cpu = {"value": v, "unit": "scenario_evals/s", "cores": oracle_cores(threads, LEARNERS[args.learner]),
-               "kind": "oracle",
-               "sample": f"first {args.cpu_sample} scenarios of {args.config} (same splits the GPU evaluates)"}
+        L = LEARNERS[args.learner]
+        if big and L == 1:
+            v = v1 = ibk_fit_rate(cfg, threads)
+            cores, st = 1, {}
+            sample = "1 of the 6 fits of split 0 (optimization O0) on one core, scenarios/s = 1/(6 t)"
+        else:
+            st = {}
+            v = oracle_rate(cfg, 0, args.cpu_sample, threads, L, stats=st)
+            cores = oracle_cores(threads, L)
+            n1 = max(1, args.cpu_sample // threads)       # single-core rate on ~1/threads of the sample
+            v1 = oracle_rate(cfg, 0, n1, 1, L) if cores > 1 else v
+            sample = f"first {args.cpu_sample} scenarios of {args.config} (same splits the GPU evaluates)"
+        cpu = {"value": v, "unit": "scenario_evals/s", "cores": cores, "kind": "oracle", "sample": sample,
+               "nproc": threads, "single_core_value": v1,
+               "precision": "quad; long double for p > 65 overdetermined fits (SURVEY 8(c))" if L == 0 else
+               ("exact IEEE (bit-exact definition)" if L == 1 else "FP64 + exact rationals (Python)"),
+               "kappa": st or None}
 
     # rank 0: the gathered tables in global scenario (C5: mask) order
-    gathered, pooled = None, None
+    gathered, pooled, guard_cases, per_exp = None, None, None, None
     if rank == 0:
         if c5:
             gathered = {"masks": D.scatter_mask_rows(tables["masks"].cpu().numpy(), all_masks, 1 << args.masks_k)}
         else:
             gathered = {k: v.cpu().numpy() for k, v in tables.items()}
             pooled = D.pooled_ratio(gathered["opt"])
+            from paper_1910_07776_b200.speedrec import OPT_SCORE_DTYPE as _OD, SCN_SCORE_DTYPE as _SD
+            g_opt = gathered["opt"].view(_OD).reshape(-1, O)
+            guard_cases = int(gathered["scn"].view(_SD)["n_guard"].astype(np.int64).sum())
+            per_exp = per_experiment_accuracy(cfg, g_opt)
     top_global = None
     if c5:   # C5 A7: local top-64 (library) -> global mask ids -> exact merge over ranks
         from paper_1910_07776_b200.speedrec import MASK_SCORE_DTYPE
@@ -530,8 +604,10 @@ def main():
                          "peak_note": f"FP64 (DFMA/DMMA shared pipe): {props.multi_processor_count} SMs x "
                                       f"{FP64_FMA_PER_CLK_PER_SM} FMA/clk x 2 x {sm_max:.0f} MHz",
                          "effective": name_dom == "k_mask_sfit",
+                         "frac_yardstick_p_eq_S": (flops_pd / (ms_dom / max(args.steps, 1) / 1e3) / 1e12 / peak
+                                                   if flops_pd and ms_dom > 0 else None),
                          "flops_note": ("SURVEY 8(d) C5 yardstick p^3/6+p^2+p per fit on the precomputed "
-                                        "Gram; the prefix-shared path (DESIGN 5.8) executes fewer flops, "
+                                        "Gram with p = |S|+1; the prefix-shared path (DESIGN 5.8) executes fewer flops, "
                                         "so frac is an effective fraction" if name_dom == "k_mask_sfit"
                                         else "M5P yardstick: the root split search only, 4 d (n-1) n flop "
                                         "per fit (DESIGN 6)" if args.learner == "m5"
@@ -541,10 +617,12 @@ def main():
                        "backend": backend if world > 1 else None, "ms_per_step": gather_ms,
                        "bytes_per_rank": int(sum(v.numel() for v in tables.values()) // world) if world > 1 else 0,
                        "in_step": True},
-            "pooled_ratio": pooled,
+            "pooled_ratio": pooled, "guard_cases": guard_cases,
+            "paper_context": PAPER_TABLE3,
             "clocks": clk_sum,
             "accuracy": {"pooled_sign_accuracy_pct": 100.0 * tt[0] / max(tt[1], 1), "cases": int(tt[1]),
-                         "recommendations": int(tt[2]), "rec_hits": int(tt[3])},
+                         "recommendations": int(tt[2]), "rec_hits": int(tt[3]),
+                         "per_experiment_pct": per_exp, "learner": args.learner, "data": "synthetic"},
             "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in stats.items()},
         }
         if c5:

@@ -478,7 +478,9 @@ sr_status sr_define_scenarios(sr_ctx* c, const sr_scenarios* s, int64_t* n_scena
 namespace {
 
 // Shared-memory plan of k_eval_warp for the current batch.
-WarpLayout plan_layout(const sr_ctx* c, int mcap, bool ibk) {
+// lean (k_fit_warp MODE 4): no test lists (prediction is k_pred_rank's) and the
+// raw-counter weights alias the factor buffer (free once the fit is solved).
+WarpLayout plan_layout(const sr_ctx* c, int mcap, bool ibk, bool lean = false) {
   WarpLayout L{};
   int off = 0;
   auto take = [&](int bytes) {
@@ -495,8 +497,8 @@ WarpLayout plan_layout(const sr_ctx* c, int mcap, bool ibk) {
   L.np_te = c->np_te;
   L.off_trs = take(4 * c->np_tr);
   L.off_yc = take(8 * c->np_tr);
-  L.off_tes = take(4 * c->np_te);
-  L.off_tek = take(4 * c->np_te);
+  L.off_tes = lean ? 0 : take(4 * c->np_te);
+  L.off_tek = lean ? 0 : take(4 * c->np_te);
   L.off_col = take(2 * dpad);
   L.off_xb = take(8 * dpad);
   L.off_s = take(8 * dpad);
@@ -507,7 +509,7 @@ WarpLayout plan_layout(const sr_ctx* c, int mcap, bool ibk) {
   L.mcap = mcap;
   // Cholesky factor, or for IBK the kKnnRows scaled training rows being scanned
   L.off_M = take(8 * std::max({rb2(mcap), mcap * (mcap + 1) / 2, ibk ? kKnnRows * d : 0}));
-  L.off_ufull = take(8 * c->C);
+  L.off_ufull = lean && rb2(mcap) >= c->C ? L.off_M : take(8 * c->C);
   L.bytes = align16(off);
   return L;
 }
@@ -1053,6 +1055,33 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   }
   if (prm->learner != SR_LINREG || c->coef_req) wmax = 16;   // the one IBK / M5P / sr_fit instantiation
   if (prm->learner == SR_M5P) wmax = SR_M5_WMAX;
+  // split LS path (DESIGN.md §5.12): k_fit_warp<16, 4, true> leaves each fit's
+  // model in a table, k_pred_rank predicts (DMMA), scores and ranks per
+  // scenario -- no EX table, no k_rank_warp.  SPEEDREC_SPLIT_LS=0 (or the
+  // opt-in fused ranking) keeps the EX-table path.
+  bool split_ls = prm->learner == SR_LINREG && !c->coef_req && !c->sweep && !agg && stage && C <= kPrMaxC &&
+                  c->n_os <= 8;
+  if (const char* e = getenv("SPEEDREC_SPLIT_LS")) split_ls = split_ls && atoi(e) != 0;
+  if (const char* e = getenv("SPEEDREC_FUSE_RANK")) split_ls = split_ls && atoi(e) == 0;
+  // k_pred_rank's shared-memory plan: rates staged with a row stride = 4 mod 16
+  // doubles (conflict-free DMMA fragment loads), labels, per-warp EX tiles
+  PredLayout PL{};
+  if (split_ls) {
+    int ld = ((C + 3) / 4) * 4;
+    while (ld % 16 != 4) ld += 4;
+    const int cm = c->n_os <= 6 ? 6 : 8;
+    int ldut = ((C + 3) & ~3) + kUextra;             // weights padded to whole k-steps, then the fields
+    while (ldut % 16 != 4) ldut += 2;
+    PL.ldxp = ld;
+    PL.ldut = ldut;
+    PL.off_x = align16(c->P * O);
+    PL.off_y = PL.off_x + align16((int)(N * ld * 8));
+    PL.off_w = PL.off_y + align16((G * O * 32 + ldut) * 8);
+    PL.wbytes = align16(2 * cm * ldut * 8 + kPrChunk * (cm + 1) * 8 + 16 + 8 * 4 + (int)N * 2);
+    PL.warps = std::min(kPrWarps, (budget - PL.off_w) / PL.wbytes);
+    PL.bytes = PL.off_w + PL.warps * PL.wbytes;
+    if (PL.warps < 4) split_ls = false;
+  }
   int budget_cap = budget;
   if (const char* e = getenv("SPEEDREC_SMEM_KB")) budget_cap = std::min(budget, std::max(16, atoi(e)) * 1024);
   int mcap = std::min(mmax, 32);
@@ -1060,7 +1089,11 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   // A/B knob: a smaller shared-memory factor (rare larger systems go to the
   // global-scratch path) frees shared memory for more warps per SM
   if (const char* e = getenv("SPEEDREC_MCAP")) mcap = std::min(mcap, std::max(8, atoi(e)));
-  WarpLayout L = plan_layout(c, mcap, prm->learner == SR_IBK);
+  // the split LS fit kernel's lean slab: no test lists, weights aliased into
+  // the factor buffer
+  // (20 warps: no faster, the register cap spills -- profiles/r2n_ab_wls.txt)
+  if (split_ls) wmax = 16;
+  WarpLayout L = plan_layout(c, mcap, prm->learner == SR_IBK, split_ls);
   int avail = budget_cap - head - (stage ? align16((int)stage_bytes) : 0);
   int wpb = std::min(wmax, avail / std::max(L.bytes, 1));
   if (wpb < 1 && stage) {
@@ -1099,33 +1132,6 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.off_stage = head;
   A.off_warps = head + (stage ? align16((int)stage_bytes) : 0);
   const int smem = A.off_warps + wpb * L.bytes;
-  // split LS path (DESIGN.md §5.12): k_fit_warp<16, 4, true> leaves each fit's
-  // model in a table, k_pred_rank predicts (DMMA), scores and ranks per
-  // scenario -- no EX table, no k_rank_warp.  SPEEDREC_SPLIT_LS=0 (or the
-  // opt-in fused ranking) keeps the EX-table path.
-  bool split_ls = prm->learner == SR_LINREG && !c->coef_req && !c->sweep && !agg && stage && C <= kPrMaxC &&
-                  c->n_os <= 8 && wmax == 16;
-  if (const char* e = getenv("SPEEDREC_SPLIT_LS")) split_ls = split_ls && atoi(e) != 0;
-  if (const char* e = getenv("SPEEDREC_FUSE_RANK")) split_ls = split_ls && atoi(e) == 0;
-  // k_pred_rank's shared-memory plan: rates staged with a row stride = 4 mod 16
-  // doubles (conflict-free DMMA fragment loads), labels, per-warp EX tiles
-  PredLayout PL{};
-  if (split_ls) {
-    int ld = ((C + 3) / 4) * 4;
-    while (ld % 16 != 4) ld += 4;
-    const int cm = c->n_os <= 6 ? 6 : 8;
-    int ldut = ((C + 3) & ~3) + kUextra;             // weights padded to whole k-steps, then the fields
-    while (ldut % 16 != 4) ldut += 2;
-    PL.ldxp = ld;
-    PL.ldut = ldut;
-    PL.off_x = align16(c->P * O);
-    PL.off_y = PL.off_x + align16((int)(N * ld * 8));
-    PL.off_w = PL.off_y + align16((G * O * 32 + ldut) * 8);
-    PL.wbytes = align16(2 * cm * ldut * 8 + kPrChunk * (cm + 1) * 8 + 16 + 8 * 4 + (int)N * 2);
-    PL.warps = std::min(kPrWarps, (budget - PL.off_w) / PL.wbytes);
-    PL.bytes = PL.off_w + PL.warps * PL.wbytes;
-    if (PL.warps < 4) split_ls = false;
-  }
   auto kfit = split_ls ? k_fit_warp<16, 4, true>
               : prm->learner == SR_IBK ? (stage ? k_fit_warp<16, 1, true> : k_fit_warp<16, 1, false>)
               : prm->learner == SR_M5P ? (stage ? k_fit_warp<SR_M5_WMAX, 3, true> : k_fit_warp<SR_M5_WMAX, 3, false>)
