@@ -62,13 +62,48 @@ __device__ __forceinline__ double scatter_reduce8(double (&v)[8], int lane) {
   return op(r, __shfl_xor_sync(FULL, r, 1));
 }
 
+// Exact guard-band count (reading R21) of one test version, as rank_scenario
+// counts it: EX within tol max(1, |EX|) of 0 or 1 (raw EX), of the threshold
+// (clamped EX), and every candidate pair (clamped EX; two clamped candidates
+// tie by rule).  Called only when the cheap screen fired (essentially never).
 template <int CMAX>
+__device__ __noinline__ int guard_count(const EvalArgs& A, const double* ut, int ldut, int Cp, const int* ols,
+                                        const int8_t* obit, const double* er, int t, int O) {
+  const int g = t >> 6, v = t & 63, p = g / A.IR;
+  const double tol = A.guard_tol;
+  double ce[CMAX];
+  unsigned cvm = 0u, ccm = 0u;
+  int guard = 0;
+  for (int q = 0; q < CMAX; ++q) {
+    const int o = ols[q];
+    const int b = o >= 0 ? obit[p * O + o] : -1;
+    ce[q] = 0.0;
+    if (!(o >= 0 && b >= 0 && !((v >> b) & 1)) || ut[q * ldut + Cp + kUflag] == 0.0) continue;
+    double e = ut[q * ldut + Cp + kUc0] + er[q];
+    if (near_tol(e, 0.0, tol) || near_tol(e, 1.0, tol)) ++guard;
+    if (e <= 0.0) {
+      e = A.clamp_floor;
+      ccm |= 1u << q;
+    }
+    ce[q] = e;
+    cvm |= 1u << q;
+  }
+  for (int q = 0; q < CMAX; ++q) {
+    if (!((cvm >> q) & 1u)) continue;
+    if (near_tol(ce[q], A.threshold, tol)) ++guard;
+    for (int r = q + 1; r < CMAX; ++r)
+      if (((cvm >> r) & 1u) && !((ccm >> q) & (ccm >> r) & 1u) && near_tol(ce[q], ce[r], tol)) ++guard;
+  }
+  return guard;
+}
+
+template <int CMAX, int KS>
 __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A, const PredLayout PL) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = A.G, O = A.O, C = A.C, N = G * 64;
   const int ldx = PL.ldxp, ldut = PL.ldut, wpb = PL.warps;
-  const int Cp = (C + 3) & ~3, ks = Cp >> 2;       // k-steps; model fields start at Cp
+  const int Cp = 4 * KS;                           // k-steps (KS = ceil(C/4)); model fields start at Cp
   int8_t* obit = reinterpret_cast<int8_t*>(smem);
   double* xs = reinterpret_cast<double*>(smem + PL.off_x);
   double* ys = reinterpret_cast<double*>(smem + PL.off_y);
@@ -161,10 +196,10 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
       for (int rb = 0; rb < kPrChunk / 8 && r0 + rb * 8 < ns; ++rb) {
         const int row = r0 + rb * 8 + rl;
         const double* xr = xs + (row < ns ? slots[row] : 0) * ldx + kl;
-        const double* br = (rl < n_os ? ut + rl * ldut : zrow) + kl;
+        const double* br = (rl < n_os ? ut + rl * ldut : zrow) + kl;   // B[k][n] = u of slot n at 4 kstep + k
         double d0 = 0.0, d1 = 0.0;
-#pragma unroll 4
-        for (int k = 0; k < ks; ++k) dmma(d0, d1, xr[4 * k], br[4 * k]);
+#pragma unroll
+        for (int k = 0; k < KS; ++k) dmma(d0, d1, xr[4 * k], br[4 * k]);
         double* er = ext + (rb * 8 + rl) * (CMAX + 1) + 2 * kl;
         if (2 * kl < CMAX) er[0] = d0;
         if (2 * kl + 1 < CMAX) er[1] = d1;
@@ -172,11 +207,13 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
       __syncwarp();
       // ---- clamp, score, rank: lane = test version ----
       const int row = r0 + lane;
+      bool scr = false;                  // a guard-band screen fired on this lane (rare)
       if (row < ns) {
         const int t = slots[row], g = t >> 6, v = t & 63, p = g / A.IR;
         const double* er = ext + lane * (CMAX + 1);
-        double ce[CMAX];
-        unsigned cvm = 0u, ccm = 0u;     // candidate / clamped bit masks
+        double ce[CMAX];                 // EX (clamped)
+        unsigned cvm = 0u;               // candidate bit mask
+        const double tol = A.guard_tol;
 #pragma unroll
         for (int q = 0; q < CMAX; ++q) {
           const int o = ols[q];
@@ -191,31 +228,31 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
             cvm |= 1u << q;
             const int k = rmv(v, b);
             double e = ut[q * ldut + Cp + kUc0] + er[q];
-            if (near_tol(e, 0.0, A.guard_tol) || near_tol(e, 1.0, A.guard_tol)) ++guard;
+            // guard band (R21), screened: tol (1 + |e|) >= tol max(1, |e|), so a
+            // miss is exact; the rule itself runs (warp-uniformly) only on a hit
+            const double te = fma(tol, fabs(e), tol);
+            scr |= fabs(e) <= te || fabs(e - 1.0) <= te;
             if (e <= 0.0) {
               e = A.clamp_floor;
-              ccm |= 1u << q;
               ++pcl[q];
             }
             const double ac = ys[(g * O + o) * 32 + k];
             pc[q] += ((e > 1.0 && ac > 1.0) || (e <= 1.0 && ac <= 1.0)) ? 1 : 0;
             const double ratio = ac * rcp_nr(e);   // AC/EX within 2 ulp (bar: 1e-9)
             ps[q] += ratio;
-            pmn[q] = fmin(pmn[q], ratio);
-            pmx[q] = fmax(pmx[q], ratio);
+            pmn[q] = dmin(pmn[q], ratio);
+            pmx[q] = dmax(pmx[q], ratio);
             ce[q] = e;
             if (A.ex_out) A.ex_out[(so * O + o) * (long long)G * 32 + g * 32 + k] = e;
           }
         }
-        // guard band (reading R21)
 #pragma unroll
         for (int q = 0; q < CMAX; ++q) {
           if (!((cvm >> q) & 1u)) continue;
-          if (near_tol(ce[q], A.threshold, A.guard_tol)) ++guard;
+          const double tq = fma(tol, fabs(ce[q]), tol);
+          scr |= fabs(ce[q] - A.threshold) <= tq;
 #pragma unroll
-          for (int r = q + 1; r < CMAX; ++r)
-            if (((cvm >> r) & 1u) && !((ccm >> q) & (ccm >> r) & 1u) && near_tol(ce[q], ce[r], A.guard_tol))
-              ++guard;
+          for (int r = q + 1; r < CMAX; ++r) scr |= ((cvm >> r) & 1u) && fabs(ce[q] - ce[r]) <= tq;
         }
         // rank (EX desc, id asc) among candidates with EX >= threshold, first max_count
         unsigned left = 0u;
@@ -239,6 +276,8 @@ __global__ void __launch_bounds__(kPrWarps * 32, 1) k_pred_rank(const EvalArgs A
           if (A.rec_out) A.rec_out[(so * G * 64 + t) * A.max_count + rk] = (int8_t)ob;
         }
       }
+      if (__any_sync(FULL, scr) && scr)      // cold: the exact guard rule of this lane's version
+        guard += guard_count<CMAX>(A, ut, ldut, Cp, ols, obit, ext + lane * (CMAX + 1), slots[row], O);
       __syncwarp();
     }
     // ---- A7 rows ----

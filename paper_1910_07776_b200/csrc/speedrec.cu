@@ -1059,8 +1059,9 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   // model in a table, k_pred_rank predicts (DMMA), scores and ranks per
   // scenario -- no EX table, no k_rank_warp.  SPEEDREC_SPLIT_LS=0 (or the
   // opt-in fused ranking) keeps the EX-table path.
+  const int ks_pr = (C + 3) / 4;                        // k_pred_rank instantiations: 1, 5, 8, 16 k-steps
   bool split_ls = prm->learner == SR_LINREG && !c->coef_req && !c->sweep && !agg && stage && C <= kPrMaxC &&
-                  c->n_os <= 8;
+                  c->n_os <= 8 && (ks_pr == 1 || ks_pr == 5 || ks_pr == 8 || ks_pr == 16);
   if (const char* e = getenv("SPEEDREC_SPLIT_LS")) split_ls = split_ls && atoi(e) != 0;
   if (const char* e = getenv("SPEEDREC_FUSE_RANK")) split_ls = split_ls && atoi(e) == 0;
   // k_pred_rank's shared-memory plan: rates staged with a row stride = 4 mod 16
@@ -1257,7 +1258,11 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     const long long fblocks = std::max(1LL, std::min(max_fit_blocks, (cc * O + wpb - 1) / wpb));
     if ((st = launch(c, "k_fit_warp", [&] { kfit<<<(unsigned)fblocks, wpb * 32, smem, c->stream>>>(A); }))) return st;
     if (split_ls) {
-      auto kpr = c->n_os <= 6 ? k_pred_rank<6> : k_pred_rank<8>;
+      const int ks = (C + 3) / 4;
+      auto kpr = c->n_os <= 6 ? (ks == 16 ? k_pred_rank<6, 16> : ks == 8 ? k_pred_rank<6, 8> : ks == 5 ? k_pred_rank<6, 5>
+                                                                                            : k_pred_rank<6, 1>)
+                              : (ks == 16 ? k_pred_rank<8, 16> : ks == 8 ? k_pred_rank<8, 8> : ks == 5 ? k_pred_rank<8, 5>
+                                                                                            : k_pred_rank<8, 1>);
       CU(cudaFuncSetAttribute(kpr, cudaFuncAttributeMaxDynamicSharedMemorySize, PL.bytes));
       const long long pblocks = std::max(1LL, std::min<long long>(c->sm_count, (cc + PL.warps - 1) / PL.warps));
       if ((st = launch(c, "k_pred_rank", [&] { kpr<<<(unsigned)pblocks, PL.warps * 32, PL.bytes, c->stream>>>(A, PL); })))
