@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
   const WarpLayout& L = A.L;
   int8_t* obit = reinterpret_cast<int8_t*>(smem);
   const int tid = threadIdx.x, nthr = blockDim.x;
-  for (int i = tid; i < A.P * A.O; i += nthr) obit[i] = A.opt_bit[i];
+  // per-GROUP optimization bits (no division by I*R in the pair loop)
+  for (int i = tid; i < A.G * A.O; i += nthr) obit[i] = A.opt_bit[(i / A.O / A.IR) * A.O + i % A.O];
   const double* X = A.x;
   int ldx = A.C;
   if (STAGED) {
@@ -337,12 +338,34 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     }
   };
 
-  for (long long f = gwarp; f < A.count * O; f += nwarps) {
-    const long long sl = f / O;
-    const int o = (int)(f - sl * O);
-    const long long s = A.first + sl, so = A.out0 + sl;
-    const long long split = s % A.sd.n_splits, fidx = s / A.sd.n_splits;
-    const uint32_t om = scored_mask(A.sd, split, O);
+  // scenario-major (A.scn_major, large batches): a warp fits all O
+  // optimizations of one scenario in turn, so the split words and the feature
+  // list are formed once per scenario; fit-major (small, latency-bound
+  // batches): one fit per work unit, spreading a scenario over warps
+  const long long units = A.scn_major ? A.count : A.count * O;
+  for (long long u = gwarp; u < units; u += nwarps) {
+  const long long sl = A.scn_major ? u : u / O;
+  const int o_lo = A.scn_major ? 0 : (int)(u - sl * O), o_hi = A.scn_major ? O : o_lo + 1;
+  const long long s = A.first + sl, so = A.out0 + sl;
+  const long long split = s % A.sd.n_splits, fidx = s / A.sd.n_splits;
+  const uint32_t om = scored_mask(A.sd, split, O);
+  // ---- A1: split membership (Table 2; R17), features ----
+  for (int g = lane; g < G; g += 32) {
+    uint64_t tr, te;
+    member_words(A.sd, split, g, tr, te);
+    trw[g] = tr;
+    tew[g] = te;
+  }
+  int d = 0;
+  for (int c0 = 0; c0 < C; c0 += 32) {
+    const int c = c0 + lane;
+    const bool in = c < C && feature_in(A.sd, fidx, c);
+    const unsigned bm = __ballot_sync(FULL, in);
+    if (in) F[d + __popc(bm & lt)] = (int16_t)c;
+    d += __popc(bm);
+  }
+  __syncwarp();
+  for (int o = o_lo; o < o_hi; ++o) {
     OptScore row;
     row.n_train = row.n_test = row.n_correct = row.n_clamped = 0;
     row.sum_ratio = row.min_ratio = row.max_ratio = 0.0;
@@ -356,27 +379,12 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     const int q = __popc(om & ((1u << o) - 1u));  // scored-optimization slot in the EX table
     double* urow = MODE == 4 ? A.utab + (sl * (long long)A.n_os + q) * A.ldu : nullptr;
 
-    // ---- A1: split membership (Table 2; R17), features, pairs ----
-    for (int g = lane; g < G; g += 32) {
-      uint64_t tr, te;
-      member_words(A.sd, split, g, tr, te);
-      trw[g] = tr;
-      tew[g] = te;
-    }
-    int d = 0;
-    for (int c0 = 0; c0 < C; c0 += 32) {
-      const int c = c0 + lane;
-      const bool in = c < C && feature_in(A.sd, fidx, c);
-      const unsigned bm = __ballot_sync(FULL, in);
-      if (in) F[d + __popc(bm & lt)] = (int16_t)c;
-      d += __popc(bm);
-    }
-    __syncwarp();
+    // ---- A1: pairs ----
     int n = 0, nt = 0;
     uint64_t fptr = 0, fpte = 0;
     #pragma unroll 1
     for (int g = 0; g < G; ++g) {
-      const int b = obit[(g / A.IR) * O + o];
+      const int b = obit[g * O + o];
       const uint64_t tr = trw[g], te = tew[g];
       if (b < 0 || (tr == 0ull && te == 0ull)) continue;
       const int v = ins0(lane, b);
@@ -642,6 +650,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     }
     __syncwarp();
     finish(sl, om);
+  }
   }
   if (A.totals && lane == 0 && tot_test) {
     atomicAdd(&A.totals[0], tot_corr);

@@ -134,6 +134,7 @@ struct EvalArgs {
   double* utab;
   int ldu;
   int n_os;              // scored-optimization slots per scenario (table rows)
+  int scn_major;         // k_fit_warp work unit: 1 = a whole scenario, 0 = one fit
 };
 // model-table row fields after the C weights (k_fit_warp MODE 4 / k_pred_rank)
 constexpr int kUc0 = 0, kUflag = 1, kUntr = 2, kUnte = 3, kUfptr = 4, kUfpte = 5, kUextra = 6;

@@ -1040,7 +1040,7 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   // forces staging of x in shared memory, SPEEDREC_WMAX in {12,16} picks the
   // warps-per-CTA variant, SPEEDREC_SMEM_KB caps shared memory per CTA.
   const int budget = c->max_smem_optin;                  // 232448 on B200
-  const int head = align16(c->P * O);
+  const int head = align16(G * O);                      // per-group optimization bits
   const int ldxs = C | 1;
   const long long stage_bytes = N * ldxs * 8;
   const int mmax = std::min(c->np_tr, c->dmax + 1);      // largest system any fit can need
@@ -1255,7 +1255,10 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     if (const char* e = getenv("SPEEDREC_FUSE_RANK"))
       A.fuse_rank = (atoi(e) != 0 && cmax == 8 && prm->learner == SR_LINREG && !c->coef_req) ? 1 : 0;
     if (A.fuse_rank) CU(cudaMemsetAsync(A.done, 0, (size_t)cc * 4, c->stream));
-    const long long fblocks = std::max(1LL, std::min(max_fit_blocks, (cc * O + wpb - 1) / wpb));
+    // whole scenarios per warp once the chunk has >= 4 scenarios per resident warp
+    A.scn_major = cc >= 4 * max_fit_blocks * wpb ? 1 : 0;
+    const long long units = A.scn_major ? cc : cc * O;
+    const long long fblocks = std::max(1LL, std::min(max_fit_blocks, (units + wpb - 1) / wpb));
     if ((st = launch(c, "k_fit_warp", [&] { kfit<<<(unsigned)fblocks, wpb * 32, smem, c->stream>>>(A); }))) return st;
     if (split_ls) {
       const int ks = (C + 3) / 4;
