@@ -298,6 +298,12 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     X = xs;
     ldx = A.ldxs;
   }
+  const double* ylab = A.ylab;          // the labels, staged when small (C1, C3: 1-3 KB)
+  if (A.stage_y) {
+    double* ys = reinterpret_cast<double*>(smem + A.off_y);
+    for (int i = tid; i < A.G * A.O * 32; i += nthr) ys[i] = A.ylab[i];
+    ylab = ys;
+  }
   __syncthreads();
 
   const int warp = tid >> 5, lane = tid & 31;
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
         if (istr) {
           const int p = n + __popc(mtr & lt);
           trs[p] = g * 64 + v;
-          yc[p] = A.ylab[lab];
+          yc[p] = ylab[lab];
           fptr ^= h;
         }
         if (iste) {
@@ -581,7 +587,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
         ++ncl;
       }
       const int gk = tek[j];
-      const double ac = A.ylab[((gk >> 5) * O + o) * 32 + (gk & 31)];
+      const double ac = ylab[((gk >> 5) * O + o) * 32 + (gk & 31)];
       ncorr += ((e > 1.0 && ac > 1.0) || (e <= 1.0 && ac <= 1.0)) ? 1 : 0;
       const double ratio = ac / e;
       rsum += ratio;

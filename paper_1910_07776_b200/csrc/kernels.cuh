@@ -135,6 +135,8 @@ struct EvalArgs {
   int ldu;
   int n_os;              // scored-optimization slots per scenario (table rows)
   int scn_major;         // k_fit_warp work unit: 1 = a whole scenario, 0 = one fit
+  int stage_y;           // 1: the labels ylab [G][O][32] staged in shared memory at off_y
+  int off_y;
 };
 // model-table row fields after the C weights (k_fit_warp MODE 4 / k_pred_rank)
 constexpr int kUc0 = 0, kUflag = 1, kUntr = 2, kUnte = 3, kUfptr = 4, kUfpte = 5, kUextra = 6;

@@ -1103,6 +1103,10 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     wpb = std::min(wmax, avail / L.bytes);
   }
   if (wpb < 1) return fail(c, SR_E_UNSUPPORTED, "evaluate: per-warp workspace %d B exceeds shared memory", L.bytes);
+  // stage the labels too when they are small and the warps keep their count
+  const int ybytes = align16(G * O * 32 * 8);
+  const int base_warps = head + (stage ? align16((int)stage_bytes) : 0);
+  const int stage_y = (ybytes <= 16384 && base_warps + ybytes + wpb * L.bytes <= budget_cap) ? 1 : 0;
   // global scratch for systems beyond the shared-memory factor: packed factor + 2 vectors
   long long mscr = (mmax > std::min(mcap, 32)) ? (long long)mmax * (mmax + 1) / 2 + 2LL * L.vmax : 0;
   // M5P: the tree workspace (scaled rows, nodes, model pool, node systems) per warp
@@ -1131,7 +1135,9 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   A.stage_x = stage;
   A.ldxs = ldxs;
   A.off_stage = head;
-  A.off_warps = head + (stage ? align16((int)stage_bytes) : 0);
+  A.stage_y = stage_y;
+  A.off_y = base_warps;
+  A.off_warps = base_warps + (stage_y ? ybytes : 0);
   const int smem = A.off_warps + wpb * L.bytes;
   auto kfit = split_ls ? k_fit_warp<16, 4, true>
               : prm->learner == SR_IBK ? (stage ? k_fit_warp<16, 1, true> : k_fit_warp<16, 1, false>)
