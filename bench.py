@@ -33,17 +33,19 @@ sys.path.insert(0, ROOT)
 FP64_FMA_PER_CLK_PER_SM = 64   # inferred from the measured DMMA loop (profiles/fp64_peak.txt)
 
 
-def fit_flops(n: np.ndarray, t: np.ndarray, d: int, refine: int = 2) -> float:
+def fit_flops(n: np.ndarray, t: np.ndarray, d: int, refine: int = 2, predict: bool = True) -> float:
     """Algorithmic FP64 flops of the fits a batch performed:
     per fit with n training pairs, t test cases and d active features,
       dual   (n-1 < d): n(n+1)/2*d + n^3/6 + n^2 + R*(2nd + n^2) + nd + td   FMA
       primal (else)   : n*d(d+1)/2 + d^3/6 + nd + d^2 + R*(2nd + d^2) + td   FMA
     R = refine when the fit's rule asks for it (dual: 2(n-1) >= d, primal:
     n-1 < 2d or n > 64), else 0.  flop = 2 * FMA.  Fits with
-    n == 0 or t == 0 do no work."""
+    n == 0 or t == 0 do no work.  predict=False drops the t*d prediction term
+    (the split LS path predicts in k_pred_rank)."""
     n = n.astype(np.float64)
-    t = t.astype(np.float64)
+    t = t.astype(np.float64) if predict else np.zeros_like(n) + (t > 0)
     live = (n > 0) & (t > 0)
+    t = t * (1.0 if predict else 0.0)
     dual = (n - 1) < d
     rd = np.where(2 * (n - 1) >= d, refine, 0)
     rp = np.where(((n - 1) < 2 * d) | (n > 64), refine, 0)
@@ -447,6 +449,7 @@ def main():
     # ---------------- roofline of the dominant kernel (FP64 ALU/DMMA bound)
     big = ds.n_groups > 64          # CTA-per-fit path (C4): prediction runs in k_rank_big
     flops_pd = None
+    flops_all = None
     name_dom = ("k_ibk_dist" if args.learner == "ibk" else "k_fit_big") if big else "k_fit_warp"
     if c5:
         # n, t per (fold, opt) do not depend on the mask: take them from one
@@ -483,7 +486,9 @@ def main():
         elif big:
             flops_launch = fit_flops_big(n_tr, n_te, ds.n_counters)
         else:
-            flops_launch = fit_flops(n_tr, n_te, ds.n_counters, refine=2)
+            split = stats.get("k_pred_rank", (0, 0.0))[0] > 0     # split LS path: prediction in k_pred_rank
+            flops_launch = fit_flops(n_tr, n_te, ds.n_counters, refine=2, predict=not split)
+            flops_all = fit_flops(n_tr, n_te, ds.n_counters, refine=2)
     n_dom, ms_dom = stats.get(name_dom, (0, 0.0))
     avg_dom = ms_dom / max(n_dom, 1)                 # average launch duration (CUDA events, live)
     launches_per_step = max(n_dom // max(args.steps, 1), 1)
@@ -509,6 +514,9 @@ def main():
     # = flops per launch / average launch time; also right for unequal launches
     achieved = flops_step / (ms_dom / max(args.steps, 1) / 1e3) / 1e12 if ms_dom > 0 else 0.0
     share = ms_dom / max(sum(v[1] for v in stats.values()), 1e-9)
+    # whole step: every algorithmic flop of the path over the step time (the
+    # split LS path's prediction runs in k_pred_rank, outside the fit kernel)
+    step_achieved = (flops_all if flops_all is not None else flops_step) / (ms / 1e3) / 1e12            # per GPU
 
     # ---------------- end to end: host buffers through the C-ABI, copies inside
     e2e = None
@@ -604,6 +612,7 @@ def main():
                          "peak_note": f"FP64 (DFMA/DMMA shared pipe): {props.multi_processor_count} SMs x "
                                       f"{FP64_FMA_PER_CLK_PER_SM} FMA/clk x 2 x {sm_max:.0f} MHz",
                          "effective": name_dom == "k_mask_sfit",
+                         "step_achieved": step_achieved, "step_frac": step_achieved / peak if peak else None,
                          "frac_yardstick_p_eq_S": (flops_pd / (ms_dom / max(args.steps, 1) / 1e3) / 1e12 / peak
                                                    if flops_pd and ms_dom > 0 else None),
                          "flops_note": ("SURVEY 8(d) C5 yardstick p^3/6+p^2+p per fit on the precomputed "
@@ -611,7 +620,9 @@ def main():
                                         "so frac is an effective fraction" if name_dom == "k_mask_sfit"
                                         else "M5P yardstick: the root split search only, 4 d (n-1) n flop "
                                         "per fit (DESIGN 6)" if args.learner == "m5"
-                                        else "algorithmic flops of the fits (DESIGN 6)")},
+                                        else "algorithmic flops of the fits, prediction (t d) counted in "
+                                        "k_pred_rank's share when the split LS path runs (DESIGN 5.12, 6); "
+                                        "step_* = all algorithmic flops over the whole step")},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "gather": {"collective": "all_gather_into_tensor" if world > 1 else "none (1 GPU)",
                        "backend": backend if world > 1 else None, "ms_per_step": gather_ms,
