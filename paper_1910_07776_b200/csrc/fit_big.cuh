@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
             double* ri = Gbuf + (c0 + (lane & 7)) * kBigGLd + c0;
             for (int j = 0; j < 8; ++j) {
               const double* rj = Gbuf + (c0 + j) * kBigGLd + c0;
-              double v = ri[j];
+              double v = lane < 8 ? ri[j] : 0.0;     // lanes >= 8 alias rows 0..7: no read of the element being written
               for (int k = 0; k < j; ++k) v = fma(-ri[k], rj[k], v);
               const double r = __shfl_sync(FULL, rsqrt_nr(v), j);   // 1/L_jj from lane j
               if (lane < 8 && lane >= j) ri[j] = v * r;            // L_ij (lane j: L_jj = v / sqrt(v))

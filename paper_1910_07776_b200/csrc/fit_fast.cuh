@@ -203,7 +203,9 @@ __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv, bo
       t0 = fma(a.x, c.x, t0);
       t1 = fma(a.y, c.y, t1);
     }
-    const double2 kij = *reinterpret_cast<const double2*>(ri + j);   // K_ij, K_i,j+1 (row i >= j+1)
+    // K_ij, K_i,j+1 (row i >= j+1); lanes past the rows (whose ri aliases row
+    // 0) read nothing: lane 0 writes row 0 in this step (racecheck-clean)
+    const double2 kij = lane < mr ? *reinterpret_cast<const double2*>(ri + j) : make_double2(0.0, 0.0);
     const double v = kij.x - (s0 + s1);           // lane j: pivot; lanes i > j: unscaled L_ij
     const double r = __shfl_sync(FULL, rsqrt_nr(v), j);  // 1/L_jj (NaN/inf iff the pivot is not > 0)
     const double lij = v * r;
