@@ -27,11 +27,14 @@
 //                prefix), EX, clamp, score, rank / recommend, per-scenario
 //                rows when asked, per-mask sums.
 #pragma once
+#include <type_traits>
+
 #include "eval_masks.cuh"
 
 namespace speedrec {
 
 constexpr int kSchurU = 10;                 // suffix counters (register system size)
+constexpr int kSfitMaxO = 6;                // optimization ids of the prefix-shared path (the paper's six)
 constexpr int kSchurT = 12;                 // largest prefix (counters before the suffix)
 constexpr int kSchurQ = kSchurU * (kSchurU + 1) / 2;
 constexpr int kRec = 80;                    // doubles per record: Q[55] r~[10] z~[10] base flags pad
@@ -40,8 +43,17 @@ constexpr int kRecR = kSchurQ, kRecZ = kSchurQ + kSchurU, kRecBase = kSchurQ + 2
 #define SPEEDREC_SFIT_THREADS 256
 #endif
 constexpr int kSfitThreads = SPEEDREC_SFIT_THREADS;
+#ifndef SPEEDREC_SFIT_SCHED        // A/B knob: register budget schedule of k_mask_sfit<D>
+#define SPEEDREC_SFIT_SCHED 0
+#endif
 #ifndef SPEEDREC_SFIT_MINB        // CTAs per SM the register budget of k_mask_sfit<D> targets
+#if SPEEDREC_SFIT_SCHED == 1
+#define SPEEDREC_SFIT_MINB(D) ((D) <= 2 ? 4 : (D) <= 8 ? 2 : 1)
+#elif SPEEDREC_SFIT_SCHED == 2
+#define SPEEDREC_SFIT_MINB(D) ((D) <= 1 ? 4 : (D) <= 8 ? 2 : 1)
+#else
 #define SPEEDREC_SFIT_MINB(D) ((D) <= 3 ? 4 : (D) <= 8 ? 2 : 1)
+#endif
 #endif
 
 struct SchurArgs {
@@ -254,7 +266,12 @@ __global__ void __launch_bounds__(128) k_mask_sprep_p(const SchurArgs SA, const 
 // EX - ybar - base of one suffix system of compile-time size D from a staged
 // record: gather Q_SS (f ascending, so the packed lower layout is preserved),
 // factor with r~ and z~ carried as augmented rows, y~.u~.
-template <int D>
+// SM: the record is staged in shared memory (plain loads), else read through
+// the read-only path (__ldg).
+template <bool SM>
+__device__ __forceinline__ double rec_ld(const double* p) { return SM ? *p : __ldg(p); }
+
+template <int D, bool SM = false>
 __device__ __forceinline__ double schur_fit(const double* R, const int* f, bool& ok) {
   if (D == 0) return 0.0;
   constexpr int TT = D * (D + 1) / 2;
@@ -263,9 +280,9 @@ __device__ __forceinline__ double schur_fit(const double* R, const int* f, bool&
   for (int i = 0; i < D; ++i) {
     const int fi = f[i], bi = fi * (fi + 1) / 2;
 #pragma unroll
-    for (int k = 0; k <= i; ++k) L[i * (i + 1) / 2 + k] = __ldg(R + bi + f[k]);
-    L[TT + i] = __ldg(R + kRecR + fi);
-    L[TT + D + i] = __ldg(R + kRecZ + fi);
+    for (int k = 0; k <= i; ++k) L[i * (i + 1) / 2 + k] = rec_ld<SM>(R + bi + f[k]);
+    L[TT + i] = rec_ld<SM>(R + kRecR + fi);
+    L[TT + D + i] = rec_ld<SM>(R + kRecZ + fi);
   }
 #pragma unroll
   for (int j = 0; j < D; ++j) {
@@ -301,135 +318,182 @@ __global__ void __launch_bounds__(kSfitThreads, SPEEDREC_SFIT_MINB(D)) k_mask_sf
   const long long S = M.sd.n_splits;
   unsigned long long t_corr = 0, t_test = 0, t_rec = 0, t_hit = 0;
   const int item = tid % n_items, chunk = tid / n_items;
-  if (chunk < fold_chunks) {
-    const int ml = SA.order[off + item];
-    const int grp = SA.group[off + item];
-    const long long fidx = M.mask0 + ml;
-    const uint32_t sfx = (mask_bits(M.sd, fidx) >> T) & ((1u << SA.U) - 1u);
-    int f[D > 0 ? D : 1];
-    {
-      uint32_t mm = sfx;
+  const bool active = chunk < fold_chunks;
+  // Records through shared memory (CTA-uniform decision): when every thread of
+  // the CTA evaluates all folds of masks sharing ONE prefix group, a fold's O
+  // records (contiguous, O x 640 B) arrive by one TMA bulk copy, double
+  // buffered one fold ahead on an mbarrier; otherwise they are gathered
+  // through L1 (__ldg).
+  // up to two prefix groups per CTA (a CTA of 256 sorted masks spans at most
+  // two groups for suffix sizes 3..7, the large launches)
+  __shared__ __align__(16) double srec[2][2][kSfitMaxO * kRec];
+  __shared__ __align__(8) uint64_t sbar[2];
+  const int i0 = blockIdx.x * blockDim.x, ilast = min(i0 + (int)blockDim.x, n_items) - 1;
+  const int g0 = i0 < n_items ? SA.group[off + i0] : 0, g1 = i0 < n_items ? SA.group[off + ilast] : 0;
+  const bool staged = fold_chunks == 1 && i0 < n_items && g1 - g0 <= 1;
+  const int ml = active ? SA.order[off + item] : 0;
+  const int grp = active ? SA.group[off + item] : 0;
+  const long long fidx = M.mask0 + ml;
+  const uint32_t sfx = active ? (mask_bits(M.sd, fidx) >> T) & ((1u << SA.U) - 1u) : 0u;
+  int f[D > 0 ? D : 1];
+  {
+    uint32_t mm = sfx;
 #pragma unroll
-      for (int i = 0; i < D; ++i) {
-        f[i] = mm ? __ffs(mm) - 1 : 0;
-        mm &= mm - 1u;
-      }
+    for (int i = 0; i < D; ++i) {
+      f[i] = mm ? __ffs(mm) - 1 : 0;
+      mm &= mm - 1u;
     }
-    int s_corr = 0, s_test = 0, s_rec = 0, s_hit = 0;
-    const int s0 = (int)(S * chunk / fold_chunks), s1 = (int)(S * (chunk + 1) / fold_chunks);
-    const double* recg = SA.rec + (long long)grp * S * O * kRec;
-    #pragma unroll 1
-    for (int split = s0; split < s1; ++split) {
-      const long long sl = fidx * S + split - M.first;
-      const uint32_t om = scored_mask(M.sd, split, O);
-      const int g = M.sd.pool_list[split >> 6], v = split & 63, p = g / M.IR;
-      double ce[kMaskMaxO];
-      bool cv[kMaskMaxO], cc[kMaskMaxO];
-      int guard = 0, untrained = 0;
+  }
+  int s_corr = 0, s_test = 0, s_rec = 0, s_hit = 0;
+  const double* recg = SA.rec + (long long)grp * S * O * kRec;
+  // one fold of this thread's mask; SM: the fold's records are in shared memory at Rb
+  // (one code path: generic loads serve both shared and global records)
+  auto fold = [&](int split, const double* Rb) {
+    constexpr bool SM = true;
+    const long long sl = fidx * S + split - M.first;
+    const uint32_t om = scored_mask(M.sd, split, O);
+    const int g = M.sd.pool_list[split >> 6], v = split & 63, p = g / M.IR;
+    double ce[kSfitMaxO];
+    bool cv[kSfitMaxO], cc[kSfitMaxO];
+    int guard = 0, untrained = 0;
 #pragma unroll
-      for (int o = 0; o < kMaskMaxO; ++o) {
-        cv[o] = cc[o] = false;
-        ce[o] = 0.0;
-        if (o >= O) continue;
-        asm volatile("" ::: "memory");   // one optimisation at a time: no load hoisting across them
-        const PrepMeta& pm = M.pm[split * O + o];
-        OptScore row;
-        row.n_train = row.n_test = row.n_correct = row.n_clamped = 0;
-        row.sum_ratio = row.min_ratio = row.max_ratio = 0.0;
-        row.fp_train = row.fp_test = 0ull;
-        const int n = pm.n;
-        if (n >= 0 && ((om >> o) & 1u)) {
-          row.n_train = n;
-          row.n_test = pm.nt;
-          row.fp_train = pm.fp_tr;
-          row.fp_test = pm.fp_te;
-          s_test += pm.nt;
-          if (n == 0 && pm.nt > 0) ++untrained;
-          if (n > 0 && pm.nt > 0) {
-            const double* R = recg + ((long long)split * O + o) * kRec;
-            const unsigned long long flags = (unsigned long long)__double_as_longlong(__ldg(R + kRecFlag));
-            bool ok = (flags & 2ull) == 0ull;
-            // an inactive suffix counter (rg = 0 in this fold) has a zero row and
-            // column in Q and zero r~, z~: its pivot is lambda and it adds exact
-            // zeros, so the fit equals the one without it (reading D3)
-            double e = pm.ybar + __ldg(R + kRecBase) + schur_fit<D>(R, f, ok);
-            if (!ok) {
-              e = pm.ybar;
-              guard += 1000000;
-            }
-            if (near_tol(e, 0.0, M.guard_tol) || near_tol(e, 1.0, M.guard_tol)) ++guard;
-            bool cl = false;
-            if (e <= 0.0) {
-              e = M.clamp_floor;
-              cl = true;
-            }
-            const double ac = pm.ac;
-            const int corr = ((e > 1.0 && ac > 1.0) || (e <= 1.0 && ac <= 1.0)) ? 1 : 0;
-            const double ratio = ac / e;
-            row.n_correct = corr;
-            row.n_clamped = cl ? 1 : 0;
-            row.sum_ratio = row.min_ratio = row.max_ratio = ratio;
-            s_corr += corr;
-            t_corr += corr;
-            t_test += 1;
-            cv[o] = true;
-            cc[o] = cl;
-            ce[o] = e;
-            if (M.ex_out) M.ex_out[(sl * O + o) * (long long)G * 32 + pm.tek] = e;
+    for (int o = 0; o < kSfitMaxO; ++o) {
+      cv[o] = cc[o] = false;
+      ce[o] = 0.0;
+      if (o >= O) continue;
+      asm volatile("" ::: "memory");   // one optimisation at a time: no load hoisting across them
+      const PrepMeta& pm = M.pm[split * O + o];
+      OptScore row;
+      row.n_train = row.n_test = row.n_correct = row.n_clamped = 0;
+      row.sum_ratio = row.min_ratio = row.max_ratio = 0.0;
+      row.fp_train = row.fp_test = 0ull;
+      const int n = pm.n;
+      if (n >= 0 && ((om >> o) & 1u)) {
+        row.n_train = n;
+        row.n_test = pm.nt;
+        row.fp_train = pm.fp_tr;
+        row.fp_test = pm.fp_te;
+        s_test += pm.nt;
+        if (n == 0 && pm.nt > 0) ++untrained;
+        if (n > 0 && pm.nt > 0) {
+          const double* R = Rb + o * kRec;
+          const unsigned long long flags = (unsigned long long)__double_as_longlong(rec_ld<SM>(R + kRecFlag));
+          bool ok = (flags & 2ull) == 0ull;
+          // an inactive suffix counter (rg = 0 in this fold) has a zero row and
+          // column in Q and zero r~, z~: its pivot is lambda and it adds exact
+          // zeros, so the fit equals the one without it (reading D3)
+          double e = pm.ybar + rec_ld<SM>(R + kRecBase) + schur_fit<D, SM>(R, f, ok);
+          if (!ok) {
+            e = pm.ybar;
+            guard += 1000000;
           }
-        }
-        if (M.opt_out) M.opt_out[sl * O + o] = row;
-      }
-      // A6: rank the held-out version's candidates (R13, R21)
-#pragma unroll
-      for (int a = 0; a < kMaskMaxO; ++a) {
-        if (!cv[a]) continue;
-        if (near_tol(ce[a], M.threshold, M.guard_tol)) ++guard;
-#pragma unroll
-        for (int b = a + 1; b < kMaskMaxO; ++b)
-          if (cv[b] && !(cc[a] && cc[b]) && near_tol(ce[a], ce[b], M.guard_tol)) ++guard;
-      }
-      int nrec = 0, nhit = 0;
-#pragma unroll
-      for (int a = 0; a < kMaskMaxO; ++a) {
-        if (!cv[a] || !(ce[a] >= M.threshold)) continue;
-        int rk = 0;
-#pragma unroll
-        for (int b = 0; b < kMaskMaxO; ++b)
-          if (b != a && cv[b] && ce[b] >= M.threshold && (ce[b] > ce[a] || (ce[b] == ce[a] && b < a))) ++rk;
-        if (rk < M.max_count) {
-          ++nrec;
-          const int bb = M.opt_bit[p * O + a];
-          if (M.ylab[(g * O + a) * 32 + rmv(v, bb)] > 1.0) ++nhit;
-          if (M.rec_out) M.rec_out[(sl * G * 64 + g * 64 + v) * M.max_count + rk] = (int8_t)a;
+          if (near_tol(e, 0.0, M.guard_tol) || near_tol(e, 1.0, M.guard_tol)) ++guard;
+          bool cl = false;
+          if (e <= 0.0) {
+            e = M.clamp_floor;
+            cl = true;
+          }
+          const double ac = pm.ac;
+          const int corr = ((e > 1.0 && ac > 1.0) || (e <= 1.0 && ac <= 1.0)) ? 1 : 0;
+          const double ratio = ac / e;
+          row.n_correct = corr;
+          row.n_clamped = cl ? 1 : 0;
+          row.sum_ratio = row.min_ratio = row.max_ratio = ratio;
+          s_corr += corr;
+          t_corr += corr;
+          t_test += 1;
+          cv[o] = true;
+          cc[o] = cl;
+          ce[o] = e;
+          if (M.ex_out) M.ex_out[(sl * O + o) * (long long)G * 32 + pm.tek] = e;
         }
       }
-      s_rec += nrec;
-      s_hit += nhit;
-      t_rec += nrec;
-      t_hit += nhit;
-      if (M.scn_out) {
-        ScnScore sr;
-        sr.n_rec = nrec;
-        sr.n_rec_hit = nhit;
-        sr.n_untrained = untrained;
-        sr.n_guard = guard;
-        M.scn_out[sl] = sr;
+      if (M.opt_out) M.opt_out[sl * O + o] = row;
+    }
+    // A6: rank the held-out version's candidates (R13, R21)
+#pragma unroll
+    for (int a = 0; a < kSfitMaxO; ++a) {
+      if (!cv[a]) continue;
+      if (near_tol(ce[a], M.threshold, M.guard_tol)) ++guard;
+#pragma unroll
+      for (int b = a + 1; b < kSfitMaxO; ++b)
+        if (cv[b] && !(cc[a] && cc[b]) && near_tol(ce[a], ce[b], M.guard_tol)) ++guard;
+    }
+    int nrec = 0, nhit = 0;
+#pragma unroll
+    for (int a = 0; a < kSfitMaxO; ++a) {
+      if (!cv[a] || !(ce[a] >= M.threshold)) continue;
+      int rk = 0;
+#pragma unroll
+      for (int b = 0; b < kSfitMaxO; ++b)
+        if (b != a && cv[b] && ce[b] >= M.threshold && (ce[b] > ce[a] || (ce[b] == ce[a] && b < a))) ++rk;
+      if (rk < M.max_count) {
+        ++nrec;
+        const int bb = M.opt_bit[p * O + a];
+        if (M.ylab[(g * O + a) * 32 + rmv(v, bb)] > 1.0) ++nhit;
+        if (M.rec_out) M.rec_out[(sl * G * 64 + g * 64 + v) * M.max_count + rk] = (int8_t)a;
       }
     }
-    if (M.mask_acc) {
-      int* acc = M.mask_acc + (long long)ml * 4;
-      if (fold_chunks == 1) {
-        acc[0] = s_corr;
-        acc[1] = s_test;
-        acc[2] = s_rec;
-        acc[3] = s_hit;
-      } else {
-        atomicAdd(acc + 0, s_corr);
-        atomicAdd(acc + 1, s_test);
-        atomicAdd(acc + 2, s_rec);
-        atomicAdd(acc + 3, s_hit);
+    s_rec += nrec;
+    s_hit += nhit;
+    t_rec += nrec;
+    t_hit += nhit;
+    if (M.scn_out) {
+      ScnScore sr;
+      sr.n_rec = nrec;
+      sr.n_rec_hit = nhit;
+      sr.n_untrained = untrained;
+      sr.n_guard = guard;
+      M.scn_out[sl] = sr;
+    }
+  };
+  if (staged) {
+    const unsigned bytes = (unsigned)(O * kRec * 8);
+    const int ng = g1 - g0 + 1;                      // 1 or 2 groups
+    const double* gsrc = SA.rec + (long long)g0 * S * O * kRec;
+    const long long gstride = S * O * kRec;
+    auto issue = [&](int split, int b) {            // the fold's records of the CTA's groups -> buffer b
+      mbar_expect_tx(&sbar[b], ng * bytes);
+      for (int q = 0; q < ng; ++q) bulk_g2s_tx(srec[b][q], gsrc + q * gstride + (long long)split * O * kRec, bytes, &sbar[b]);
+    };
+    if (threadIdx.x == 0) {
+      mbar_init(&sbar[0], 1);
+      mbar_init(&sbar[1], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) issue(0, 0);
+    unsigned phase = 0u;
+    const int mine = grp - g0;
+    #pragma unroll 1
+    for (int split = 0; split < (int)S; ++split) {
+      const int b = split & 1;
+      if (threadIdx.x == 0 && split + 1 < S) {      // next fold (buffer b^1 freed by the last barrier)
+        fence_proxy_async();
+        issue(split + 1, b ^ 1);
       }
+      mbar_wait(&sbar[b], (phase >> b) & 1u);
+      phase ^= 1u << b;
+      if (active) fold(split, srec[b][mine]);
+      __syncthreads();                               // every thread is done with buffer b
+    }
+  } else if (active) {
+    const int s0 = (int)(S * chunk / fold_chunks), s1 = (int)(S * (chunk + 1) / fold_chunks);
+    #pragma unroll 1
+    for (int split = s0; split < s1; ++split) fold(split, recg + (long long)split * O * kRec);
+  }
+  if (active && M.mask_acc) {
+    int* acc = M.mask_acc + (long long)ml * 4;
+    if (fold_chunks == 1) {
+      acc[0] = s_corr;
+      acc[1] = s_test;
+      acc[2] = s_rec;
+      acc[3] = s_hit;
+    } else {
+      atomicAdd(acc + 0, s_corr);
+      atomicAdd(acc + 1, s_test);
+      atomicAdd(acc + 2, s_rec);
+      atomicAdd(acc + 3, s_hit);
     }
   }
   if (M.totals) {

@@ -299,6 +299,18 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned 
                "l"(gsrc), "r"(bytes), "r"(b)
                : "memory");
 }
+// split form: one arrive.expect_tx for the total, then copies that only complete_tx
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_tx(void* sdst, const void* gsrc, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(sdst)),
+               "l"(gsrc), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
   const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile(

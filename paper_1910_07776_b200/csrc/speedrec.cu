@@ -722,7 +722,7 @@ sr_status run_mask_path(sr_ctx* c, const sr_params* prm, long long first, long l
   if (const char* e = getenv("SPEEDREC_MASK_PATH")) mode = atoi(e);
   const int K = c->mask_or ? 32 - __builtin_clz(c->mask_or) : 0;
   const int U = std::min(kSchurU, K), T = K - U;
-  if (mode == 2 && T <= kSchurT && K <= C) {
+  if (mode == 2 && T <= kSchurT && K <= C && O <= kSfitMaxO) {
     if ((st = run_schur_path(c, M, S, T, U, mask0, nm))) return st;
     *used = true;
     return SR_OK;
