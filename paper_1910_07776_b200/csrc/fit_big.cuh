@@ -355,6 +355,9 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       // copy mapping: thread (row crow, features ca0 + 8q); rows >= n and
       // features >= d are zero-filled
       // rows crow (all threads) and 32 + crow (t < 128) of the chunk
+      // every counter selected (d == C, so Fl[a] == a) and C even: each row
+      // is one contiguous span -> 16-byte copies (half the copy instructions)
+      const bool contig = d == C && (C & 1) == 0;
       auto issue = [&](int ch, int slot, int slot2) {
         double* st = ring + (ch % 3) * kGramChunk * kBigLd;
 #pragma unroll
@@ -362,13 +365,26 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
           const int row = crow + 32 * h;
           if (row >= kGramChunk) break;
           const int sl_ = h ? slot2 : slot;
-          double* dst = st + row * kBigLd + ca0;
           const double* xr = A.x + (sl_ >= 0 ? (long long)sl_ * C : 0);
+          if (contig) {
+            double* dst = st + row * kBigLd;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int a = ca0 + 8 * q;
-            const bool ok_ = sl_ >= 0 && a < d;
-            cp_async8(dst + 8 * q, xr + (ok_ ? Fl[a] : 0), ok_);
+            for (int q = 0; q < 8; ++q) {
+              const int a = 2 * ca0 + 16 * q;
+              const bool ok_ = sl_ >= 0 && a < d;
+              const unsigned dd = (unsigned)__cvta_generic_to_shared(dst + a);
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dd), "l"(xr + (ok_ ? a : 0)),
+                           "r"(ok_ ? 16 : 0)
+                           : "memory");
+            }
+          } else {
+            double* dst = st + row * kBigLd + ca0;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const int a = ca0 + 8 * q;
+              const bool ok_ = sl_ >= 0 && a < d;
+              cp_async8(dst + 8 * q, xr + (ok_ ? Fl[a] : 0), ok_);
+            }
           }
           if (ca0 == 0) {
             const int r = ch * kGramChunk + row;
@@ -390,9 +406,9 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
           const int r = fh + 2 * j;
           const bool live = fin && cc * kGramChunk + r < n;
           double xv = st[r * kBigLd + fa];
-          if (live) {
-            pmn = fmin(pmn, xv);
-            pmx = fmax(pmx, xv);
+          if (live) {                 // rates: finite, >= 0 (validated): no NaN handling
+            pmn = dmin(pmn, xv);
+            pmx = dmax(pmx, xv);
             psm += xv;
           }
           xv = live ? xv - cshift : 0.0;

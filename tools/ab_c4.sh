@@ -1,0 +1,7 @@
+#!/bin/bash
+# C4 (592 of 1e7 splits): per-kernel ms.
+cd "$(dirname "$0")/.."
+B="--config C4 --splits 592 --steps 5 --warmup 2 --no-e2e --no-extra --no-cpu-baseline"
+python bench.py $B 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1])
+k=d['kernels']; print('C4', round(d['ms_per_step'],2), 'ms/step', {n: round(v['ms']/5,2) for n,v in k.items() if v['launches']}, 'frac', round(d['roofline']['frac'],4))"
