@@ -501,10 +501,10 @@ def main():
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         ent = tj.get(name_dom)
         if ent and ent["workload"] == args.config:
-            per_launch_units = (count / launches_per_step) if name_dom != "k_mask_sfit" else None
-            if name_dom == "k_mask_sfit" or abs(per_launch_units - ent["units"]) <= 1:
-                traffic = ent["read"] + ent["write"]
-                traffic_note = f"{ent['per']}; {ent['source']}"
+            per_unit = (ent["read"] + ent["write"]) / ent["units"]
+            units = ent["units"] if name_dom == "k_mask_sfit" else count / launches_per_step
+            traffic = per_unit * units
+            traffic_note = f"{per_unit:.0f} B per {ent['per']} x {units:.0f} units per launch; {ent['source']}"
     except (OSError, ValueError, KeyError):
         pass
     clk_sum = clk.summary()

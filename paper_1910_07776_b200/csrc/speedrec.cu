@@ -1153,12 +1153,17 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
   // ---- per-chunk exchange buffers (EX table, trained masks, guard counts) ----
   const int tg_stride = 32 * c->n_tg;
   const int ex_stride = c->n_os * tg_stride;
-  long long chunk_bytes = 1024LL << 20;                 // EX table per launch (SPEEDREC_CHUNK_MB overrides; tools/sweep_c3.sh)
+  // exchange table per launch (SPEEDREC_CHUNK_MB overrides; tools/sweep_c3.sh,
+  // tools/ab_chunk.sh): 1 GB; the split LS path with device outputs takes the
+  // whole batch in one launch pair (fewer tails: C3 39.6 -> 38.9 ms), with host
+  // outputs 1 GB chunks so each chunk's rows copy back under the next one's fits
+  long long chunk_bytes = 1024LL << 20;
   if (const char* e = getenv("SPEEDREC_CHUNK_MB")) chunk_bytes = std::max(1LL, atoll(e)) << 20;
   // model-table row (split LS path): k_pred_rank's shared-memory row stride,
   // so one bulk copy moves a scenario's rows
   const int ldu = split_ls ? PL.ldut : ((C + kUextra + 1) / 2) * 2;
   const long long row_bytes = split_ls ? 8LL * c->n_os * ldu : 8LL * ex_stride;
+  if (split_ls && out->on_device && !getenv("SPEEDREC_CHUNK_MB")) chunk_bytes = 4096LL << 20;
   const long long chunk = std::max(1LL, std::min<long long>(count, chunk_bytes / row_bytes));
   if (split_ls) {
     if ((st = ensure(c, c->utab, (size_t)(chunk * row_bytes)))) return st;
