@@ -482,7 +482,10 @@ def main():
         if args.learner == "ibk":
             flops_launch = knn_flops(n_tr, n_te, ds.n_counters)
         elif args.learner == "m5":
-            flops_launch = m5_flops(n_tr, n_te, ds.n_counters)
+            # executed split-search FP64 operations of the step's grown trees
+            # (sr_last_work, the last timed evaluate); root-only yardstick as fallback
+            work = ctx.last_work()
+            flops_launch = float(work) if work > 0 else m5_flops(n_tr, n_te, ds.n_counters)
         elif big:
             flops_launch = fit_flops_big(n_tr, n_te, ds.n_counters)
         else:
@@ -618,8 +621,9 @@ def main():
                          "flops_note": ("SURVEY 8(d) C5 yardstick p^3/6+p^2+p per fit on the precomputed "
                                         "Gram with p = |S|+1; the prefix-shared path (DESIGN 5.8) executes fewer flops, "
                                         "so frac is an effective fraction" if name_dom == "k_mask_sfit"
-                                        else "M5P yardstick: the root split search only, 4 d (n-1) n flop "
-                                        "per fit (DESIGN 6)" if args.learner == "m5"
+                                        else "M5P: the FP64 operations the grown trees' split searches "
+                                        "executed (sr_last_work: first-pass adds + second-pass sub/mul/add per "
+                                        "candidate, DESIGN 5.11)" if args.learner == "m5"
                                         else "algorithmic flops of the fits, prediction (t d) counted in "
                                         "k_pred_rank's share when the split LS path runs (DESIGN 5.12, 6); "
                                         "step_* = all algorithmic flops over the whole step")},

@@ -279,6 +279,13 @@ int32_t sr_kernel_stats(sr_ctx* ctx, int32_t cap, const char** names, int32_t* l
 sr_status sr_reset_kernel_stats(sr_ctx* ctx); /* zero the accumulated counts and times */
 /* Kernels launched by the last sr_evaluate call. */
 int32_t sr_last_launch_count(const sr_ctx* ctx);
+/* Executed work of the last sr_evaluate with learner SR_M5P: the FP64
+ * operations of every split search the grown trees ran (P:151 model-tree
+ * induction, reading M1): per searched node and feature, m label additions of
+ * the first pass for every candidate row, 3m more for every scored candidate
+ * (+ 2m for a redone adjacent-double candidate).  0 for the other learners or
+ * before any M5P evaluate; synchronizes the context stream; < 0 on error. */
+int64_t sr_last_work(sr_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -328,6 +328,16 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
   const long long gwarp = (long long)blockIdx.x * A.warps_per_block + warp;
   const long long nwarps = (long long)gridDim.x * A.warps_per_block;
   double* scr = A.gscratch ? A.gscratch + gwarp * A.mscratch : nullptr;
+  // M5P teams (A.m5_team warps per fit): every member fits
+  // the same tree in its own slab, the split search is shared; only the lead
+  // warp writes outputs
+  const int tw = MODE == 3 ? A.m5_team : 1;
+  const int trank = warp % tw;
+  const bool lead = trank == 0;
+  const long long team = gwarp / tw, nteams = nwarps / tw;
+  __shared__ double m5x[3 * kMaxWarpsPerBlock];
+  unsigned long long m5ops = 0;           // executed split-search FP64 operations (this lane)
+  const M5Team m5t{tw, trank, 1 + warp / tw, m5x + 3 * (warp - trank), &m5ops};
   const int G = A.G, O = A.O, C = A.C;
   unsigned long long tot_corr = 0, tot_test = 0, tot_rec = 0, tot_hit = 0;
   // fused A6 (A.fuse_rank): the warp finishing the last scored fit of a
@@ -349,7 +359,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
   // list are formed once per scenario; fit-major (small, latency-bound
   // batches): one fit per work unit, spreading a scenario over warps
   const long long units = A.scn_major ? A.count : A.count * O;
-  for (long long u = gwarp; u < units; u += nwarps) {
+  for (long long u = team; u < units; u += nteams) {
   const long long sl = A.scn_major ? u : u / O;
   const int o_lo = A.scn_major ? 0 : (int)(u - sl * O), o_hi = A.scn_major ? O : o_lo + 1;
   const long long s = A.first + sl, so = A.out0 + sl;
@@ -377,7 +387,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     row.sum_ratio = row.min_ratio = row.max_ratio = 0.0;
     row.fp_train = row.fp_test = 0ull;
     if (!((om >> o) & 1u)) {
-      if (lane == 0 && A.opt_out) A.opt_out[so * O + o] = row;
+      if (lane == 0 && lead && A.opt_out) A.opt_out[so * O + o] = row;
       // no scored optimization at all: nothing will finish, rank (empty row) here
       if (MODE == 0 && A.fuse_rank && om == 0u && o == 0) rank_scenario<8>(A, sl, lane, true, tot_rec, tot_hit);
       continue;
@@ -423,7 +433,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     row.fp_train = warp_xor(fptr);
     row.fp_test = warp_xor(fpte);
     __syncwarp();
-    if (n > 0 && lane == 0 && MODE != 4) atomicOr(&A.trained[sl], 1u << o);
+    if (n > 0 && lane == 0 && lead && MODE != 4) atomicOr(&A.trained[sl], 1u << o);
     auto put_counts = [&](double flag) {   // MODE 4: the model-table row's fields after u, c0
       if (lane == 0) {
         double* e = urow + ((A.C + 3) & ~3);   // fields after the k-step-padded weights
@@ -441,8 +451,8 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
         put_counts(n > 0 ? 1.0 : 0.0);
         continue;
       }
-      if (lane == 0 && A.opt_out) A.opt_out[so * O + o] = row;
-      if (A.agg && lane == 0 && nt > 0) atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 1], nt);
+      if (lane == 0 && lead && A.opt_out) A.opt_out[so * O + o] = row;
+      if (A.agg && lane == 0 && lead && nt > 0) atomicAdd(&A.mask_acc[(fidx - A.mask0) * 4 + 1], nt);
       finish(sl, om);
       continue;
     }
@@ -593,8 +603,10 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
       rsum += ratio;
       rmin = fmin(rmin, ratio);
       rmax = fmax(rmax, ratio);
-      ext[test_group_index(A.sd, split, gk >> 5) * 32 + (gk & 31)] = cl ? -e : e;
-      if (A.ex_out) A.ex_out[(so * O + o) * (long long)G * 32 + gk] = e;
+      if (lead) {
+        ext[test_group_index(A.sd, split, gk >> 5) * 32 + (gk & 31)] = cl ? -e : e;
+        if (A.ex_out) A.ex_out[(so * O + o) * (long long)G * 32 + gk] = e;
+      }
     };
     if (m5) {    // NEXT-2: grow + prune the tree in the warp's scratch slab, then lanes over tests
       M5Work W = m5_carve(scr, L.np_tr, A.C);
@@ -606,7 +618,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
       __syncwarp();
       int tg = 0;
       bool tok = true;
-      m5_build(W, n, deff, yc, A.lambda, A.refine, A.guard_tol, lane, &tg, &tok);
+      m5_build(W, n, deff, yc, A.lambda, A.refine, A.guard_tol, lane, &tg, &tok, m5t);
       if (lane == 0) guard += tg + (tok ? 0 : 1000000);   // warp-uniform counts: once, not per lane
       for (int j = lane; j < nt; j += 32) score(j, m5_predict(W, X + (long long)tes[j] * ldx, col, uv, wv));
     } else if (ibk) {   // NEXT-1: IBk prediction, all lanes sweep together (knn_ex)
@@ -644,9 +656,11 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     row.max_ratio = warp_max(rmax);
     if (MODE == 2 && nt == 0) row.min_ratio = row.max_ratio = 0.0;   // fitted, nothing tested
     guard = warp_isum(guard);
-    tot_corr += row.n_correct;
-    tot_test += nt;
-    if (lane == 0) {
+    if (lead) {
+      tot_corr += row.n_correct;
+      tot_test += nt;
+    }
+    if (lane == 0 && lead) {
       if (A.opt_out) A.opt_out[so * O + o] = row;
       if (guard) atomicAdd(&A.guard_acc[sl], guard);
       if (A.agg) {
@@ -661,6 +675,10 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
   if (A.totals && lane == 0 && tot_test) {
     atomicAdd(&A.totals[0], tot_corr);
     atomicAdd(&A.totals[1], tot_test);
+  }
+  if (MODE == 3 && A.work) {                // every team member adds its own share of the search
+    const unsigned long long w = warp_usum(m5ops);
+    if (lane == 0 && w) atomicAdd(A.work, w);
   }
   if (A.totals && lane == 0 && (tot_rec | tot_hit)) {
     atomicAdd(&A.totals[2], tot_rec);

@@ -137,6 +137,8 @@ struct EvalArgs {
   int scn_major;         // k_fit_warp work unit: 1 = a whole scenario, 0 = one fit
   int stage_y;           // 1: the labels ylab [G][O][32] staged in shared memory at off_y
   int off_y;
+  int m5_team;           // M5P: warps per fit (1, 2 or 4; divides warps_per_block)
+  unsigned long long* work;    // M5P: executed split-search FP64 operations (sr_last_work), or null
 };
 // model-table row fields after the C weights (k_fit_warp MODE 4 / k_pred_rank)
 constexpr int kUc0 = 0, kUflag = 1, kUntr = 2, kUnte = 3, kUfptr = 4, kUfpte = 5, kUextra = 6;

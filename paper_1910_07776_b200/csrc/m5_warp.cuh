@@ -222,8 +222,25 @@ SR_UNROLL(SR_M5_UNROLL)
 #endif
 constexpr int kM5WideRows = SR_M5_WIDE_ROWS;   // A/B knob
 
+// A team of tw warps fitting the same tree (identical data in each warp's
+// slab): the split search's candidates are dealt round-robin over the team and
+// the best one is agreed through shared memory (xch: 3 doubles per warp of the
+// CTA, team members contiguous; named barrier bar_id over the team's threads).
+struct M5Team {
+  int tw, trank, bar_id;
+  double* xch;       // the team's first warp's slot
+  unsigned long long* ops;   // this lane's count of executed split-search FP64 operations
+};
+
+__device__ __forceinline__ void m5_team_sync(const M5Team& T) {
+  if (T.tw > 1) asm volatile("bar.sync %0, %1;" ::"r"(T.bar_id), "r"(T.tw * 32) : "memory");
+}
+
+// SOLO: a one-warp fit (stride-1 candidate loops, no team exchange).
+template <bool SOLO>
 __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const double* y, double sdT, int lane,
-                                int& ba, double& bt) {
+                                int& ba, double& bt, const M5Team& T) {
+  const int tr = SOLO ? 0 : T.trank, ts = SOLO ? 1 : T.tw;
   double bs = -INFINITY;
   ba = 0x7fffffff;
   bt = INFINITY;
@@ -237,9 +254,11 @@ __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const
     const int ld = W.ld;
     if (m <= kM5WideRows) {
       #pragma unroll 1
-      for (int j = 0; j < m; ++j) {
+      for (int j = tr; j < m; j += ts) {
         double sdr, thr;
-        if (m5_candidate(xa, ld, yv, m, j, frac, sdT, sdr, thr) && m5_better(sdr, a, thr, bs, ba, bt)) {
+        const bool cand = m5_candidate(xa, ld, yv, m, j, frac, sdT, sdr, thr);
+        *T.ops += (unsigned long long)(cand ? 4 * m : m);   // first pass m adds; a candidate's second 3m
+        if (cand && m5_better(sdr, a, thr, bs, ba, bt)) {
           bs = sdr;
           ba = a;
           bt = thr;
@@ -248,8 +267,9 @@ __device__ double m5_best_split(const M5Work& W, int lo, int hi, int deff, const
       continue;
     }
     #pragma unroll 1
-    for (int j = 0; j < m; j += 2) {
+    for (int j = 2 * tr; j < m; j += 2 * ts) {
       const bool two = j + 1 < m;
+      *T.ops += (unsigned long long)(2 * m);       // the fused first pass of rows j, j + 1
       const double u0 = xa[j * ld], u1 = two ? xa[(j + 1) * ld] : INFINITY;
       bool d0 = false, d1 = false;
       double n0 = INFINITY, n1 = INFINITY, sL0 = 0.0, sR0 = 0.0, sL1 = 0.0, sR1 = 0.0;
@@ -277,8 +297,11 @@ SR_UNROLL(SR_M5_UNROLL)
         double thr = __dmul_rn(__dadd_rn(u, nx), 0.5), sdr;
         if (thr < nx) {
           sdr = m5_score(xa, ld, yv, m, u, c ? sL1 : sL0, c ? sR1 : sR0, c ? nL1 : nL0, frac, sdT);
+          *T.ops += (unsigned long long)(3 * m);
         } else if (!m5_candidate(xa, ld, yv, m, j + c, frac, sdT, sdr, thr)) {
           continue;
+        } else {
+          *T.ops += (unsigned long long)(5 * m);   // redo pass (m) + first (m) + second (3m)
         }
         if (m5_better(sdr, a, thr, bs, ba, bt)) {
           bs = sdr;
@@ -297,6 +320,24 @@ SR_UNROLL(SR_M5_UNROLL)
       ba = oa;
       bt = ot;
     }
+  }
+  if (!SOLO) {      // agree on the team's best candidate (same total order: any split of the work)
+    if (lane == 0) {
+      T.xch[3 * T.trank + 0] = bs;
+      T.xch[3 * T.trank + 1] = (double)ba;
+      T.xch[3 * T.trank + 2] = bt;
+    }
+    m5_team_sync(T);
+    for (int r = 0; r < T.tw; ++r) {
+      const double os = T.xch[3 * r + 0], ot = T.xch[3 * r + 2];
+      const int oa = (int)T.xch[3 * r + 1];
+      if (m5_better(os, oa, ot, bs, ba, bt)) {
+        bs = os;
+        ba = oa;
+        bt = ot;
+      }
+    }
+    m5_team_sync(T);   // the slots are free again
   }
   return bs;
 }
@@ -446,7 +487,7 @@ __device__ bool m5_node_fit(const M5Work& W, int lo, int hi, unsigned long long 
 // gets the pruning decisions within tol of their boundary; *ok false if a
 // node factorisation broke down.
 __device__ int m5_build(const M5Work& W, int n, int deff, double* y, double lambda, int nref, double tol,
-                        int lane, int* guard, bool* ok) {
+                        int lane, int* guard, bool* ok, const M5Team& T) {
   if (lane == 0) {
     W.nlo[0] = 0;
     W.nhi[0] = n;
@@ -464,7 +505,9 @@ __device__ int m5_build(const M5Work& W, int n, int deff, double* y, double lamb
     double bt = 0.0;
     if (hi - lo >= kM5MinSplit) {
       const double sdT = m5_sd(lo, hi, y);
-      if (!(sdT < sd_min)) split = m5_best_split(W, lo, hi, deff, y, sdT, lane, ba, bt) > 0.0;
+      if (!(sdT < sd_min))
+        split = (T.tw == 1 ? m5_best_split<true>(W, lo, hi, deff, y, sdT, lane, ba, bt, T)
+                           : m5_best_split<false>(W, lo, hi, deff, y, sdT, lane, ba, bt, T)) > 0.0;
     }
     if (split) {
       const int nL = m5_partition(W, lo, hi, ba, bt, y, lane);

@@ -90,6 +90,7 @@ struct sr_ctx {
   DevBuf sw_buf;
   DevBuf extab, trained, guard_acc, mask_acc, done;   // fit -> rank exchange (warp path)
   DevBuf utab;                                        // fit -> k_pred_rank model table (split LS path)
+  DevBuf work;                                        // M5P executed split-search operations (sr_last_work)
   // accounting
   bool timing = false;
   std::vector<KStat> kstats;
@@ -268,7 +269,7 @@ void sr_destroy(sr_ctx* c) {
                     &c->big_flag, &c->extab, &c->trained, &c->guard_acc, &c->mask_acc, &c->done, &c->fit_coef,
                     &c->mp_G, &c->mp_r, &c->mp_z, &c->mp_meta, &c->mp_perm, &c->mp_rec, &c->mp_order,
                     &c->mp_units, &c->mp_pfx, &c->mp_glist, &c->sw_buf, &c->ibk_lists, &c->ibk_xs, &c->ibk_meta,
-                    &c->utab})
+                    &c->utab, &c->work})
     release(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->cp_events) cudaEventDestroy(e);
@@ -1172,6 +1173,11 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     return st;
   }
   A.utab = (double*)c->utab.p;
+  if (prm->learner == SR_M5P) {
+    if ((st = ensure(c, c->work, 8))) return st;
+    CU(cudaMemsetAsync(c->work.p, 0, 8, c->stream));
+    A.work = (unsigned long long*)c->work.p;
+  }
   A.ldu = ldu;
   A.n_os = c->n_os;
   A.extab = (double*)c->extab.p;
@@ -1269,7 +1275,18 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
     // whole scenarios per warp once the chunk has >= 4 scenarios per resident warp
     A.scn_major = cc >= 4 * max_fit_blocks * wpb ? 1 : 0;
     const long long units = A.scn_major ? cc : cc * O;
-    const long long fblocks = std::max(1LL, std::min(max_fit_blocks, (units + wpb - 1) / wpb));
+    // M5P teams: when the fits leave warps idle, 2 or 4 warps share each
+    // fit's split search; SPEEDREC_M5_TEAM forces 1/2/4
+    A.m5_team = 1;
+    if (prm->learner == SR_M5P) {
+      // teams of 2 once the work units (many of them cheap: unscored or small
+      // fits) no longer fill the warps 1.25 times (C2: 9.4 -> 7.8 ms; teams of
+      // 4 and teams on C3 are slower, profiles/r3i_ab_m5team.txt)
+      if (units * 4 <= 5 * max_fit_blocks * wpb) A.m5_team = 2;
+      if (const char* e = getenv("SPEEDREC_M5_TEAM")) A.m5_team = atoi(e) >= 4 ? 4 : atoi(e) >= 2 ? 2 : 1;
+      if (wpb % A.m5_team) A.m5_team = 1;
+    }
+    const long long fblocks = std::max(1LL, std::min(max_fit_blocks, (units * A.m5_team + wpb - 1) / wpb));
     if ((st = launch(c, "k_fit_warp", [&] { kfit<<<(unsigned)fblocks, wpb * 32, smem, c->stream>>>(A); }))) return st;
     if (split_ls) {
       const int ks = (C + 3) / 4;
@@ -1551,5 +1568,18 @@ sr_status sr_reset_kernel_stats(sr_ctx* c) {
 }
 
 int32_t sr_last_launch_count(const sr_ctx* c) { return c ? c->last_launches : (int32_t)SR_E_ARG; }
+
+int64_t sr_last_work(sr_ctx* c) {
+  if (!c) return (int64_t)SR_E_ARG;
+  if (!c->work.p) return 0;
+  cudaSetDevice(c->device);
+  unsigned long long w = 0;
+  if (cudaMemcpyAsync(&w, c->work.p, 8, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return (int64_t)SR_E_CUDA;
+  }
+  return (int64_t)w;
+}
 
 }  // extern "C"

@@ -72,7 +72,7 @@ MASK_SCORE_DTYPE = np.dtype([("n_correct", "<i4"), ("n_test", "<i4"), ("n_rec", 
 EXPORTS = ["sr_create", "sr_destroy", "sr_last_error", "sr_version", "sr_load_dataset",
            "sr_define_scenarios", "sr_default_params", "sr_evaluate", "sr_rates", "sr_synchronize",
            "sr_set_timing", "sr_kernel_stats", "sr_reset_kernel_stats", "sr_last_launch_count",
-           "sr_fit", "sr_predict", "sr_recommend", "sr_sweep"]
+           "sr_fit", "sr_predict", "sr_recommend", "sr_sweep", "sr_last_work"]
 
 _lib = None
 
@@ -113,6 +113,8 @@ def lib() -> ct.CDLL:
         L.sr_reset_kernel_stats.restype = ct.c_int32
         L.sr_last_launch_count.argtypes = [ct.c_void_p]
         L.sr_last_launch_count.restype = ct.c_int32
+        L.sr_last_work.argtypes = [ct.c_void_p]
+        L.sr_last_work.restype = ct.c_int64
         L.sr_fit.argtypes = [ct.c_void_p, ct.POINTER(sr_params), ct.c_int64, ct.c_void_p]
         L.sr_sweep.argtypes = [ct.c_void_p, ct.POINTER(sr_params), ct.c_int64, ct.c_int64, ct.c_int32, ct.c_void_p,
                                ct.c_int32, ct.c_void_p, ct.c_void_p, ct.c_void_p]
@@ -316,6 +318,10 @@ class Context:
 
     def last_launch_count(self) -> int:
         return int(lib().sr_last_launch_count(self._h))
+
+    def last_work(self) -> int:
+        """sr_last_work: executed M5P split-search FP64 operations of the last evaluate."""
+        return int(lib().sr_last_work(self._h))
 
 
 def predict(coef: np.ndarray, counters: np.ndarray, cycles: float, params: Optional[sr_params] = None) -> np.ndarray:
