@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
   // list are formed once per scenario; fit-major (small, latency-bound
   // batches): one fit per work unit, spreading a scenario over warps
   const long long units = A.scn_major ? A.count : A.count * O;
+  if (MODE == 4) SR_WT(-1);
   for (long long u = team; u < units; u += nteams) {
   const long long sl = A.scn_major ? u : u / O;
   const int o_lo = A.scn_major ? 0 : (int)(u - sl * O), o_hi = A.scn_major ? O : o_lo + 1;
@@ -381,6 +382,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     d += __popc(bm);
   }
   __syncwarp();
+  if (MODE == 4) SR_WT(0);
   for (int o = o_lo; o < o_hi; ++o) {
     OptScore row;
     row.n_train = row.n_test = row.n_correct = row.n_clamped = 0;
@@ -433,6 +435,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     row.fp_train = warp_xor(fptr);
     row.fp_test = warp_xor(fpte);
     __syncwarp();
+    if (MODE == 4) SR_WT(1);
     if (n > 0 && lane == 0 && lead && MODE != 4) atomicOr(&A.trained[sl], 1u << o);
     auto put_counts = [&](double flag) {   // MODE 4: the model-table row's fields after u, c0
       if (lane == 0) {
@@ -449,6 +452,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     if (n == 0 || (nt == 0 && MODE != 2)) {
       if (MODE == 4) {
         put_counts(n > 0 ? 1.0 : 0.0);
+        SR_WT(7);
         continue;
       }
       if (lane == 0 && lead && A.opt_out) A.opt_out[so * O + o] = row;
@@ -535,6 +539,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
         sv[p] = 0.0;
       }
     }
+    if (MODE == 4) SR_WT(2);
     double c0 = 0.0;
     bool ok = true;
     if (!ibk && !m5) {
@@ -580,6 +585,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
         for (int c = lane; c < Cp; c += 32) urow[c] = c < C ? ufull[c] : 0.0;
         if (lane == 0) urow[Cp + kUc0] = c0;
         put_counts(ok ? 1.0 : 2.0);
+        SR_WT(7);
         continue;
       }
     }
@@ -676,6 +682,13 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     atomicAdd(&A.totals[0], tot_corr);
     atomicAdd(&A.totals[1], tot_test);
   }
+#if SR_WARP_TIMING
+  if (MODE == 4 && blockIdx.x == 0 && lane == 0) {
+    const long long* a = sr_wt_acc[warp];
+    printf("SR_WT warp %d: setup %lld pairs %lld stats %lld gram %lld chol %lld solve %lld xta %lld out %lld\n", warp,
+           a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]);
+  }
+#endif
   if (MODE == 3 && A.work) {                // every team member adds its own share of the search
     const unsigned long long w = warp_usum(m5ops);
     if (lane == 0 && w) atomicAdd(A.work, w);

@@ -181,6 +181,55 @@ __device__ SR_FAST_FN double solve_rl(const double* M, int m, int lane, double m
 // On exit M holds L (scaled); myinv = 1/L_{lane,lane}.
 // aug: row m holds a right-hand side b (m < 32); the same column steps turn it
 // into y = L^-1 b (forward substitution fused into the factorisation).
+#ifndef SPEEDREC_CHOL_BLK
+#define SPEEDREC_CHOL_BLK 1
+#endif
+#ifndef SPEEDREC_CHOL_PAR
+#define SPEEDREC_CHOL_PAR 0
+#endif
+#ifndef SPEEDREC_SOLVE_PAR
+#define SPEEDREC_SOLVE_PAR 0
+#endif
+// Trailing update of chol_ll's blocked form after the 8-column panel
+// [P-8, P): M[r][c] -= sum_{k in panel} L_rk L_ck for P <= c <= r, r < mr,
+// c < m, as 8x8 DMMA tiles (two k-steps of 4; the B fragment of tile (I, J)
+// is block-row J's A fragment, L L^T being symmetric).  Replaces the panel's
+// terms in every later column's row-prefix sum.
+__device__ SR_FAST_FN void chol_trail(double* M, int P, int m, int mr, int lane) {
+  const int rl = lane >> 2, kl = lane & 3;
+  const int I0 = P >> 3, nbr = (mr + 7) >> 3, nbc = (m + 7) >> 3;
+  double f0[4], f1[4];
+#pragma unroll
+  for (int I = 0; I < 4; ++I) {
+    const int r = I * 8 + rl;
+    f0[I] = f1[I] = 0.0;
+    if (I >= I0 && I < nbr && r < mr) {
+      const double* rp = M + rb2(r) + P - 8 + kl;
+      f0[I] = rp[0];
+      f1[I] = rp[4];
+    }
+  }
+#pragma unroll
+  for (int I = 1; I < 4; ++I) {
+    if (I < I0 || I >= nbr) continue;
+    const int r = I * 8 + rl;
+    double* rowp = M + rb2(r < mr ? r : 0);
+#pragma unroll
+    for (int J = 1; J <= I; ++J) {
+      if (J < I0 || J >= nbc) continue;
+      const int c = J * 8 + 2 * kl;
+      const bool in = r < mr && c <= r;           // then c + 1 is inside row r's padded length
+      const double2 cv = in ? *reinterpret_cast<const double2*>(rowp + c) : make_double2(0.0, 0.0);
+      double d0 = cv.x, d1 = cv.y;
+      dmma(d0, d1, -f0[I], f0[J]);
+      dmma(d0, d1, -f1[I], f1[J]);
+      if (in && c < m) rowp[c] = d0;
+      if (in && c + 1 <= r && c + 1 < m) rowp[c + 1] = d1;
+    }
+  }
+  __syncwarp();
+}
+
 __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv, bool aug = false) {
   myinv = 0.0;
   const int mr = m + (aug ? 1 : 0);               // rows carried through the column steps
@@ -188,13 +237,22 @@ __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv, bo
   const double* rj = M;                           // row j (j even), advanced two rows per step
   // two columns per step: the row-prefix sums over k < j for columns j and
   // j+1 share the loads of row i; column j+1 then takes the k = j term with
-  // L_{j+1,j} from lane j+1.  One __syncwarp per two pivots.
+  // L_{j+1,j} from lane j+1.  One __syncwarp per two pivots.  Blocked form
+  // (SPEEDREC_CHOL_BLK): at every 8-column boundary the finished panel is
+  // subtracted from the trailing matrix on DMMA (chol_trail), so the prefix
+  // sums run over the current panel's columns only (<= 6 terms).
   #pragma unroll 1
   for (int j = 0; j < m; j += 2) {
     const double* rj1 = j + 1 < m ? rj + j + 2 : rj;   // row j+1 (row j has padded length j+2)
     double s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
+#if SPEEDREC_CHOL_BLK
+    const int kb = j & ~7;
+    if (kb == j && j > 0) chol_trail(M, j, m, mr, lane);
+#else
+    const int kb = 0;
+#endif
     SR_UNROLL(SR_UNROLL_CHOL)
-    for (int k = 0; k < j; k += 2) {              // j even: pairs cover k < j exactly
+    for (int k = kb; k < j; k += 2) {              // j even: pairs cover [kb, j) exactly
       const double2 a = *reinterpret_cast<const double2*>(ri + k);
       const double2 b = *reinterpret_cast<const double2*>(rj + k);
       const double2 c = *reinterpret_cast<const double2*>(rj1 + k);
@@ -207,6 +265,27 @@ __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv, bo
     // 0) read nothing: lane 0 writes row 0 in this step (racecheck-clean)
     const double2 kij = lane < mr ? *reinterpret_cast<const double2*>(ri + j) : make_double2(0.0, 0.0);
     const double v = kij.x - (s0 + s1);           // lane j: pivot; lanes i > j: unscaled L_ij
+#if SPEEDREC_CHOL_PAR
+    // both pivots of the step from one round of broadcasts: with p_j = v_j,
+    // w = v_{j+1,j} and K' = K'_{j+1,j+1} (row-prefix sums applied), the next
+    // pivot is p_{j+1} = K' - w^2 / p_j, so 1/L_{j+1,j+1} = rsqrt(K' p_j - w^2)
+    // * sqrt(p_j) = rsqrt(K' p_j - w^2) * p_j / L_jj: the two rsqrt chains
+    // run side by side instead of one after the other
+    const double vj = __shfl_sync(FULL, v, j);
+    const double r = rsqrt_nr(vj);                // 1/L_jj in every lane (NaN/inf iff p_j is not > 0)
+    const double lij = v * r;
+    if (lane >= j && lane < mr) ri[j] = lij;
+    if (lane == j) myinv = r;
+    if (j + 1 < m) {
+      const double kp = kij.y - (t0 + t1);        // lane i: K'_{i,j+1}
+      const double w = __shfl_sync(FULL, v, j + 1);
+      const double kp1 = __shfl_sync(FULL, kp, j + 1);
+      const double r1 = rsqrt_nr(fma(kp1, vj, -(w * w))) * (vj * r);
+      const double v1 = kp - lij * (w * r);       // lane j+1: pivot; lanes i > j+1: unscaled L_i,j+1
+      if (lane > j && lane < mr) ri[j + 1] = v1 * r1;
+      if (lane == j + 1) myinv = r1;
+    }
+#else
     const double r = __shfl_sync(FULL, rsqrt_nr(v), j);  // 1/L_jj (NaN/inf iff the pivot is not > 0)
     const double lij = v * r;
     if (lane >= j && lane < mr) ri[j] = lij;
@@ -218,6 +297,7 @@ __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv, bo
       if (lane > j && lane < mr) ri[j + 1] = v1 * r1;
       if (lane == j + 1) myinv = r1;
     }
+#endif
     rj += 2 * j + 4;                              // row j+2 (rows j, j+1 have padded length j+2)
     __syncwarp();
   }
@@ -228,6 +308,29 @@ __device__ SR_FAST_FN bool chol_ll(double* M, int m, int lane, double& myinv, bo
 
 // z <- L^{-T} z for the chol_ll factor; z lane-owned, m <= 32.
 __device__ SR_FAST_FN double solve_bwd(const double* M, int m, int lane, double myinv, double z) {
+#if SPEEDREC_SOLVE_PAR
+  // two unknowns per step from one round of broadcasts: x_j = z_j / L_jj and
+  // x_{j-1} = (z_{j-1} - L_{j,j-1} x_j) / L_{j-1,j-1} in every lane, then
+  // lanes i < j-1 take both updates (the 1/L_jj broadcasts and L_{j,j-1}
+  // do not depend on z, so they leave the dependency chain)
+  int j = m - 1;
+  #pragma unroll 1
+  for (; j >= 1; j -= 2) {
+    const double* rj = M + rb2(j);
+    const double* rj1 = M + rb2(j - 1);
+    const double ij = __shfl_sync(FULL, myinv, j), ij1 = __shfl_sync(FULL, myinv, j - 1);
+    const double ljj1 = rj[j - 1];
+    const double lji = lane < j - 1 ? rj[lane] : 0.0, lj1i = lane < j - 1 ? rj1[lane] : 0.0;
+    const double zj = __shfl_sync(FULL, z, j), zj1 = __shfl_sync(FULL, z, j - 1);
+    const double xj = zj * ij;
+    const double xj1 = fma(-ljj1, xj, zj1) * ij1;
+    if (lane < j - 1) z = fma(-lj1i, xj1, fma(-lji, xj, z));
+    if (lane == j) z = xj;
+    if (lane == j - 1) z = xj1;
+  }
+  if (j == 0 && lane == 0) z *= myinv;
+  return z;
+#endif
   const double* rj = M + rb2(m - 1) + lane;         // row j, column `lane`
   #pragma unroll 1
   for (int j = m - 1; j >= 0; --j) {                // backward: L^T x = y
@@ -294,6 +397,7 @@ __device__ SR_FAST_FN bool fit_fast(const FastView& f, const double* yc, double 
                          double* scratch, double* uwork, double* wout, int lane, int mcap) {
   const int m = DUAL ? f.n : f.deff;
   gram_fast<DUAL, SX>(f, m, lambda, Mpk, lane);
+  SR_WT(3);
   double myinv;
 #if SPEEDREC_CHOL_RL
   const bool aug = false;
@@ -305,6 +409,7 @@ __device__ SR_FAST_FN bool fit_fast(const FastView& f, const double* yc, double 
     __syncwarp();
   }
   const bool ok = chol_ll(Mpk, m, lane, myinv, aug);
+  SR_WT(4);
   if (DUAL) {
     double alpha = lane < f.n ? (aug ? Mpk[rb2(m) + lane] : yc[lane]) : 0.0;
     alpha = aug ? solve_bwd(Mpk, m, lane, myinv, alpha) : solve_ll(Mpk, m, lane, myinv, alpha);
@@ -317,7 +422,9 @@ __device__ SR_FAST_FN bool fit_fast(const FastView& f, const double* yc, double 
       alpha += solve_ll(Mpk, m, lane, myinv, e);
       __syncwarp();
     }
+    SR_WT(5);
     xt_alpha_lanes<SX>(f, alpha, wout, lane, scratch);
+    SR_WT(6);
   } else {
     // rhs_a = s_a * sum_i (x_ia - xb_a) * yc_i, lane a < deff <= 32
     double w = 0.0;

@@ -256,6 +256,25 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 #define SR_UNROLL_XTA 2
 #endif
 
+// Instrumented build (-DSR_WARP_TIMING=1): k_fit_warp MODE 4 charges the
+// cycles between consecutive SR_WT(k) marks to phase k, per warp (lane 0);
+// CTA 0 prints its warps' totals at exit.  Timing only, never a bench build.
+#if SR_WARP_TIMING
+__device__ long long sr_wt_acc[148 * 32][8];
+__device__ long long sr_wt_last[148 * 32];
+__device__ __forceinline__ void sr_wt(int k) {
+  if ((threadIdx.x & 31) == 0) {
+    const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const long long now = clock64();
+    if (k >= 0) sr_wt_acc[w][k] += now - sr_wt_last[w];
+    sr_wt_last[w] = now;
+  }
+}
+#define SR_WT(k) sr_wt(k)
+#else
+#define SR_WT(k)
+#endif
+
 // min / max of non-NaN doubles: one compare + select (fmin/fmax add NaN handling)
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
