@@ -43,6 +43,12 @@ constexpr int kRecR = kSchurQ, kRecZ = kSchurQ + kSchurU, kRecBase = kSchurQ + 2
 #define SPEEDREC_SFIT_THREADS 256
 #endif
 constexpr int kSfitThreads = SPEEDREC_SFIT_THREADS;
+#ifndef SPEEDREC_SFIT_NBUF         // record buffers of the staged fold loop
+#define SPEEDREC_SFIT_NBUF 3
+#endif
+#ifndef SPEEDREC_SFIT_ILP_D        // suffix sizes below this let the compiler interleave optimisations
+#define SPEEDREC_SFIT_ILP_D 0
+#endif
 #ifndef SPEEDREC_SFIT_SCHED        // A/B knob: register budget schedule of k_mask_sfit<D>
 #define SPEEDREC_SFIT_SCHED 0
 #endif
@@ -326,8 +332,9 @@ __global__ void __launch_bounds__(kSfitThreads, SPEEDREC_SFIT_MINB(D)) k_mask_sf
   // through L1 (__ldg).
   // up to two prefix groups per CTA (a CTA of 256 sorted masks spans at most
   // two groups for suffix sizes 3..7, the large launches)
-  __shared__ __align__(16) double srec[2][2][kSfitMaxO * kRec];
-  __shared__ __align__(8) uint64_t sbar[2];
+  constexpr int NB = SPEEDREC_SFIT_NBUF;            // fold buffers (prefetch distance NB - 1)
+  __shared__ __align__(16) double srec[NB][2][kSfitMaxO * kRec];
+  __shared__ __align__(8) uint64_t sbar[NB];
   const int i0 = blockIdx.x * blockDim.x, ilast = min(i0 + (int)blockDim.x, n_items) - 1;
   const int g0 = i0 < n_items ? SA.group[off + i0] : 0, g1 = i0 < n_items ? SA.group[off + ilast] : 0;
   const bool staged = fold_chunks == 1 && i0 < n_items && g1 - g0 <= 1;
@@ -361,7 +368,9 @@ __global__ void __launch_bounds__(kSfitThreads, SPEEDREC_SFIT_MINB(D)) k_mask_sf
       cv[o] = cc[o] = false;
       ce[o] = 0.0;
       if (o >= O) continue;
-      asm volatile("" ::: "memory");   // one optimisation at a time: no load hoisting across them
+      // one optimisation at a time (no load hoisting across them) for the larger
+      // systems; the small ones may interleave two fits' pivot chains
+      if (D >= SPEEDREC_SFIT_ILP_D) asm volatile("" ::: "memory");
       const PrepMeta& pm = M.pm[split * O + o];
       OptScore row;
       row.n_train = row.n_test = row.n_correct = row.n_clamped = 0;
@@ -457,20 +466,20 @@ __global__ void __launch_bounds__(kSfitThreads, SPEEDREC_SFIT_MINB(D)) k_mask_sf
       for (int q = 0; q < ng; ++q) bulk_g2s_tx(srec[b][q], gsrc + q * gstride + (long long)split * O * kRec, bytes, &sbar[b]);
     };
     if (threadIdx.x == 0) {
-      mbar_init(&sbar[0], 1);
-      mbar_init(&sbar[1], 1);
+      for (int q = 0; q < NB; ++q) mbar_init(&sbar[q], 1);
       fence_mbar_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0) issue(0, 0);
+    if (threadIdx.x == 0)
+      for (int q = 0; q < NB - 1 && q < S; ++q) issue(q, q);
     unsigned phase = 0u;
     const int mine = grp - g0;
     #pragma unroll 1
     for (int split = 0; split < (int)S; ++split) {
-      const int b = split & 1;
-      if (threadIdx.x == 0 && split + 1 < S) {      // next fold (buffer b^1 freed by the last barrier)
+      const int b = split % NB;
+      if (threadIdx.x == 0 && split + NB - 1 < S) {  // fold split+NB-1 (its buffer was freed by the last barrier)
         fence_proxy_async();
-        issue(split + 1, b ^ 1);
+        issue(split + NB - 1, (split + NB - 1) % NB);
       }
       mbar_wait(&sbar[b], (phase >> b) & 1u);
       phase ^= 1u << b;

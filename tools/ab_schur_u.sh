@@ -1,3 +1,6 @@
+#!/bin/bash
+# A/B harness of the (not kept) SPEEDREC_SCHUR_U knob, profiles/r4c_ab_schur_u.txt; the knob is gone,
+# so today every U runs the default split.
 B="--config C5 --masks-k 20 --steps 5 --warmup 2 --no-e2e --no-extra --no-cpu-baseline"
 for u in 10 9 8; do
   SPEEDREC_SCHUR_U=$u python -m pytest tests/test_gpu_parity.py -k c5 -x -q 2>&1 | tail -1
