@@ -19,6 +19,12 @@
 namespace speedrec {
 
 constexpr int kBigThreads = 256;
+#ifndef SPEEDREC_GRAM_SHIFT        // 1: Gram in coordinates shifted by the first training row; 0: raw
+#define SPEEDREC_GRAM_SHIFT 1
+#endif
+#ifndef SPEEDREC_GRAM_EXPERIMENT   // timing probes of the Gram pass (1 no statistics, 2 no barrier, 3 no shift, 4 no min/max): wrong results
+#define SPEEDREC_GRAM_EXPERIMENT 0
+#endif
 constexpr int kBigChunk = 32;   // training rows per refinement chunk (8 k-steps)
 #ifndef SPEEDREC_GRAM_CHUNK
 #define SPEEDREC_GRAM_CHUNK 32
@@ -346,7 +352,11 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       for (int J = 0; J < 8; ++J) accU[J][0] = accU[J][1] = accS[J][0] = accS[J][1] = 0.0;
       const int fa = t & (kBigMaxD - 1), fh = t >> 7;
       const bool fin = fa < d;
+#if SPEEDREC_GRAM_SHIFT
       const double cshift = fin ? A.x[(long long)trs[0] * C + Fl[fa]] : 0.0;
+#else
+      const double cshift = 0.0;            // raw coordinates: no in-place shift pass
+#endif
       double pmn = INFINITY, pmx = -INFINITY, psm = 0.0, prh = 0.0;
       double* ring = Gbuf;                                  // [3][kGramChunk][kBigLd] (spills into the free rch space)
       double* yring = rpt;                                  // [3][kGramChunk] centred labels of the stage rows
@@ -407,13 +417,20 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
           const bool live = fin && cc * kGramChunk + r < n;
           double xv = st[r * kBigLd + fa];
           if (live) {                 // rates: finite, >= 0 (validated): no NaN handling
+#if SPEEDREC_GRAM_EXPERIMENT != 4
             pmn = dmin(pmn, xv);
             pmx = dmax(pmx, xv);
+#endif
             psm += xv;
           }
+#if SPEEDREC_GRAM_EXPERIMENT == 3 || !SPEEDREC_GRAM_SHIFT     // no in-place shift (raw coordinates)
+          if (!live) xv = 0.0;
+          prh = fma(xv, ys[r], prh);
+#else
           xv = live ? xv - cshift : 0.0;
           if (fin) st[r * kBigLd + fa] = xv;
           prh = fma(xv, ys[r], prh);
+#endif
         }
       };
       issue(0, gslot(0, crow), gslot(0, crow + 32));
@@ -428,8 +445,13 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       // iteration ch: contract chunk ch on DMMA while the same warps fold and
       // shift chunk ch+1 (two rows per k-step); one barrier per chunk
       for (int ch = 0; ch < nchunks; ++ch) {
+#if SPEEDREC_GRAM_EXPERIMENT == 2     // timing probe only (wrong results): no per-chunk barrier
+        cp_wait<0>();
+        if (ch == 0) __syncthreads();
+#else
         cp_wait<0>();                                       // this thread's copies of chunk ch+1 landed
         __syncthreads();                                    // chunk ch shifted, ch+1 visible, ch-1 free
+#endif
         if (ch + 2 < nchunks) {
           issue(ch + 2, slot_pf, slot_pf2);
           slot_pf = gslot(ch + 3, crow);
@@ -440,7 +462,11 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
         const bool nxt = ch + 1 < nchunks;
 #pragma unroll
         for (int k0 = 0; k0 < kGramChunk; k0 += 4) {
+#if SPEEDREC_GRAM_EXPERIMENT == 1     // timing probe only (wrong results): no statistics pass
+          (void)nxt;
+#else
           if (nxt) shift_rows(ch + 1, k0 / 2, k0 / 2 + 2);
+#endif
           const double* base = cur + (k0 + kl) * kBigLd + rl;
           double f[16];
 #pragma unroll
