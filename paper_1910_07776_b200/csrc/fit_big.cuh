@@ -19,7 +19,10 @@
 namespace speedrec {
 
 constexpr int kBigThreads = 256;
-#ifndef SPEEDREC_GRAM_SHIFT        // 1: Gram in coordinates shifted by the first training row; 0: raw
+#ifndef SPEEDREC_GRAM_FRAGSTATS    // 1: D3 statistics from the warps' own DMMA A fragments (raw coordinates)
+#define SPEEDREC_GRAM_FRAGSTATS 1
+#endif
+#ifndef SPEEDREC_GRAM_SHIFT        // FRAGSTATS 0 only: 1 Gram shifted by the first training row (in place), 0 raw
 #define SPEEDREC_GRAM_SHIFT 1
 #endif
 #ifndef SPEEDREC_GRAM_EXPERIMENT   // timing probes of the Gram pass (1 no statistics, 2 no barrier, 3 no shift, 4 no min/max): wrong results
@@ -352,12 +355,18 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       for (int J = 0; J < 8; ++J) accU[J][0] = accU[J][1] = accS[J][0] = accS[J][1] = 0.0;
       const int fa = t & (kBigMaxD - 1), fh = t >> 7;
       const bool fin = fa < d;
-#if SPEEDREC_GRAM_SHIFT
+#if SPEEDREC_GRAM_SHIFT && !SPEEDREC_GRAM_FRAGSTATS
       const double cshift = fin ? A.x[(long long)trs[0] * C + Fl[fa]] : 0.0;
 #else
       const double cshift = 0.0;            // raw coordinates: no in-place shift pass
 #endif
       double pmn = INFINITY, pmx = -INFINITY, psm = 0.0, prh = 0.0;
+#if SPEEDREC_GRAM_FRAGSTATS
+      // lane (rl, kl) of warp w folds rows = kl (mod 4) of features I1*8+rl and
+      // I2*8+rl (its A fragments) into min / max / sum / sum x y~; the quads
+      // combine them after the pass (fixed order)
+      double qmn = INFINITY, qmx = -INFINITY, qsm = 0.0, qrh = 0.0;
+#endif
       double* ring = Gbuf;                                  // [3][kGramChunk][kBigLd] (spills into the free rch space)
       double* yring = rpt;                                  // [3][kGramChunk] centred labels of the stage rows
       const int nchunks = (n + kGramChunk - 1) / kGramChunk;
@@ -440,7 +449,9 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       int slot_pf = gslot(2, crow), slot_pf2 = gslot(2, crow + 32);
       cp_wait<1>();
       __syncthreads();
+#if !SPEEDREC_GRAM_FRAGSTATS
       shift_rows(0, 0, kGramChunk / 2);
+#endif
       const int rl = lane >> 2, kl = lane & 3;
       // iteration ch: contract chunk ch on DMMA while the same warps fold and
       // shift chunk ch+1 (two rows per k-step); one barrier per chunk
@@ -462,7 +473,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
         const bool nxt = ch + 1 < nchunks;
 #pragma unroll
         for (int k0 = 0; k0 < kGramChunk; k0 += 4) {
-#if SPEEDREC_GRAM_EXPERIMENT == 1     // timing probe only (wrong results): no statistics pass
+#if SPEEDREC_GRAM_EXPERIMENT == 1 || SPEEDREC_GRAM_FRAGSTATS     // (1: timing probe only, wrong results)
           (void)nxt;
 #else
           if (nxt) shift_rows(ch + 1, k0 / 2, k0 / 2 + 2);
@@ -480,9 +491,52 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
             dmma(accS[J][0], accS[J][1], lo ? fa1 : fa2, lo ? f[J] : f[15 - J]);
           }
           dmma(accX[0], accX[1], fa2, fa2);
+#if SPEEDREC_GRAM_FRAGSTATS
+          {   // rows past n and features past d are zero-filled: they add exact zeros to the sums
+            const double yv = yring[(ch % 3) * kGramChunk + k0 + kl];
+            if (ch * kGramChunk + k0 + kl < n) {   // rates: finite, >= 0 (validated): no NaN handling
+              pmn = dmin(pmn, fa1);
+              pmx = dmax(pmx, fa1);
+              qmn = dmin(qmn, fa2);
+              qmx = dmax(qmx, fa2);
+            }
+            psm += fa1;
+            qsm += fa2;
+            prh = fma(fa1, yv, prh);
+            qrh = fma(fa2, yv, qrh);
+          }
+#endif
         }
       }
       cp_wait<0>();
+#if SPEEDREC_GRAM_FRAGSTATS
+#pragma unroll
+      for (int off = 1; off <= 2; off <<= 1) {     // the quad's four row residues (fixed order)
+        pmn = dmin(pmn, __shfl_xor_sync(FULL, pmn, off));
+        pmx = dmax(pmx, __shfl_xor_sync(FULL, pmx, off));
+        psm += __shfl_xor_sync(FULL, psm, off);
+        prh += __shfl_xor_sync(FULL, prh, off);
+        qmn = dmin(qmn, __shfl_xor_sync(FULL, qmn, off));
+        qmx = dmax(qmx, __shfl_xor_sync(FULL, qmx, off));
+        qsm += __shfl_xor_sync(FULL, qsm, off);
+        qrh += __shfl_xor_sync(FULL, qrh, off);
+      }
+      __syncthreads();                                      // ring consumed; Gbuf free
+      if (kl == 0) {
+        const int a1 = I1 * 8 + rl, a2 = I2 * 8 + rl;
+        zv[a1] = pmn;
+        wv[a1] = pmx;
+        rhs[a1] = psm;
+        invd[a1] = prh;
+        zv[a2] = qmn;
+        wv[a2] = qmx;
+        rhs[a2] = qsm;
+        invd[a2] = qrh;
+      }
+      __syncthreads();
+      if (fh == 0) {
+        const double mn = zv[fa], mx = wv[fa], sm = rhs[fa], rh = invd[fa];
+#else
       // statistics of D3 from the two row halves (fixed order), rhs, shift difference
       if (fh == 1) {
         zv[fa] = pmn;
@@ -493,6 +547,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_fit_big(const BigArgs A) {
       __syncthreads();                                      // ring consumed; Gbuf free
       if (fh == 0) {
         const double mn = fmin(pmn, zv[fa]), mx = fmax(pmx, wv[fa]), sm = psm + rhs[fa], rh = prh + invd[fa];
+#endif
         const bool act = fin && mx > mn;
         const double xbar = fin ? sm / (double)n : 0.0;
         const double sc = act ? 1.0 / (mx - mn) : 0.0;
