@@ -43,6 +43,9 @@ constexpr int kRecR = kSchurQ, kRecZ = kSchurQ + kSchurU, kRecBase = kSchurQ + 2
 #define SPEEDREC_SFIT_THREADS 256
 #endif
 constexpr int kSfitThreads = SPEEDREC_SFIT_THREADS;
+#ifndef SPEEDREC_SFIT_PROBE        // timing probes (1 no factorization, 2 no ranking): wrong results
+#define SPEEDREC_SFIT_PROBE 0
+#endif
 #ifndef SPEEDREC_SFIT_NBUF         // record buffers of the staged fold loop
 #define SPEEDREC_SFIT_NBUF 3
 #endif
@@ -359,13 +362,13 @@ __global__ void __launch_bounds__(kSfitThreads, SPEEDREC_SFIT_MINB(D)) k_mask_sf
     constexpr bool SM = true;
     const long long sl = fidx * S + split - M.first;
     const uint32_t om = scored_mask(M.sd, split, O);
-    const int g = M.sd.pool_list[split >> 6], v = split & 63, p = g / M.IR;
+    const int g = M.sd.pool_list[split >> 6], v = split & 63;
     double ce[kSfitMaxO];
-    bool cv[kSfitMaxO], cc[kSfitMaxO];
+    bool cv[kSfitMaxO], cc[kSfitMaxO], hit[kSfitMaxO];   // hit: AC > 1 (the held-out case's own label)
     int guard = 0, untrained = 0;
 #pragma unroll
     for (int o = 0; o < kSfitMaxO; ++o) {
-      cv[o] = cc[o] = false;
+      cv[o] = cc[o] = hit[o] = false;
       ce[o] = 0.0;
       if (o >= O) continue;
       // one optimisation at a time (no load hoisting across them) for the larger
@@ -391,7 +394,11 @@ __global__ void __launch_bounds__(kSfitThreads, SPEEDREC_SFIT_MINB(D)) k_mask_sf
           // an inactive suffix counter (rg = 0 in this fold) has a zero row and
           // column in Q and zero r~, z~: its pivot is lambda and it adds exact
           // zeros, so the fit equals the one without it (reading D3)
+#if SPEEDREC_SFIT_PROBE == 1   // timing probe only (wrong results): no suffix factorization
+          double e = pm.ybar + rec_ld<SM>(R + kRecBase) + rec_ld<SM>(R + f[0]);
+#else
           double e = pm.ybar + rec_ld<SM>(R + kRecBase) + schur_fit<D, SM>(R, f, ok);
+#endif
           if (!ok) {
             e = pm.ybar;
             guard += 1000000;
@@ -412,6 +419,7 @@ __global__ void __launch_bounds__(kSfitThreads, SPEEDREC_SFIT_MINB(D)) k_mask_sf
           t_corr += corr;
           t_test += 1;
           cv[o] = true;
+          hit[o] = ac > 1.0;
           cc[o] = cl;
           ce[o] = e;
           if (M.ex_out) M.ex_out[(sl * O + o) * (long long)G * 32 + pm.tek] = e;
@@ -419,30 +427,48 @@ __global__ void __launch_bounds__(kSfitThreads, SPEEDREC_SFIT_MINB(D)) k_mask_sf
       }
       if (M.opt_out) M.opt_out[sl * O + o] = row;
     }
-    // A6: rank the held-out version's candidates (R13, R21)
+#if SPEEDREC_SFIT_PROBE == 2   // timing probe only (wrong results): no guard / ranking rules
+    int nrec = cv[0] ? 1 : 0, nhit = cc[1] ? 1 : 0;
+    (void)ce;
+    (void)hit;
+#else
+    // A6: rank the held-out version's candidates (R13, R21), one pass
+    // over the 15 candidate pairs: the guard band of R21 (near_tol with the
+    // first one's scale, as k_rank_warp) and the rank order (EX desc, id asc:
+    // for a < b, b outranks a iff EX_b > EX_a) of those at or above the
+    // threshold.  A recommendation's hit is its own held-out label AC > 1.
+    double ta[kSfitMaxO];
+    unsigned left = 0u;
+    int rk[kSfitMaxO];
 #pragma unroll
     for (int a = 0; a < kSfitMaxO; ++a) {
+      rk[a] = 0;
+      ta[a] = M.guard_tol * (fabs(ce[a]) > 1.0 ? fabs(ce[a]) : 1.0);   // near_tol(ce[a], .)
       if (!cv[a]) continue;
-      if (near_tol(ce[a], M.threshold, M.guard_tol)) ++guard;
+      if (fabs(ce[a] - M.threshold) <= ta[a]) ++guard;
+      if (ce[a] >= M.threshold) left |= 1u << a;
+    }
 #pragma unroll
-      for (int b = a + 1; b < kSfitMaxO; ++b)
-        if (cv[b] && !(cc[a] && cc[b]) && near_tol(ce[a], ce[b], M.guard_tol)) ++guard;
+    for (int a = 0; a < kSfitMaxO; ++a) {
+#pragma unroll
+      for (int b = a + 1; b < kSfitMaxO; ++b) {
+        if (!(cv[a] && cv[b])) continue;
+        if (!(cc[a] && cc[b]) && fabs(ce[a] - ce[b]) <= ta[a]) ++guard;
+        if (((left >> a) & (left >> b) & 1u) != 0u) {
+          if (ce[b] > ce[a]) ++rk[a];
+          else ++rk[b];
+        }
+      }
     }
     int nrec = 0, nhit = 0;
 #pragma unroll
     for (int a = 0; a < kSfitMaxO; ++a) {
-      if (!cv[a] || !(ce[a] >= M.threshold)) continue;
-      int rk = 0;
-#pragma unroll
-      for (int b = 0; b < kSfitMaxO; ++b)
-        if (b != a && cv[b] && ce[b] >= M.threshold && (ce[b] > ce[a] || (ce[b] == ce[a] && b < a))) ++rk;
-      if (rk < M.max_count) {
-        ++nrec;
-        const int bb = M.opt_bit[p * O + a];
-        if (M.ylab[(g * O + a) * 32 + rmv(v, bb)] > 1.0) ++nhit;
-        if (M.rec_out) M.rec_out[(sl * G * 64 + g * 64 + v) * M.max_count + rk] = (int8_t)a;
-      }
+      if (!((left >> a) & 1u) || rk[a] >= M.max_count) continue;
+      ++nrec;
+      if (hit[a]) ++nhit;
+      if (M.rec_out) M.rec_out[(sl * G * 64 + g * 64 + v) * M.max_count + rk[a]] = (int8_t)a;
     }
+#endif
     s_rec += nrec;
     s_hit += nhit;
     t_rec += nrec;
