@@ -1113,10 +1113,18 @@ static __global__ void __launch_bounds__(kBigThreads, 1) k_rank_big4(const BigAr
     const double* src = A.x + (long long)g * 64 * C;
     double* dst = xs + buf * 64 * XLD;
     const int per_row = C / 2;
-    for (int i = t; i < 64 * per_row; i += kBigThreads) {
-      const int r = i / per_row, c2 = (i % per_row) * 2;
-      const unsigned d = (unsigned)__cvta_generic_to_shared(dst + r * XLD + c2);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + r * C + c2) : "memory");
+    if (kBigThreads % per_row == 0) {             // a fixed 16-byte column per thread, no division per copy
+      const int c2 = (t % per_row) * 2, rs = kBigThreads / per_row;
+      for (int r = t / per_row; r < 64; r += rs) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(dst + r * XLD + c2);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + r * C + c2) : "memory");
+      }
+    } else {
+      for (int i = t; i < 64 * per_row; i += kBigThreads) {
+        const int r = i / per_row, c2 = (i % per_row) * 2;
+        const unsigned d = (unsigned)__cvta_generic_to_shared(dst + r * XLD + c2);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + r * C + c2) : "memory");
+      }
     }
     // the group's labels ylab[g][o][k] (the same for every scenario)
     const double* ysrc = A.ylab + (long long)g * O * 32;
@@ -1155,20 +1163,31 @@ static __global__ void __launch_bounds__(kBigThreads, 1) k_rank_big4(const BigAr
     // ---- EX tile: (64 versions) x (C counters) times (C) x (NC columns) ----
     {
       const double* xt = xs + (g & 1) * 64 * XLD;
-      double acc[NC / 8][2];
+      // two accumulator sets over alternating k-steps (independent DMMA
+      // chains), added at the end
+      double acc[NC / 8][2], acc2[NC / 8][2];
 #pragma unroll
-      for (int nt = 0; nt < NC / 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+      for (int nt = 0; nt < NC / 8; ++nt) acc[nt][0] = acc[nt][1] = acc2[nt][0] = acc2[nt][1] = 0.0;
       const double* arow = xt + (warp * 8 + rl) * XLD + kl;
-#pragma unroll 4
-      for (int k0 = 0; k0 < C; k0 += 4) {
+      int k0 = 0;
+#pragma unroll 2
+      for (; k0 + 4 < C; k0 += 8) {
+        const double a = arow[k0], a2 = arow[k0 + 4];
+#pragma unroll
+        for (int nt = 0; nt < NC / 8; ++nt) {
+          dmma(acc[nt][0], acc[nt][1], a, Us[(nt * 8 + rl) * ULD + k0 + kl]);
+          dmma(acc2[nt][0], acc2[nt][1], a2, Us[(nt * 8 + rl) * ULD + k0 + 4 + kl]);
+        }
+      }
+      if (k0 < C) {
         const double a = arow[k0];
 #pragma unroll
         for (int nt = 0; nt < NC / 8; ++nt) dmma(acc[nt][0], acc[nt][1], a, Us[(nt * 8 + rl) * ULD + k0 + kl]);
       }
 #pragma unroll
       for (int nt = 0; nt < NC / 8; ++nt) {
-        exs[(warp * 8 + rl) * (NC + 1) + nt * 8 + 2 * kl] = acc[nt][0];
-        exs[(warp * 8 + rl) * (NC + 1) + nt * 8 + 2 * kl + 1] = acc[nt][1];
+        exs[(warp * 8 + rl) * (NC + 1) + nt * 8 + 2 * kl] = acc[nt][0] + acc2[nt][0];
+        exs[(warp * 8 + rl) * (NC + 1) + nt * 8 + 2 * kl + 1] = acc[nt][1] + acc2[nt][1];
       }
     }
     __syncthreads();
