@@ -615,6 +615,7 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
       }
     };
     if (m5) {    // NEXT-2: grow + prune the tree in the warp's scratch slab, then lanes over tests
+      SR_M5T(-1);
       M5Work W = m5_carve(scr, L.np_tr, A.C);
       W.ld = deff > 0 ? deff : 1;    // rows of the active features only
       for (int e = lane; e < n * deff; e += 32) {
@@ -622,11 +623,14 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
         W.Xs[r * W.ld + a] = (X[(long long)trs[r] * ldx + col[a]] - uv[a]) / wv[a];
       }
       __syncwarp();
+      SR_M5T(4);
       int tg = 0;
       bool tok = true;
       m5_build(W, n, deff, yc, A.lambda, A.refine, A.guard_tol, lane, &tg, &tok, m5t);
       if (lane == 0) guard += tg + (tok ? 0 : 1000000);   // warp-uniform counts: once, not per lane
+      SR_M5T(-1);
       for (int j = lane; j < nt; j += 32) score(j, m5_predict(W, X + (long long)tes[j] * ldx, col, uv, wv));
+      SR_M5T(5);
     } else if (ibk) {   // NEXT-1: IBk prediction, all lanes sweep together (knn_ex)
       const int kk = min(A.k_nn, n);
       #pragma unroll 1
@@ -682,6 +686,13 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
     atomicAdd(&A.totals[0], tot_corr);
     atomicAdd(&A.totals[1], tot_test);
   }
+#if SR_WARP_TIMING && SR_M5_TIMING
+  if (MODE == 3 && blockIdx.x < 4 && lane == 0) {
+    const long long* a = sr_wt_acc[blockIdx.x * A.warps_per_block + warp];
+    printf("SR_M5T cta %d warp %d: search %lld partition %lld models %lld prune %lld rows %lld predict %lld\n",
+           blockIdx.x, warp, a[0], a[1], a[2], a[3], a[4], a[5]);
+  }
+#endif
 #if SR_WARP_TIMING
   if (MODE == 4 && blockIdx.x == 0 && lane == 0) {
     const long long* a = sr_wt_acc[warp];

@@ -274,6 +274,13 @@ __device__ __forceinline__ void sr_wt(int k) {
 #else
 #define SR_WT(k)
 #endif
+// M5P phases (-DSR_M5_TIMING=1, same accumulators): 0 split search, 1
+// partition, 2 node models, 3 pruning residuals, 4 scaled rows, 5 prediction
+#if SR_M5_TIMING && SR_WARP_TIMING
+#define SR_M5T(k) sr_wt(k)
+#else
+#define SR_M5T(k)
+#endif
 
 // min / max of non-NaN doubles: one compare + select (fmin/fmax add NaN handling)
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }

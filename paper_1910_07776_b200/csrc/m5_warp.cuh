@@ -497,6 +497,7 @@ __device__ int m5_build(const M5Work& W, int n, int deff, double* y, double lamb
   const double sd_root = m5_sd(0, n, y);
   const double sd_min = __dmul_rn(kM5SdFrac, sd_root);
   int nn = 1;
+  SR_M5T(-1);
   #pragma unroll 1
   for (int i = 0; i < nn; ++i) {
     const int lo = W.nlo[i], hi = W.nhi[i];
@@ -509,8 +510,10 @@ __device__ int m5_build(const M5Work& W, int n, int deff, double* y, double lamb
         split = (T.tw == 1 ? m5_best_split<true>(W, lo, hi, deff, y, sdT, lane, ba, bt, T)
                            : m5_best_split<false>(W, lo, hi, deff, y, sdT, lane, ba, bt, T)) > 0.0;
     }
+    SR_M5T(0);
     if (split) {
       const int nL = m5_partition(W, lo, hi, ba, bt, y, lane);
+      SR_M5T(1);
       if (lane == 0) {
         W.feat[i] = ba;
         W.thr[i] = bt;
@@ -547,7 +550,9 @@ __device__ int m5_build(const M5Work& W, int n, int deff, double* y, double lamb
     const int lo = W.nlo[i], hi = W.nhi[i], m = hi - lo;
     const unsigned long long al = W.allow[i];
     double* mdl = W.pool + W.moff[i];
+    SR_M5T(-1);
     good &= m5_node_fit(W, lo, hi, al, y, lambda, nref, mdl, lane);
+    SR_M5T(2);
     double rs = 0.0;
     for (int k = lo + lane; k < hi; k += 32) {
       const int r = k;
@@ -574,6 +579,7 @@ __device__ int m5_build(const M5Work& W, int n, int deff, double* y, double lamb
       }
     }
     __syncwarp();
+    SR_M5T(3);
   }
   *guard = __shfl_sync(FULL, g, 0);
   *ok = good;
