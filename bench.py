@@ -282,7 +282,10 @@ def run_other_configs(args):
             r = d["roofline"]
             res[name] = {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
                          "workload": d["config"]["workload"], "scenarios_per_step": d["config"]["splits_per_gpu"],
-                         "scaling": d["scaling"], "roofline": {k: r[k] for k in ("kernel", "achieved", "frac")},
+                         "scaling": d["scaling"],
+                         "roofline": {k: r.get(k) for k in ("bound", "kernel", "achieved", "peak", "unit", "frac",
+                                                            "traffic", "traffic_note", "kernel_share_of_step",
+                                                            "effective", "frac_yardstick_p_eq_S")},
                          "cpu_baseline": d.get("cpu_baseline"), "accuracy": d.get("accuracy"),
                          "guard_cases": d.get("guard_cases"),
                          "top_masks_head": d.get("top_masks_head")}
@@ -503,7 +506,7 @@ def main():
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         ent = tj.get(name_dom)
-        if ent and ent["workload"] == args.config:
+        if ent and ent["workload"] == args.config and ent.get("learner", "linreg") == args.learner:
             per_unit = (ent["read"] + ent["write"]) / ent["units"]
             units = ent["units"] if name_dom == "k_mask_sfit" else count / launches_per_step
             traffic = per_unit * units
