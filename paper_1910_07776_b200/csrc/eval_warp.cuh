@@ -359,8 +359,18 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
   // list are formed once per scenario; fit-major (small, latency-bound
   // batches): one fit per work unit, spreading a scenario over warps
   const long long units = A.scn_major ? A.count : A.count * O;
+  // work units: the first nteams by warp index, then (A.queue) one at a time
+  // from a launch-wide counter, so warps that drew cheap scenarios keep
+  // working instead of waiting out the last warps of a static stride (the
+  // outputs are per unit, the totals integer: the order changes nothing)
+  auto next_unit = [&](long long u) -> long long {
+    if (MODE == 3 || A.queue == nullptr) return u + nteams;
+    unsigned long long v = 0ull;
+    if (lane == 0) v = atomicAdd(A.queue, 1ull);
+    return (long long)__shfl_sync(FULL, v, 0) + nteams;
+  };
   if (MODE == 4) SR_WT(-1);
-  for (long long u = team; u < units; u += nteams) {
+  for (long long u = team; u < units; u = next_unit(u)) {
   const long long sl = A.scn_major ? u : u / O;
   const int o_lo = A.scn_major ? 0 : (int)(u - sl * O), o_hi = A.scn_major ? O : o_lo + 1;
   const long long s = A.first + sl, so = A.out0 + sl;

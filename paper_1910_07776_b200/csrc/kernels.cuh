@@ -103,6 +103,7 @@ struct EvalArgs {
   uint32_t* trained;     // [count] bit o set iff optimization o has >= 1 training pair
   int* guard_acc;        // [count] guard cases counted by the fit kernel
   int* done;             // [count] scored fits finished (fused ranking)
+  unsigned long long* queue;   // k_fit_warp work units handed out past the first nteams (nullptr: static stride)
   int fuse_rank;         // 1: k_fit_warp ranks each scenario after its last fit (no k_rank_warp)
   // outputs (device, indexed by out0 + local scenario)
   OptScore* opt_out;     // [.][O] or null

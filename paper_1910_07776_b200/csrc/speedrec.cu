@@ -51,6 +51,8 @@ struct sr_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t cstream = nullptr;        // copy stream: D2H of finished chunks overlaps later ones
+  cudaStream_t fstream[8] = {};          // side streams of a fork-join launch group (launch_group)
+  cudaEvent_t fevent[9] = {};            // its fork / join events (no timing)
   std::vector<cudaEvent_t> cp_events;
   std::string err;
   int sm_count = 0;
@@ -91,6 +93,7 @@ struct sr_ctx {
   DevBuf extab, trained, guard_acc, mask_acc, done;   // fit -> rank exchange (warp path)
   DevBuf utab;                                        // fit -> k_pred_rank model table (split LS path)
   DevBuf work;                                        // M5P executed split-search operations (sr_last_work)
+  DevBuf qctr;                                        // k_fit_warp dynamic work-unit counter
   // accounting
   bool timing = false;
   std::vector<KStat> kstats;
@@ -177,6 +180,58 @@ sr_status launch(sr_ctx* c, const char* name, F&& f) {
   }
   c->kstats[id].launches++;
   c->last_launches++;
+  return SR_OK;
+}
+
+// A group of independent launches of one kernel family (disjoint outputs)
+// spread over up to 8 side streams forked from and joined back into the
+// context stream, so one launch's tail wave overlaps the next launch's first
+// (DESIGN.md §5.8).  f(i, stream) issues launch i.  Timing (when on): one
+// event pair on the context stream around the whole group, charged to `name`
+// with n launches, so the family's summed time is the group's wall time.
+// SPEEDREC_GROUP_STREAMS=1 keeps the launches on the context stream.
+template <typename F>
+sr_status launch_group(sr_ctx* c, const char* name, int n, F&& f) {
+  if (n <= 0) return SR_OK;
+  static const int env_k = [] {
+    const char* e = getenv("SPEEDREC_GROUP_STREAMS");
+    return e ? atoi(e) : 8;
+  }();
+  const int k = std::max(1, std::min(std::min(env_k, 8), n));
+  const int id = kstat_id(c, name);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {
+    e0 = take_event(c);
+    e1 = take_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  if (k == 1) {
+    for (int i = 0; i < n; ++i) {
+      const cudaError_t ce = f(i, c->stream);
+      if (ce != cudaSuccess) return fail(c, SR_E_CUDA, "launch of %s: %s", name, cudaGetErrorString(ce));
+    }
+  } else {
+    for (int q = 0; q < k; ++q)
+      if (!c->fstream[q]) CU(cudaStreamCreateWithFlags(&c->fstream[q], cudaStreamNonBlocking));
+    for (int q = 0; q <= k; ++q)
+      if (!c->fevent[q]) CU(cudaEventCreateWithFlags(&c->fevent[q], cudaEventDisableTiming));
+    CU(cudaEventRecord(c->fevent[k], c->stream));                     // fork
+    for (int q = 0; q < k; ++q) CU(cudaStreamWaitEvent(c->fstream[q], c->fevent[k], 0));
+    for (int i = 0; i < n; ++i) {
+      const cudaError_t ce = f(i, c->fstream[i % k]);
+      if (ce != cudaSuccess) return fail(c, SR_E_CUDA, "launch of %s: %s", name, cudaGetErrorString(ce));
+    }
+    for (int q = 0; q < k; ++q) {                                      // join
+      CU(cudaEventRecord(c->fevent[q], c->fstream[q]));
+      CU(cudaStreamWaitEvent(c->stream, c->fevent[q], 0));
+    }
+  }
+  if (c->timing) {
+    cudaEventRecord(e1, c->stream);
+    c->pending.push_back({id, {e0, e1}});
+  }
+  c->kstats[id].launches += n;
+  c->last_launches += n;
   return SR_OK;
 }
 
@@ -269,7 +324,7 @@ void sr_destroy(sr_ctx* c) {
                     &c->big_flag, &c->extab, &c->trained, &c->guard_acc, &c->mask_acc, &c->done, &c->fit_coef,
                     &c->mp_G, &c->mp_r, &c->mp_z, &c->mp_meta, &c->mp_perm, &c->mp_rec, &c->mp_order,
                     &c->mp_units, &c->mp_pfx, &c->mp_glist, &c->sw_buf, &c->ibk_lists, &c->ibk_xs, &c->ibk_meta,
-                    &c->utab, &c->work})
+                    &c->utab, &c->work, &c->qctr})
     release(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->cp_events) cudaEventDestroy(e);
@@ -277,6 +332,13 @@ void sr_destroy(sr_ctx* c) {
     cudaStreamSynchronize(c->cstream);
     cudaStreamDestroy(c->cstream);
   }
+  for (cudaStream_t fs : c->fstream)
+    if (fs) {
+      cudaStreamSynchronize(fs);
+      cudaStreamDestroy(fs);
+    }
+  for (cudaEvent_t e : c->fevent)
+    if (e) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -587,33 +649,34 @@ sr_status run_schur_path(sr_ctx* c, const MaskArgs& M, long long S, int T, int U
   SA.group = (const int32_t*)c->mp_units.p;
   if (T <= kSchurU && (int)c->splan_goff.size() == kSchurU + 2 &&
       c->splan_goff[kSchurU + 1] == c->splan_groups) {   // register records per prefix size
-    for (int pp = 0; pp <= kSchurU; ++pp) {
-      const int g0 = c->splan_goff[pp], ng = c->splan_goff[pp + 1] - g0;
-      if (ng == 0) continue;
-      const long long nth = (long long)ng * S * O;
-      cudaError_t ce = cudaSuccess;
-      const sr_status s2 = launch(c, "k_mask_sprep", [&] {
-        ce = mask_sprep_launch(pp, (unsigned)((nth + 127) / 128), c->stream, SA, (const int32_t*)c->mp_glist.p + g0, ng);
-      });
-      if (ce != cudaSuccess) return fail(c, SR_E_CUDA, "k_mask_sprep_p<%d>: %s", pp, cudaGetErrorString(ce));
-      if (s2) return s2;
-    }
+    std::vector<int> pps;                    // prefix sizes present (independent record groups)
+    for (int pp = 0; pp <= kSchurU; ++pp)
+      if (c->splan_goff[pp + 1] > c->splan_goff[pp]) pps.push_back(pp);
+    if ((st = launch_group(c, "k_mask_sprep", (int)pps.size(), [&](int i, cudaStream_t stg) {
+          const int pp = pps[i], g0 = c->splan_goff[pp], ng = c->splan_goff[pp + 1] - g0;
+          const long long nth = (long long)ng * S * O;
+          return mask_sprep_launch(pp, (unsigned)((nth + 127) / 128), stg, SA, (const int32_t*)c->mp_glist.p + g0, ng);
+        })))
+      return st;
   } else if ((st = launch(c, "k_mask_sprep",
                           [&] { k_mask_sprep<<<(unsigned)((nrec + 127) / 128), 128, 0, c->stream>>>(SA); }))) {
     return st;
   }
-  for (int d = 0; d <= kSchurU; ++d) {
-    const int off = c->splan_doff[d], n_it = c->splan_doff[d + 1] - off;
-    if (n_it == 0) continue;
+  // suffix sizes present, the largest launches first (the smaller ones fill
+  // the tail waves of the large ones on the other side streams)
+  std::vector<int> ds;
+  for (int d = 0; d <= kSchurU; ++d)
+    if (c->splan_doff[d + 1] > c->splan_doff[d]) ds.push_back(d);
+  std::stable_sort(ds.begin(), ds.end(), [&](int a, int b) {
+    return c->splan_doff[a + 1] - c->splan_doff[a] > c->splan_doff[b + 1] - c->splan_doff[b];
+  });
+  return launch_group(c, "k_mask_sfit", (int)ds.size(), [&](int i, cudaStream_t stg) {
+    const int d = ds[i], off = c->splan_doff[d], n_it = c->splan_doff[d + 1] - off;
     const long long want = (long long)c->sm_count * 1024;
     const int fc = (int)std::max(1LL, std::min<long long>(S, want / n_it));
     const unsigned grid = (unsigned)(((long long)n_it * fc + kSfitThreads - 1) / kSfitThreads);
-    cudaError_t ce = cudaSuccess;
-    const sr_status s2 = launch(c, "k_mask_sfit", [&] { ce = mask_sfit_launch(d, grid, c->stream, SA, off, n_it, fc); });
-    if (ce != cudaSuccess) return fail(c, SR_E_CUDA, "k_mask_sfit<%d>: %s", d, cudaGetErrorString(ce));
-    if (s2) return s2;
-  }
-  return SR_OK;
+    return mask_sfit_launch(d, grid, stg, SA, off, n_it, fc);
+  });
 }
 
 // Feature-mask path: LOO batches of whole feature masks
@@ -1287,6 +1350,17 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
       if (wpb % A.m5_team) A.m5_team = 1;
     }
     const long long fblocks = std::max(1LL, std::min(max_fit_blocks, (units * A.m5_team + wpb - 1) / wpb));
+    // dynamic work units (not M5P teams; SPEEDREC_DYN_UNITS=0: static stride)
+    static const bool dyn_units = [] {
+      const char* e = getenv("SPEEDREC_DYN_UNITS");
+      return e ? atoi(e) != 0 : true;
+    }();
+    A.queue = nullptr;
+    if (dyn_units && prm->learner != SR_M5P && units > fblocks * wpb) {
+      if ((st = ensure(c, c->qctr, 8))) return st;
+      CU(cudaMemsetAsync(c->qctr.p, 0, 8, c->stream));
+      A.queue = (unsigned long long*)c->qctr.p;
+    }
     if ((st = launch(c, "k_fit_warp", [&] { kfit<<<(unsigned)fblocks, wpb * 32, smem, c->stream>>>(A); }))) return st;
     if (split_ls) {
       const int ks = (C + 3) / 4;
