@@ -841,9 +841,14 @@ sr_status evaluate_big_ibk(sr_ctx* c, const sr_params* prm, long long first, lon
   I.tek = (int32_t*)(lp + (size_t)fits * np * 16);
   I.xs = (double*)c->ibk_xs.p;
   I.meta = (IbkMeta*)c->ibk_meta.p;
-  // test-tile chunks per fit: ~8 waves of one CTA per SM (small tail), at most one tile each
+  // test-tile chunks per fit: one test tile per CTA, so the block scheduler
+  // balances the ~25k tiles of a batch over the SMs (CTAs past a fit's tiles
+  // exit at once); ~8 waves of multi-tile CTAs left a 0.4-wave tail and
+  // 19/20-tile imbalance: 361 -> 339 ms per C4-IBK step, profiles/r5d_ab_ibk_chunks.txt
   const long long tiles_max = (np / 2 + kIbkTT - 1) / kIbkTT;
-  I.chunks = (int)std::max(1LL, std::min<long long>(tiles_max, (8LL * c->sm_count + fits - 1) / fits));
+  I.chunks = (int)std::max(1LL, tiles_max);
+  if (const char* e = getenv("SPEEDREC_IBK_CHUNKS"))   // A/B knob: test-tile chunks per fit
+    I.chunks = (int)std::max(1LL, std::min<long long>(tiles_max, atoll(e)));
   EvalArgs& E = I.E;
   E.x = B.x;
   E.ylab = B.ylab;
