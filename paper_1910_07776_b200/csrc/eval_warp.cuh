@@ -363,8 +363,19 @@ __global__ void __launch_bounds__(WMAX * 32, MODE == 3 ? SR_M5_MINB : 1) k_fit_w
   // from a launch-wide counter, so warps that drew cheap scenarios keep
   // working instead of waiting out the last warps of a static stride (the
   // outputs are per unit, the totals integer: the order changes nothing)
+  // (M5P teams: the lead warp draws, its team reads the unit from a shared slot)
+  __shared__ long long m5q[kMaxWarpsPerBlock];
   auto next_unit = [&](long long u) -> long long {
-    if (MODE == 3 || A.queue == nullptr) return u + nteams;
+    if (A.queue == nullptr) return u + nteams;
+    if (MODE == 3) {
+      if (lead && lane == 0) m5q[warp - trank] = (long long)atomicAdd(A.queue, 1ull) + nteams;
+      if (tw > 1) m5_team_sync(m5t);
+      else __syncwarp();
+      const long long nu = m5q[warp - trank];
+      if (tw > 1) m5_team_sync(m5t);   // every member has read the slot before the next draw
+      else __syncwarp();
+      return nu;
+    }
     unsigned long long v = 0ull;
     if (lane == 0) v = atomicAdd(A.queue, 1ull);
     return (long long)__shfl_sync(FULL, v, 0) + nteams;

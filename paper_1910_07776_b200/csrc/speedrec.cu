@@ -1355,13 +1355,13 @@ sr_status sr_evaluate(sr_ctx* c, const sr_params* prm, int64_t first, int64_t co
       if (wpb % A.m5_team) A.m5_team = 1;
     }
     const long long fblocks = std::max(1LL, std::min(max_fit_blocks, (units * A.m5_team + wpb - 1) / wpb));
-    // dynamic work units (not M5P teams; SPEEDREC_DYN_UNITS=0: static stride)
+    // dynamic work units (SPEEDREC_DYN_UNITS=0: static stride)
     static const bool dyn_units = [] {
       const char* e = getenv("SPEEDREC_DYN_UNITS");
       return e ? atoi(e) != 0 : true;
     }();
     A.queue = nullptr;
-    if (dyn_units && prm->learner != SR_M5P && units > fblocks * wpb) {
+    if (dyn_units && units * A.m5_team > fblocks * wpb) {
       if ((st = ensure(c, c->qctr, 8))) return st;
       CU(cudaMemsetAsync(c->qctr.p, 0, 8, c->stream));
       A.queue = (unsigned long long*)c->qctr.p;
