@@ -217,14 +217,13 @@ sr_status launch_group(sr_ctx* c, const char* name, int n, F&& f) {
       if (!c->fevent[q]) CU(cudaEventCreateWithFlags(&c->fevent[q], cudaEventDisableTiming));
     CU(cudaEventRecord(c->fevent[k], c->stream));                     // fork
     for (int q = 0; q < k; ++q) CU(cudaStreamWaitEvent(c->fstream[q], c->fevent[k], 0));
-    for (int i = 0; i < n; ++i) {
-      const cudaError_t ce = f(i, c->fstream[i % k]);
-      if (ce != cudaSuccess) return fail(c, SR_E_CUDA, "launch of %s: %s", name, cudaGetErrorString(ce));
-    }
-    for (int q = 0; q < k; ++q) {                                      // join
+    cudaError_t first_err = cudaSuccess;
+    for (int i = 0; i < n && first_err == cudaSuccess; ++i) first_err = f(i, c->fstream[i % k]);
+    for (int q = 0; q < k; ++q) {                                      // join (also after a failed launch)
       CU(cudaEventRecord(c->fevent[q], c->fstream[q]));
       CU(cudaStreamWaitEvent(c->stream, c->fevent[q], 0));
     }
+    if (first_err != cudaSuccess) return fail(c, SR_E_CUDA, "launch of %s: %s", name, cudaGetErrorString(first_err));
   }
   if (c->timing) {
     cudaEventRecord(e1, c->stream);
