@@ -425,19 +425,31 @@ __device__ bool m5_node_fit(const M5Work& W, int lo, int hi, unsigned long long 
   }
   __syncwarp();
   const int ne = p * (p + 1) / 2;
-  for (int e = lane; e < ne; e += 32) {
-    int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+  auto tri = [](int e, int& i, int& j) {     // packed lower-triangle index -> (i, j)
+    i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
     while ((i + 1) * (i + 2) / 2 <= e) ++i;
     while (i * (i + 1) / 2 > e) --i;
-    const int j = e - i * (i + 1) / 2;
-    const int ai = W.fl[i], aj = W.fl[j];
-    const double xi = W.xbar[i], xj = W.xbar[j];
-    double s = 0.0;
+    j = e - i * (i + 1) / 2;
+  };
+  // two entries per lane pass (e, e + 32): two independent FMA chains over the
+  // rows, each entry's own chain in row order as before (same rounding)
+  for (int e0 = lane; e0 < ne; e0 += 64) {
+    const int e1 = e0 + 32;
+    const bool two = e1 < ne;
+    int i0, j0, i1, j1;
+    tri(e0, i0, j0);
+    if (two) tri(e1, i1, j1);
+    else i1 = i0, j1 = j0;
+    const int a0 = W.fl[i0], b0 = W.fl[j0], a1 = W.fl[two ? i1 : i0], b1 = W.fl[two ? j1 : j0];
+    const double x0 = W.xbar[i0], y0 = W.xbar[j0], x1 = W.xbar[two ? i1 : i0], y1 = W.xbar[two ? j1 : j0];
+    double s0 = 0.0, s1 = 0.0;
     for (int k = lo; k < hi; ++k) {
       const double* xr = W.Xs + k * W.ld;
-      s = fma(xr[ai] - xi, xr[aj] - xj, s);
+      s0 = fma(xr[a0] - x0, xr[b0] - y0, s0);
+      s1 = fma(xr[a1] - x1, xr[b1] - y1, s1);
     }
-    W.M[e] = s + (i == j ? lambda : 0.0);
+    W.M[e0] = s0 + (i0 == j0 ? lambda : 0.0);
+    if (two) W.M[e1] = s1 + (i1 == j1 ? lambda : 0.0);
   }
   for (int j = lane; j < p; j += 32) {
     const int a = W.fl[j];
